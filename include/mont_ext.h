@@ -1,0 +1,85 @@
+/*
+ * mont_ext.h -- extended entry points of libmont.so: explicit launch
+ * configuration for the hot kernels (used by bench.py and the tuning sweeps),
+ * the counter-based synthetic input generator (device side of synth/), and
+ * the two measurement microbenchmarks that provide the roofline denominators
+ * (SURVEY.md §2.3 K7, K8).  Same conventions as mont.h (device pointers,
+ * asynchronous on `stream`, status codes, no global state).
+ */
+#ifndef MONT_EXT_H_
+#define MONT_EXT_H_
+
+#include "mont.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Launch configuration.  Zero fields select the library default.
+ *   threads   : threads per CTA (multiple of 32, <= 1024)
+ *   ctas_per_sm: CTAs per SM for the persistent grid (grid = SMs * ctas_per_sm)
+ *   unroll    : 128-bit chunks per thread per loop trip (1, 2, 4 or 8)
+ *   variant   : kernel variant (kernel-specific; 0 = default).
+ *                 mont_mul_vec_ex : 0 = LDG.128 grid-stride, 1 = flat grid
+ *                                   (one trip per thread, no loop)
+ *                 mont_pow_vec_ex : 0 = 2-bit fixed window, 1 = binary
+ *                                   ladder with selects, 2 = 3-bit window
+ *                 mont_mul_twiddle_ex : 0 = bulk-copy (TMA) staged table,
+ *                                   1 = table read through L1/L2 (no smem)
+ *   chunk     : mont_mul_twiddle_ex only: table columns staged per CTA
+ *               (multiple of 4; 0 = min(len, 16384)).                       */
+typedef struct mont_launch {
+    int threads;
+    int ctas_per_sm;
+    int unroll;
+    int variant;
+    int chunk;
+} mont_launch_t;
+
+mont_status_t mont_mul_vec_ex(const mont_ctx_t *ctx, uint32_t *c, const uint32_t *a, const uint32_t *b,
+                              size_t n, const mont_launch_t *cfg, cudaStream_t stream);
+mont_status_t mont_mul_twiddle_ex(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *x,
+                                  const uint32_t *tw, size_t batch, size_t len,
+                                  const mont_launch_t *cfg, cudaStream_t stream);
+mont_status_t mont_pow_vec_ex(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *base,
+                              const uint32_t *exp, size_t n, const mont_launch_t *cfg,
+                              cudaStream_t stream);
+
+/* Device side of the seeded generator of synth/ (SURVEY.md Appendix B):
+ *   h(seed, stream, i) = splitmix64_mix(seed + (stream * 2^40 + i + 1) * GAMMA)
+ * for i = start .. start + n - 1, mapped by `mode`:
+ *   0 : floor(h * p / 2^64)              uniform in [0, p)
+ *   1 : 1 + floor(h * (p - 1) / 2^64)    uniform in [1, p)
+ *   2 : h >> 33                          31-bit exponent (p ignored)
+ * If `specials` is nonzero, index i is then overwritten with 0, 1 or p-1 when
+ * h(seed, stream + 16, i) mod 300 is 0, 1 or 2 (BASELINE configs[1] "1 % of
+ * entries set to 0, 1 or P-1"; reading G13).  No modular
+ * arithmetic of the method happens here. */
+mont_status_t synth_fill(uint32_t *out, size_t n, uint64_t seed, uint32_t stream, uint64_t start,
+                         uint32_t p, int mode, int specials, cudaStream_t stream_);
+
+/* Microbenchmarks (roofline denominators, not part of the method).
+ * mb_triad: c[i] = a[i] ^ b[i] over n uint32 with the same launch shape as
+ *   mont_mul_vec: 12 bytes per element, the achievable 2-read/1-write HBM rate.
+ * mb_copy: out[i] = in[i], 8 bytes per element.
+ * mb_imad: every thread runs `iters` trips of 8 independent dependency chains
+ *   of one integer-multiply instruction kind (0 = IMAD mul.lo, 1 = IMAD.HI
+ *   mul.hi, 2 = IMAD.WIDE mul.wide, 3 = one signed Montgomery product:
+ *   mul.lo, mul.hi, mul.lo, mul.hi, sub), writing one word per thread to
+ *   sink[]; the caller times it and divides the executed count by time.
+ *   grid = SMs * ctas_per_sm (cfg may be NULL). */
+mont_status_t mb_triad(uint32_t *c, const uint32_t *a, const uint32_t *b, size_t n,
+                       const mont_launch_t *cfg, cudaStream_t stream);
+mont_status_t mb_copy(uint32_t *out, const uint32_t *in, size_t n, const mont_launch_t *cfg,
+                      cudaStream_t stream);
+mont_status_t mb_imad(uint32_t *sink, int kind, int iters, const mont_launch_t *cfg, cudaStream_t stream,
+                      unsigned long long *threads_launched);
+
+/* Number of SMs of the current device (cached per device), or -1. */
+int mont_sm_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MONT_EXT_H_ */

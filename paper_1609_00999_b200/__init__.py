@@ -1,0 +1,256 @@
+"""Batched 32-bit Montgomery modular multiplication on B200 (sm_100a).
+
+Thin Python binding over the C ABI of ``libmont.so`` (include/mont.h,
+include/mont_ext.h).  Argument marshalling only: every step of the path runs
+in the library's CUDA kernels; torch supplies device memory, streams and the
+process group.  There is no CPU fallback -- importing this package on a box
+whose library is missing raises, and every launcher raises on a non-OK
+status.
+
+Paper: arxiv 1609.00999, "Automatic Generation of Vectorized Montgomery
+Algorithm".  REDC(a, b) = a*b*R^-1 mod P, R = 2^32 (Alg. 2,
+PAPER.md:95-99).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "libmont.so"
+
+__all__ = [
+    "Ctx", "MontError", "ctx_init", "to_mont", "from_mont", "mul_vec", "mul_twiddle", "pow_vec",
+    "checksum", "twiddle_table", "synth_fill", "Launch", "lib", "LIB_PATH",
+]
+
+
+class MontError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        super().__init__(f"{where}: {_strerror(status)} (status {status})")
+
+
+class Ctx(C.Structure):
+    """mont_ctx_t: {p, pneg = -p^-1 mod 2^32, r1 = 2^32 mod p, r2 = 2^64 mod p}."""
+    _fields_ = [("p", C.c_uint32), ("pneg", C.c_uint32), ("r1", C.c_uint32), ("r2", C.c_uint32)]
+
+    def __repr__(self):
+        return f"Ctx(p={self.p}, pneg={self.pneg}, r1={self.r1}, r2={self.r2})"
+
+
+class Launch(C.Structure):
+    """mont_launch_t (include/mont_ext.h); zero fields = library default."""
+    _fields_ = [("threads", C.c_int), ("ctas_per_sm", C.c_int), ("unroll", C.c_int),
+                ("variant", C.c_int), ("chunk", C.c_int)]
+
+
+_lib = None
+_P = C.c_void_p
+_S = C.c_size_t
+_CTX = C.POINTER(Ctx)
+_LAUNCH = C.POINTER(Launch)
+
+# name -> (restype, argtypes); mirrors include/mont.h and include/mont_ext.h
+SIGNATURES = {
+    "mont_ctx_init": (C.c_int, [_CTX, C.c_uint32]),
+    "to_mont": (C.c_int, [_CTX, _P, _P, _S, _P]),
+    "from_mont": (C.c_int, [_CTX, _P, _P, _S, _P]),
+    "mont_mul_vec": (C.c_int, [_CTX, _P, _P, _P, _S, _P]),
+    "mont_mul_twiddle": (C.c_int, [_CTX, _P, _P, _P, _S, _S, _P]),
+    "mont_pow_vec": (C.c_int, [_CTX, _P, _P, _P, _S, _P]),
+    "mont_checksum": (C.c_int, [_CTX, _P, _P, _S, _P]),
+    "mont_twiddle_table": (C.c_int, [_CTX, _P, C.c_uint32, _S, _P]),
+    "mont_strerror": (C.c_char_p, [C.c_int]),
+    "mont_build_arch": (C.c_int, []),
+    "mont_mul_vec_ex": (C.c_int, [_CTX, _P, _P, _P, _S, _LAUNCH, _P]),
+    "mont_mul_twiddle_ex": (C.c_int, [_CTX, _P, _P, _P, _S, _S, _LAUNCH, _P]),
+    "mont_pow_vec_ex": (C.c_int, [_CTX, _P, _P, _P, _S, _LAUNCH, _P]),
+    "synth_fill": (C.c_int, [_P, _S, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint32, C.c_int, C.c_int, _P]),
+    "mb_triad": (C.c_int, [_P, _P, _P, _S, _LAUNCH, _P]),
+    "mb_copy": (C.c_int, [_P, _P, _S, _LAUNCH, _P]),
+    "mb_imad": (C.c_int, [_P, C.c_int, C.c_int, _LAUNCH, _P, C.POINTER(C.c_ulonglong)]),
+    "mont_sm_count": (C.c_int, []),
+}
+
+
+def lib():
+    """Load libmont.so (built in-tree by __graft_entry__.build() / make)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                              f"g.build()'` (no CPU fallback exists)")
+        L = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _strerror(status: int) -> str:
+    try:
+        return lib().mont_strerror(status).decode()
+    except Exception:  # pragma: no cover
+        return "unknown"
+
+
+def _check(status: int, where: str) -> None:
+    if status != 0:
+        raise MontError(status, where)
+
+
+def ctx_init(p: int) -> Ctx:
+    """Host-only Montgomery context (mont_ctx_init)."""
+    c = Ctx()
+    _check(lib().mont_ctx_init(C.byref(c), p), "mont_ctx_init")
+    return c
+
+
+# ------------------------------------------------------------ tensor helpers
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_handle(stream) -> int:
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _dev_u32(t, name):
+    torch = _torch()
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (the library takes device pointers only)")
+    if t.dtype not in (torch.uint32, torch.int32):
+        raise TypeError(f"{name} must be uint32 (or int32 bit pattern), got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def _out_like(out, ref, name="out"):
+    torch = _torch()
+    if out is None:
+        return torch.empty_like(ref, dtype=torch.uint32)
+    _dev_u32(out, name)
+    if out.numel() != ref.numel():
+        raise ValueError(f"{name} has {out.numel()} elements, expected {ref.numel()}")
+    return out
+
+
+def _ptr(t) -> int:
+    return t.data_ptr()
+
+
+def _cfg(cfg):
+    return C.byref(cfg) if cfg is not None else None
+
+
+def mul_vec(ctx: Ctx, a, b, out=None, stream=None, cfg: Launch | None = None):
+    """c[i] = a[i] b[i] R^-1 mod P (mont_mul_vec)."""
+    _dev_u32(a, "a"), _dev_u32(b, "b")
+    if a.numel() != b.numel():
+        raise ValueError("a and b differ in length")
+    out = _out_like(out, a)
+    s = _stream_handle(stream)
+    if cfg is None:
+        _check(lib().mont_mul_vec(C.byref(ctx), _ptr(out), _ptr(a), _ptr(b), a.numel(), s), "mont_mul_vec")
+    else:
+        _check(lib().mont_mul_vec_ex(C.byref(ctx), _ptr(out), _ptr(a), _ptr(b), a.numel(), C.byref(cfg), s),
+               "mont_mul_vec_ex")
+    return out
+
+
+def to_mont(ctx: Ctx, x, out=None, stream=None):
+    _dev_u32(x, "x")
+    out = _out_like(out, x)
+    _check(lib().to_mont(C.byref(ctx), _ptr(out), _ptr(x), x.numel(), _stream_handle(stream)), "to_mont")
+    return out
+
+
+def from_mont(ctx: Ctx, x, out=None, stream=None):
+    _dev_u32(x, "x")
+    out = _out_like(out, x)
+    _check(lib().from_mont(C.byref(ctx), _ptr(out), _ptr(x), x.numel(), _stream_handle(stream)), "from_mont")
+    return out
+
+
+def mul_twiddle(ctx: Ctx, x, tw, out=None, stream=None, cfg: Launch | None = None):
+    """out[r][j] = x[r][j] tw[j] R^-1 mod P for x of shape (batch, len)."""
+    _dev_u32(x, "x"), _dev_u32(tw, "tw")
+    if x.dim() != 2 or tw.dim() != 1 or x.shape[1] != tw.shape[0]:
+        raise ValueError("x must be (batch, len) and tw (len,)")
+    out = _out_like(out, x)
+    batch, length = x.shape
+    s = _stream_handle(stream)
+    if cfg is None:
+        _check(lib().mont_mul_twiddle(C.byref(ctx), _ptr(out), _ptr(x), _ptr(tw), batch, length, s),
+               "mont_mul_twiddle")
+    else:
+        _check(lib().mont_mul_twiddle_ex(C.byref(ctx), _ptr(out), _ptr(x), _ptr(tw), batch, length,
+                                         C.byref(cfg), s), "mont_mul_twiddle_ex")
+    return out
+
+
+def pow_vec(ctx: Ctx, base, exp, out=None, stream=None, cfg: Launch | None = None):
+    """out[i] = base[i]^exp[i] mod P, plain in/out (mont_pow_vec)."""
+    _dev_u32(base, "base"), _dev_u32(exp, "exp")
+    if base.numel() != exp.numel():
+        raise ValueError("base and exp differ in length")
+    out = _out_like(out, base)
+    s = _stream_handle(stream)
+    if cfg is None:
+        _check(lib().mont_pow_vec(C.byref(ctx), _ptr(out), _ptr(base), _ptr(exp), base.numel(), s),
+               "mont_pow_vec")
+    else:
+        _check(lib().mont_pow_vec_ex(C.byref(ctx), _ptr(out), _ptr(base), _ptr(exp), base.numel(),
+                                     C.byref(cfg), s), "mont_pow_vec_ex")
+    return out
+
+
+def checksum(ctx: Ctx, x, acc=None, stream=None):
+    """Adds sum(x) into the int64 device scalar `acc` (created zeroed if None); returns acc."""
+    torch = _torch()
+    _dev_u32(x, "x")
+    if acc is None:
+        acc = torch.zeros(1, dtype=torch.int64, device=x.device)
+    _check(lib().mont_checksum(C.byref(ctx), _ptr(acc), _ptr(x), x.numel(), _stream_handle(stream)),
+           "mont_checksum")
+    return acc
+
+
+def twiddle_table(ctx: Ctx, w: int, length: int, device="cuda", out=None, stream=None):
+    """tw[j] = to_mont(w^j mod P) on the GPU (mont_twiddle_table)."""
+    torch = _torch()
+    if out is None:
+        out = torch.empty(length, dtype=torch.uint32, device=device)
+    _dev_u32(out, "out")
+    _check(lib().mont_twiddle_table(C.byref(ctx), _ptr(out), w, length, _stream_handle(stream)),
+           "mont_twiddle_table")
+    return out
+
+
+def synth_fill(out, seed: int, stream_id: int, start: int, p: int, mode: int = 0, specials: bool = False,
+               stream=None):
+    """Device side of synth/: counter-based inputs straight into HBM (include/mont_ext.h)."""
+    _dev_u32(out, "out")
+    _check(lib().synth_fill(_ptr(out), out.numel(), seed, stream_id, start, p, mode, int(bool(specials)),
+                            _stream_handle(stream)), "synth_fill")
+    return out
+
+
+def sm_count() -> int:
+    return int(lib().mont_sm_count())
+
+
+if os.environ.get("MONT_EAGER_LOAD", "1") == "1":
+    lib()

@@ -1,0 +1,341 @@
+// k_elementwise.cu -- the HBM-bound streaming kernels of the path:
+//   K1 mont_mul_vec  c[i] = REDC(a[i], b[i])         12 B/elem
+//   K4 to_mont       out[i] = REDC(in[i], R^2 mod P)  8 B/elem  (A2)
+//   K5 from_mont     out[i] = REDC(in[i], 1)          8 B/elem  (A10)
+//   K6 mont_checksum *acc += sum x[i]                 4 B/elem  (A11)
+// plus the triad/copy microbenchmarks that share K1's launch shape.
+//
+// B200 design: the paper vectorises REDC across the 4 lanes of
+// a 128-bit SSE register (§3.2, :125).  Here each thread owns whole
+// 128-bit chunks (4 residues = one uint4), loaded with LDG.E.128 on the
+// non-coherent path and stored evict-first; a CTA moves a contiguous tile of
+// U * threads chunks per trip and tiles are dealt round-robin to a persistent
+// grid of SMs * k CTAs.  All U loads of a trip are issued before any
+// arithmetic (memory-level parallelism), the REDC math is ~7 integer
+// instructions per residue and hides under the HBM stream.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "abi_util.h"
+
+namespace mont {
+
+struct OpMul {
+    uint32_t p, pneg;
+    __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return redc(a, b, p, pneg); }
+};
+struct OpTo {
+    uint32_t p, pneg, r2;
+    __device__ __forceinline__ uint32_t operator()(uint32_t x) const { return redc(x, r2, p, pneg); }
+};
+struct OpFrom {
+    uint32_t p, pneg;
+    __device__ __forceinline__ uint32_t operator()(uint32_t x) const { return redc1(x, p, pneg); }
+};
+struct OpXor {  // triad microbenchmark: no modular math
+    __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a ^ b; }
+};
+struct OpCopy {
+    __device__ __forceinline__ uint32_t operator()(uint32_t x) const { return x; }
+};
+
+template <class Op>
+__device__ __forceinline__ uint4 apply4(const Op &op, const uint4 &a, const uint4 &b) {
+    return make_uint4(op(a.x, b.x), op(a.y, b.y), op(a.z, b.z), op(a.w, b.w));
+}
+template <class Op>
+__device__ __forceinline__ uint4 apply4(const Op &op, const uint4 &a) {
+    return make_uint4(op(a.x), op(a.y), op(a.z), op(a.w));
+}
+
+// ---------------------------------------------------------------- binary map
+// Vector body over n4 chunks of a4/b4/c4 (16-byte aligned), plus `head`
+// scalar elements before it and `tail` after it, handled by CTA 0.
+template <int U, class Op>
+__global__ void __launch_bounds__(512) k_map2(Op op, uint32_t *c, const uint32_t *a, const uint32_t *b,
+                                                uint32_t head, size_t n4, uint32_t tail) {
+    if (blockIdx.x == 0 && threadIdx.x < head + tail) {
+        size_t i = threadIdx.x < head ? threadIdx.x : head + 4 * n4 + (threadIdx.x - head);
+        c[i] = op(a[i], b[i]);
+    }
+    const uint4 *a4 = reinterpret_cast<const uint4 *>(a + head);
+    const uint4 *b4 = reinterpret_cast<const uint4 *>(b + head);
+    uint4 *c4 = reinterpret_cast<uint4 *>(c + head);
+    const size_t tile = (size_t)U * blockDim.x;
+    const size_t ntiles_full = n4 / tile;
+    size_t t = blockIdx.x;
+    for (; t < ntiles_full; t += gridDim.x) {
+        const size_t base = t * tile + threadIdx.x;
+        uint4 va[U], vb[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) va[k] = ld_stream(a4 + base + (size_t)k * blockDim.x);
+#pragma unroll
+        for (int k = 0; k < U; ++k) vb[k] = ld_stream(b4 + base + (size_t)k * blockDim.x);
+#pragma unroll
+        for (int k = 0; k < U; ++k) st_stream(c4 + base + (size_t)k * blockDim.x, apply4(op, va[k], vb[k]));
+    }
+    if (t == ntiles_full) {  // the one partial tile, owned by exactly one CTA
+        for (size_t i = t * tile + threadIdx.x; i < n4; i += blockDim.x)
+            st_stream(c4 + i, apply4(op, ld_stream(a4 + i), ld_stream(b4 + i)));
+    }
+}
+
+// 32-bit path for operands that do not share an address mod 16
+template <int U, class Op>
+__global__ void __launch_bounds__(512) k_map2_scalar(Op op, uint32_t *c, const uint32_t *a, const uint32_t *b,
+                                                       size_t n) {
+    const size_t tile = (size_t)U * blockDim.x;
+    for (size_t t0 = (size_t)blockIdx.x * tile; t0 < n; t0 += (size_t)gridDim.x * tile) {
+        uint32_t va[U], vb[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            size_t i = t0 + (size_t)k * blockDim.x + threadIdx.x;
+            va[k] = i < n ? ld_stream1(a + i) : 0u;
+            vb[k] = i < n ? ld_stream1(b + i) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            size_t i = t0 + (size_t)k * blockDim.x + threadIdx.x;
+            if (i < n) st_stream1(c + i, op(va[k], vb[k]));
+        }
+    }
+}
+
+// ----------------------------------------------------------------- unary map
+template <int U, class Op>
+__global__ void __launch_bounds__(512) k_map1(Op op, uint32_t *out, const uint32_t *in, uint32_t head, size_t n4,
+                                                uint32_t tail) {
+    if (blockIdx.x == 0 && threadIdx.x < head + tail) {
+        size_t i = threadIdx.x < head ? threadIdx.x : head + 4 * n4 + (threadIdx.x - head);
+        out[i] = op(in[i]);
+    }
+    const uint4 *i4 = reinterpret_cast<const uint4 *>(in + head);
+    uint4 *o4 = reinterpret_cast<uint4 *>(out + head);
+    const size_t tile = (size_t)U * blockDim.x;
+    const size_t ntiles_full = n4 / tile;
+    size_t t = blockIdx.x;
+    for (; t < ntiles_full; t += gridDim.x) {
+        const size_t base = t * tile + threadIdx.x;
+        uint4 v[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) v[k] = ld_stream(i4 + base + (size_t)k * blockDim.x);
+#pragma unroll
+        for (int k = 0; k < U; ++k) st_stream(o4 + base + (size_t)k * blockDim.x, apply4(op, v[k]));
+    }
+    if (t == ntiles_full) {
+        for (size_t i = t * tile + threadIdx.x; i < n4; i += blockDim.x) st_stream(o4 + i, apply4(op, ld_stream(i4 + i)));
+    }
+}
+
+template <int U, class Op>
+__global__ void __launch_bounds__(512) k_map1_scalar(Op op, uint32_t *out, const uint32_t *in, size_t n) {
+    const size_t tile = (size_t)U * blockDim.x;
+    for (size_t t0 = (size_t)blockIdx.x * tile; t0 < n; t0 += (size_t)gridDim.x * tile) {
+        uint32_t v[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            size_t i = t0 + (size_t)k * blockDim.x + threadIdx.x;
+            v[k] = i < n ? ld_stream1(in + i) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            size_t i = t0 + (size_t)k * blockDim.x + threadIdx.x;
+            if (i < n) st_stream1(out + i, op(v[k]));
+        }
+    }
+}
+
+// ------------------------------------------------------------------ checksum
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <int U>
+__global__ void __launch_bounds__(512) k_sum(unsigned long long *acc, const uint32_t *x, uint32_t head, size_t n4,
+                                               uint32_t tail) {
+    unsigned long long s = 0;
+    if (blockIdx.x == 0 && threadIdx.x < head + tail) {
+        size_t i = threadIdx.x < head ? threadIdx.x : head + 4 * n4 + (threadIdx.x - head);
+        s += x[i];
+    }
+    const uint4 *x4 = reinterpret_cast<const uint4 *>(x + head);
+    const size_t tile = (size_t)U * blockDim.x;
+    for (size_t t0 = (size_t)blockIdx.x * tile; t0 < n4; t0 += (size_t)gridDim.x * tile) {
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            size_t i = t0 + (size_t)k * blockDim.x + threadIdx.x;
+            if (i < n4) {
+                uint4 v = ld_stream(x4 + i);
+                s += (unsigned long long)v.x + v.y + (unsigned long long)v.z + v.w;
+            }
+        }
+    }
+    __shared__ unsigned long long warp_part[32];
+    s = warp_sum(s);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) warp_part[wid] = s;
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = (blockDim.x + 31) >> 5;
+        s = lane < nw ? warp_part[lane] : 0ull;
+        s = warp_sum(s);
+        if (lane == 0 && s) atomicAdd(acc, s);
+    }
+}
+
+// ------------------------------------------------------------------- helpers
+template <class Op>
+static mont_status_t launch_map2(const Op &op, uint32_t *c, const uint32_t *a, const uint32_t *b, size_t n,
+                                 const Launch &L, cudaStream_t s) {
+    const int sms = sm_count();
+    if (sms <= 0) return MONT_ECUDA;
+    const uintptr_t pa = (uintptr_t)a, pb = (uintptr_t)b, pc = (uintptr_t)c;
+    const bool flat = L.variant == 1;
+    if (same_mod16(pa, pb) && same_mod16(pa, pc)) {
+        const uint32_t head = head_elems(pa, n);
+        const size_t n4 = (n - head) / 4;
+        const uint32_t tail = (uint32_t)((n - head) % 4);
+        const size_t tile = (size_t)L.unroll * L.threads;
+        size_t grid = flat ? (n4 + tile - 1) / tile : (size_t)sms * L.ctas_per_sm;
+        const size_t need = (n4 + tile - 1) / tile;
+        if (grid > need) grid = need;
+        if (grid == 0) grid = 1;
+        if (grid > 0x7fffffff) return MONT_EUNSUPPORTED;
+        switch (L.unroll) {
+            case 1: k_map2<1><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, head, n4, tail); break;
+            case 2: k_map2<2><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, head, n4, tail); break;
+            case 4: k_map2<4><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, head, n4, tail); break;
+            default: k_map2<8><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, head, n4, tail); break;
+        }
+    } else {
+        const size_t tile = (size_t)L.unroll * L.threads;
+        size_t grid = (size_t)sms * L.ctas_per_sm;
+        const size_t need = (n + tile - 1) / tile;
+        if (grid > need) grid = need;
+        switch (L.unroll) {
+            case 1: k_map2_scalar<1><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, n); break;
+            case 2: k_map2_scalar<2><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, n); break;
+            case 4: k_map2_scalar<4><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, n); break;
+            default: k_map2_scalar<8><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, n); break;
+        }
+    }
+    return launch_status();
+}
+
+template <class Op>
+static mont_status_t launch_map1(const Op &op, uint32_t *out, const uint32_t *in, size_t n, const Launch &L,
+                                 cudaStream_t s) {
+    const int sms = sm_count();
+    if (sms <= 0) return MONT_ECUDA;
+    const uintptr_t pi = (uintptr_t)in, po = (uintptr_t)out;
+    if (same_mod16(pi, po)) {
+        const uint32_t head = head_elems(pi, n);
+        const size_t n4 = (n - head) / 4;
+        const uint32_t tail = (uint32_t)((n - head) % 4);
+        const size_t tile = (size_t)L.unroll * L.threads;
+        size_t grid = L.variant == 1 ? (n4 + tile - 1) / tile : (size_t)sms * L.ctas_per_sm;
+        const size_t need = (n4 + tile - 1) / tile;
+        if (grid > need) grid = need;
+        if (grid == 0) grid = 1;
+        if (grid > 0x7fffffff) return MONT_EUNSUPPORTED;
+        switch (L.unroll) {
+            case 1: k_map1<1><<<(unsigned)grid, L.threads, 0, s>>>(op, out, in, head, n4, tail); break;
+            case 2: k_map1<2><<<(unsigned)grid, L.threads, 0, s>>>(op, out, in, head, n4, tail); break;
+            case 4: k_map1<4><<<(unsigned)grid, L.threads, 0, s>>>(op, out, in, head, n4, tail); break;
+            default: k_map1<8><<<(unsigned)grid, L.threads, 0, s>>>(op, out, in, head, n4, tail); break;
+        }
+    } else {
+        const size_t tile = (size_t)L.unroll * L.threads;
+        size_t grid = (size_t)sms * L.ctas_per_sm;
+        const size_t need = (n + tile - 1) / tile;
+        if (grid > need) grid = need;
+        switch (L.unroll) {
+            case 1: k_map1_scalar<1><<<(unsigned)grid, L.threads, 0, s>>>(op, out, in, n); break;
+            case 2: k_map1_scalar<2><<<(unsigned)grid, L.threads, 0, s>>>(op, out, in, n); break;
+            case 4: k_map1_scalar<4><<<(unsigned)grid, L.threads, 0, s>>>(op, out, in, n); break;
+            default: k_map1_scalar<8><<<(unsigned)grid, L.threads, 0, s>>>(op, out, in, n); break;
+        }
+    }
+    return launch_status();
+}
+
+// defaults chosen by the sweep recorded in DESIGN.md §6
+static const Launch kMulVecDefault{512, 4, 4, 0, 0};
+static const Launch kMap1Default{512, 4, 4, 0, 0};
+
+}  // namespace mont
+
+using namespace mont;
+
+extern "C" mont_status_t mont_mul_vec_ex(const mont_ctx_t *ctx, uint32_t *c, const uint32_t *a, const uint32_t *b,
+                                         size_t n, const mont_launch_t *cfg, cudaStream_t stream) {
+    if (!ctx_ok(ctx)) return ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
+    if (n == 0) return MONT_OK;
+    if (!a || !b || !c || ((uintptr_t)a | (uintptr_t)b | (uintptr_t)c) & 3u) return MONT_EINVAL_ARG;
+    const Launch L = resolve(cfg, kMulVecDefault);
+    if (!launch_ok(L)) return MONT_EINVAL_ARG;
+    return launch_map2(OpMul{ctx->p, ctx->pneg}, c, a, b, n, L, stream);
+}
+
+extern "C" mont_status_t mont_mul_vec(const mont_ctx_t *ctx, uint32_t *c, const uint32_t *a, const uint32_t *b,
+                                      size_t n, cudaStream_t stream) {
+    return mont_mul_vec_ex(ctx, c, a, b, n, nullptr, stream);
+}
+
+extern "C" mont_status_t to_mont(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *in, size_t n,
+                                 cudaStream_t stream) {
+    if (!ctx_ok(ctx)) return ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
+    if (n == 0) return MONT_OK;
+    if (!in || !out || ((uintptr_t)in | (uintptr_t)out) & 3u) return MONT_EINVAL_ARG;
+    return launch_map1(OpTo{ctx->p, ctx->pneg, ctx->r2}, out, in, n, kMap1Default, stream);
+}
+
+extern "C" mont_status_t from_mont(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *in, size_t n,
+                                   cudaStream_t stream) {
+    if (!ctx_ok(ctx)) return ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
+    if (n == 0) return MONT_OK;
+    if (!in || !out || ((uintptr_t)in | (uintptr_t)out) & 3u) return MONT_EINVAL_ARG;
+    return launch_map1(OpFrom{ctx->p, ctx->pneg}, out, in, n, kMap1Default, stream);
+}
+
+extern "C" mont_status_t mont_checksum(const mont_ctx_t *ctx, unsigned long long *acc, const uint32_t *x, size_t n,
+                                       cudaStream_t stream) {
+    if (!ctx_ok(ctx)) return ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
+    if (n == 0) return MONT_OK;
+    if (!acc || !x || ((uintptr_t)acc & 7u) || ((uintptr_t)x & 3u)) return MONT_EINVAL_ARG;
+    const int sms = sm_count();
+    if (sms <= 0) return MONT_ECUDA;
+    const uint32_t head = head_elems((uintptr_t)x, n);
+    const size_t n4 = (n - head) / 4;
+    const uint32_t tail = (uint32_t)((n - head) % 4);
+    const int threads = 512;
+    const size_t tile = 4 * (size_t)threads;
+    size_t grid = (size_t)sms * 4;
+    const size_t need = (n4 + tile - 1) / tile;
+    if (grid > need) grid = need;
+    if (grid == 0) grid = 1;
+    k_sum<4><<<(unsigned)grid, threads, 0, stream>>>(acc, x, head, n4, tail);
+    return launch_status();
+}
+
+extern "C" mont_status_t mb_triad(uint32_t *c, const uint32_t *a, const uint32_t *b, size_t n,
+                                  const mont_launch_t *cfg, cudaStream_t stream) {
+    if (n == 0) return MONT_OK;
+    if (!a || !b || !c) return MONT_EINVAL_ARG;
+    const Launch L = resolve(cfg, kMulVecDefault);
+    if (!launch_ok(L)) return MONT_EINVAL_ARG;
+    return launch_map2(OpXor{}, c, a, b, n, L, stream);
+}
+
+extern "C" mont_status_t mb_copy(uint32_t *out, const uint32_t *in, size_t n, const mont_launch_t *cfg,
+                                 cudaStream_t stream) {
+    if (n == 0) return MONT_OK;
+    if (!in || !out) return MONT_EINVAL_ARG;
+    const Launch L = resolve(cfg, kMap1Default);
+    if (!launch_ok(L)) return MONT_EINVAL_ARG;
+    return launch_map1(OpCopy{}, out, in, n, L, stream);
+}
+
+extern "C" int mont_sm_count(void) { return sm_count(); }

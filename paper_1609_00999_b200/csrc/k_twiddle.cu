@@ -1,0 +1,220 @@
+// k_twiddle.cu -- K2 mont_mul_twiddle: out[r][j] = REDC(x[r][j], tw[j])
+// (BASELINE configs[2]: batch 4096 x len 2^14, the
+// twiddle multiply of one NTT stage of the paper's modular FFTs).
+//
+// B200 design: the grid is 2-D, blockIdx.x = a column chunk of
+// the table (<= 16384 entries = 64 KiB by default), blockIdx.y = a contiguous
+// block of rows.  Each CTA stages its chunk of tw ONCE into shared memory with
+// the bulk-copy engine (cp.async.bulk global->shared, completion counted on an
+// mbarrier by transaction bytes -- the TMA path, SASS UBLKCP), then streams
+// its rows of x through registers with 128-bit non-coherent loads and
+// evict-first stores; the table operand comes from shared memory (LDS.128,
+// conflict-free: consecutive lanes read consecutive 16 B).  HBM traffic is the
+// 8 B/elem of x and out; the table costs gridDim.x*gridDim.y*64 KiB of L2
+// reads, ~0.1 % of the stream at configs[2].
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "abi_util.h"
+
+namespace mont {
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+    } while (!done);
+}
+
+__device__ __forceinline__ uint4 redc4(const uint4 &x, const uint4 &t, uint32_t p, uint32_t pneg) {
+    return make_uint4(redc(x.x, t.x, p, pneg), redc(x.y, t.y, p, pneg), redc(x.z, t.z, p, pneg),
+                      redc(x.w, t.w, p, pneg));
+}
+
+// Vector path: len % 4 == 0, x/out/tw 16-byte aligned.  TMA = stage the table
+// chunk in smem with cp.async.bulk; otherwise read it through L1 (__ldg).
+template <int U, bool TMA>
+__global__ void __launch_bounds__(512) k_twiddle(Ctx c, uint32_t *out, const uint32_t *x, const uint32_t *tw,
+                                                  size_t batch, size_t len, uint32_t chunk, size_t rows_per_cta) {
+    extern __shared__ __align__(128) uint4 s_tw[];
+    __shared__ __align__(8) uint64_t bar;
+    const size_t c0 = (size_t)blockIdx.x * chunk;
+    const size_t r0 = (size_t)blockIdx.y * rows_per_cta;
+    if (r0 >= batch || c0 >= len) return;  // uniform per CTA
+    const size_t cwz = len - c0 < chunk ? len - c0 : chunk;
+    const uint32_t cw4 = (uint32_t)(cwz >> 2);
+    const size_t nrows = batch - r0 < rows_per_cta ? batch - r0 : rows_per_cta;
+    const uint4 *t4 = reinterpret_cast<const uint4 *>(tw + c0);
+    if (TMA) {
+        if (threadIdx.x == 0) {
+            mbar_init(&bar, 1);
+            fence_mbar_init();
+            const uint32_t bytes = cw4 * 16u;
+            mbar_expect_tx(&bar, bytes);
+            const uint32_t piece = 16384u;
+            for (uint32_t off = 0; off < bytes; off += piece) {
+                const uint32_t nb = bytes - off < piece ? bytes - off : piece;
+                bulk_g2s(reinterpret_cast<char *>(s_tw) + off, reinterpret_cast<const char *>(t4) + off, nb, &bar);
+            }
+        }
+        __syncthreads();  // barrier initialised before anyone polls it
+    }
+    const uint4 *x4 = reinterpret_cast<const uint4 *>(x);
+    uint4 *o4 = reinterpret_cast<uint4 *>(out);
+    const size_t len4 = len >> 2;
+    const size_t col0 = c0 >> 2;
+    // running (row, col) position of this thread in the CTA's rows x cw4 tile
+    const uint32_t step_r = blockDim.x / cw4, step_c = blockDim.x % cw4;
+    size_t row = threadIdx.x / cw4;
+    uint32_t col = threadIdx.x % cw4;
+    bool waited = !TMA;
+    while (row < nrows) {
+        uint4 v[U];
+        size_t idx[U];
+        uint32_t cc[U];
+        bool ok[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            ok[k] = row < nrows;
+            idx[k] = (r0 + row) * len4 + col0 + col;
+            cc[k] = col;
+            if (ok[k]) v[k] = ld_stream(x4 + idx[k]);
+            col += step_c;
+            row += step_r;
+            if (col >= cw4) {
+                col -= cw4;
+                ++row;
+            }
+        }
+        if (!waited) {  // first trip: the table copy overlapped the first loads
+            mbar_wait(&bar, 0);
+            waited = true;
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            if (ok[k]) {
+                const uint4 t = TMA ? s_tw[cc[k]] : __ldg(t4 + cc[k]);
+                st_stream(o4 + idx[k], redc4(v[k], t, c.p, c.pneg));
+            }
+        }
+    }
+    if (!waited) mbar_wait(&bar, 0);  // never leave with a copy in flight
+}
+
+// Scalar fallback (len % 4 != 0 or misaligned operands)
+__global__ void __launch_bounds__(256) k_twiddle_scalar(Ctx c, uint32_t *out, const uint32_t *x, const uint32_t *tw,
+                                                         size_t batch, size_t len) {
+    for (size_t r = blockIdx.y; r < batch; r += gridDim.y) {
+        const uint32_t *xr = x + r * len;
+        uint32_t *orow = out + r * len;
+        for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += (size_t)gridDim.x * blockDim.x)
+            st_stream1(orow + j, redc(ld_stream1(xr + j), __ldg(tw + j), c.p, c.pneg));
+    }
+}
+
+static const Launch kTwDefault{512, 3, 4, 0, 16384};
+
+template <int U, bool TMA>
+static mont_status_t launch_tw(const Ctx &c, uint32_t *out, const uint32_t *x, const uint32_t *tw, size_t batch,
+                               size_t len, const Launch &L, int sms, cudaStream_t s) {
+    size_t chunk = (size_t)L.chunk;
+    if (chunk > len) chunk = len;
+    chunk = (chunk + 3) & ~(size_t)3;
+    const size_t nchunks = (len + chunk - 1) / chunk;
+    const size_t smem = TMA ? chunk * 4 : 0;
+    if (smem > 227 * 1024) return MONT_EINVAL_ARG;
+    if (nchunks > 0x7fffffff) return MONT_EUNSUPPORTED;
+    const size_t target = (size_t)sms * L.ctas_per_sm;
+    size_t gy = (target + nchunks - 1) / nchunks;
+    if (gy > batch) gy = batch;
+    if (gy > 65535) gy = 65535;
+    const size_t rows_per_cta = (batch + gy - 1) / gy;
+    gy = (batch + rows_per_cta - 1) / rows_per_cta;
+    if (TMA && smem > 48 * 1024) {
+        if (cudaFuncSetAttribute(k_twiddle<U, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+            return MONT_ECUDA;
+    }
+    dim3 grid((unsigned)nchunks, (unsigned)gy);
+    k_twiddle<U, TMA><<<grid, L.threads, smem, s>>>(c, out, x, tw, batch, len, (uint32_t)chunk, rows_per_cta);
+    return launch_status();
+}
+
+}  // namespace mont
+
+using namespace mont;
+
+extern "C" mont_status_t mont_mul_twiddle_ex(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *x,
+                                             const uint32_t *tw, size_t batch, size_t len,
+                                             const mont_launch_t *cfg, cudaStream_t stream) {
+    if (!ctx_ok(ctx)) return ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
+    if (batch == 0) return MONT_OK;
+    if (len == 0) return MONT_EINVAL_ARG;
+    if (!out || !x || !tw || ((uintptr_t)out | (uintptr_t)x | (uintptr_t)tw) & 3u) return MONT_EINVAL_ARG;
+    if (batch > ((size_t)-1) / len) return MONT_EINVAL_ARG;
+    const Launch L = resolve(cfg, kTwDefault);
+    if (L.threads < 32 || L.threads > 512 || (L.threads & 31) || L.ctas_per_sm < 1 || L.chunk < 4 ||
+        (L.chunk & 3) || !(L.unroll == 1 || L.unroll == 2 || L.unroll == 4 || L.unroll == 8) || L.variant < 0 ||
+        L.variant > 1)
+        return MONT_EINVAL_ARG;
+    const int sms = sm_count();
+    if (sms <= 0) return MONT_ECUDA;
+    const Ctx c = to_dev(ctx);
+    const bool vec = (len % 4 == 0) && (((uintptr_t)out | (uintptr_t)x | (uintptr_t)tw) & 15u) == 0;
+    if (!vec) {
+        size_t gx = (len + 255) / 256;
+        if (gx > (size_t)sms * 8) gx = (size_t)sms * 8;
+        size_t gy = ((size_t)sms * 8 + gx - 1) / gx;
+        if (gy > batch) gy = batch;
+        if (gy > 65535) gy = 65535;
+        k_twiddle_scalar<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, stream>>>(c, out, x, tw, batch, len);
+        return launch_status();
+    }
+    if (L.variant == 0) {
+        switch (L.unroll) {
+            case 1: return launch_tw<1, true>(c, out, x, tw, batch, len, L, sms, stream);
+            case 2: return launch_tw<2, true>(c, out, x, tw, batch, len, L, sms, stream);
+            case 4: return launch_tw<4, true>(c, out, x, tw, batch, len, L, sms, stream);
+            default: return launch_tw<8, true>(c, out, x, tw, batch, len, L, sms, stream);
+        }
+    }
+    switch (L.unroll) {
+        case 1: return launch_tw<1, false>(c, out, x, tw, batch, len, L, sms, stream);
+        case 2: return launch_tw<2, false>(c, out, x, tw, batch, len, L, sms, stream);
+        case 4: return launch_tw<4, false>(c, out, x, tw, batch, len, L, sms, stream);
+        default: return launch_tw<8, false>(c, out, x, tw, batch, len, L, sms, stream);
+    }
+}
+
+extern "C" mont_status_t mont_mul_twiddle(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *x,
+                                          const uint32_t *tw, size_t batch, size_t len, cudaStream_t stream) {
+    return mont_mul_twiddle_ex(ctx, out, x, tw, batch, len, nullptr, stream);
+}

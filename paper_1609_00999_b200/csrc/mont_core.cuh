@@ -1,0 +1,131 @@
+// mont_core.cuh -- device-side Montgomery REDC for R = 2^32 on sm_100a.
+//
+// PAPER.md Alg. 2 (REDC, :95-99) with the GPU refinement of the §3.2 dataflow
+// (:121-139): the paper gathers high and low 32-bit halves of 2-way 64-bit
+// products with shuffles because SSE has no high-half multiply; sm_100a has
+// one (mul.hi.u32 -> IMAD.HI), so the three integer multiplications
+// become four single-issue FMAHeavy-pipe instructions and no
+// gather exists:
+//
+//   T  = a*b                 mul.lo + mul.hi       (A3, "needs twice the width", :123)
+//   m  = lo(T) * P' mod 2^32 mul.lo                (A4, the "short product", :93, :129)
+//   t  = (T + m P) / 2^32    mul.hi + carry        (A5, the "2-way addition ... carries", :137)
+//   t >= P ? t - P : t       min(t, t - P)         (A6, "selectively subtracting P", :139)
+//
+// The low half of m*P is never formed: lo(T) + lo(mP) = 0 (mod 2^32) by the
+// choice of m, so the carry into the high word is exactly [lo(T) != 0].
+// With P < 2^31 and a*b < R*P the pre-subtract t lies in [0, 2P)
+// and fits 32 bits, so min(t, t-P) on unsigned words is the single conditional
+// subtract.
+//
+// A second, "signed" form (used by the pow ladder) keeps values in the open
+// interval (-P, P) as int32 and needs no correction between products:
+//   m = lo(T) * P^-1 mod 2^32 ; t = (T - m P) / 2^32   (exact, arithmetic shift)
+// T - mP = 0 (mod 2^32) exactly, and |t| <= (|T| + 2^31 P) / 2^32 < P whenever
+// |a*b| < 2^31 P, which holds for |a|, |b| < P < 2^31.  It differs from the
+// paper's P' only in sign (P^-1 = -P'), reading G2.
+#pragma once
+#include <stdint.h>
+
+namespace mont {
+
+struct Ctx {  // mirrors mont_ctx_t (by value in kernel params)
+    uint32_t p, pneg, r1, r2;
+};
+
+__device__ __forceinline__ uint32_t umin(uint32_t x, uint32_t y) { return x < y ? x : y; }
+
+// canonical REDC(a*b): a*b < 2^32 * P required; returns [0, P).
+// "wide" form: T = a*b (IMAD.WIDE), m = lo(T) P' (IMAD), then
+// (T + m P) >> 32 is ONE IMAD.WIDE with the 64-bit T as addend -- the carry of
+// the paper's "2-way addition" is done inside the multiplier.
+// T + mP < 2 R P < 2^64, so nothing overflows.  3 FMAHeavy ops + 1 ALU op.
+__device__ __forceinline__ uint64_t mul_wide_u32(uint32_t a, uint32_t b) {
+    uint64_t r;
+    asm("mul.wide.u32 %0, %1, %2;" : "=l"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ int64_t mul_wide_s32(int32_t a, int32_t b) {
+    int64_t r;
+    asm("mul.wide.s32 %0, %1, %2;" : "=l"(r) : "r"(a), "r"(b));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t redc(uint32_t a, uint32_t b, uint32_t p, uint32_t pneg) {
+    const uint64_t T = mul_wide_u32(a, b);                       // IMAD.WIDE.U32
+    const uint32_t m = (uint32_t)T * pneg;                       // IMAD
+    const uint32_t t = (uint32_t)(((uint64_t)m * p + T) >> 32);  // IMAD.HI.U32, 64-bit addend
+    return umin(t, t - p);
+}
+
+// "hi/lo" form with mul.lo / mul.hi only (kept for the microbenchmark and as
+// the literal reading of the three multiplications): 4 FMAHeavy ops.
+__device__ __forceinline__ uint32_t redc_hl(uint32_t a, uint32_t b, uint32_t p, uint32_t pneg) {
+    uint32_t lo = a * b;
+    uint32_t hi = __umulhi(a, b);
+    uint32_t m = lo * pneg;
+    uint32_t t = __umulhi(m, p) + hi + (lo != 0u ? 1u : 0u);
+    return umin(t, t - p);
+}
+
+// REDC(x * 1) = x R^-1 mod P: T = x, so only m and (x + m P) >> 32 (A10)
+__device__ __forceinline__ uint32_t redc1(uint32_t x, uint32_t p, uint32_t pneg) {
+    const uint32_t m = x * pneg;
+    const uint32_t t = (uint32_t)(((uint64_t)m * p + x) >> 32);
+    return umin(t, t - p);
+}
+
+// signed lazy form: |a|,|b| < P  ->  result in (-P, P), congruent to a b R^-1.
+// negp = -P, pinv = P^-1 mod 2^32.  T - m P = 0 (mod 2^32) exactly, so the
+// arithmetic shift of the IMAD.WIDE result is the exact division by R.
+// 3 FMAHeavy ops, no ALU op.
+__device__ __forceinline__ int32_t sredc(int32_t a, int32_t b, int32_t negp, int32_t pinv) {
+    const int64_t T = mul_wide_s32(a, b);                       // IMAD.WIDE
+    const int32_t m = (int32_t)T * pinv;                        // IMAD
+    return (int32_t)(((int64_t)m * negp + T) >> 32);            // IMAD.HI, 64-bit addend
+}
+
+// signed hi/lo form (4 FMAHeavy ops + 1 ALU op), microbenchmark reference
+__device__ __forceinline__ int32_t sredc_hl(int32_t a, int32_t b, int32_t p, int32_t pinv) {
+    int32_t lo = a * b;
+    int32_t hi = __mulhi(a, b);
+    int32_t m = lo * pinv;
+    return hi - __mulhi(m, p);
+}
+
+// signed REDC(x * 1) for |x| < P -> (-P, P)
+__device__ __forceinline__ int32_t sredc1(int32_t x, int32_t negp, int32_t pinv) {
+    const int32_t m = x * pinv;
+    return (int32_t)(((int64_t)m * negp + (int64_t)x) >> 32);
+}
+
+// (-P, P) -> [0, P)
+__device__ __forceinline__ uint32_t canon(int32_t t, int32_t p) {
+    uint32_t u = (uint32_t)t;
+    return umin(u, u + (uint32_t)p);
+}
+
+// streaming 128-bit loads / stores: read-only path, no L1 allocation, 256B L2
+// prefetch hint; stores evict-first (each byte is touched exactly once)
+__device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
+    uint4 r;
+    asm("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_stream(uint4 *p, const uint4 &v) {
+    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ uint32_t ld_stream1(const uint32_t *p) {
+    uint32_t r;
+    asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_stream1(uint32_t *p, uint32_t v) {
+    asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+}  // namespace mont

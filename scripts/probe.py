@@ -1,0 +1,145 @@
+"""Quick on-GPU sweep: microbenchmarks (IMAD kinds, triad/copy) and kernel launch-config
+sweeps.  Prints one JSON object per measurement.  Used to pick library defaults
+(DESIGN.md §6); not part of the product."""
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import paper_1609_00999_b200 as m  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--what", default="all")
+ap.add_argument("--reps", type=int, default=20)
+args = ap.parse_args()
+
+dev = torch.device("cuda:0")
+s = torch.cuda.current_stream()
+sms = m.sm_count()
+
+
+def timeit(fn, reps=args.reps, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for e0, e1 in ev:
+        e0.record()
+        fn()
+        e1.record()
+    torch.cuda.synchronize()
+    t = sorted(e0.elapsed_time(e1) for e0, e1 in ev)
+    return t[len(t) // 2] * 1e-3, t[0] * 1e-3
+
+
+def out(**kw):
+    print(json.dumps(kw), flush=True)
+
+
+def lib():
+    return m.lib()
+
+
+if args.what in ("all", "imad"):
+    import ctypes as C
+    sink = torch.empty(sms * 32 * 256, dtype=torch.uint32, device=dev)
+    names = {0: "IMAD", 1: "IMAD.HI", 2: "IMAD.WIDE", 3: "sredc_hl", 4: "redc_hl", 5: "sredc_wide", 6: "redc_wide"}
+    for kind in range(7):
+        for ctas in (4, 8):
+            iters = 2000
+            nthr = C.c_ulonglong(0)
+            cfg = m.Launch(ctas_per_sm=ctas)
+
+            def f():
+                st = lib().mb_imad(sink.data_ptr(), kind, iters, C.byref(cfg), s.cuda_stream, C.byref(nthr))
+                assert st == 0
+
+            med, best = timeit(f, reps=5)
+            ops = nthr.value * iters * 64
+            out(what="imad", kind=names[kind], ctas_per_sm=ctas, ops=ops, sec=med,
+                gops=ops / med / 1e9, per_sm_per_clk_at_1965=ops / med / sms / 1.965e9)
+
+if args.what in ("all", "hbm"):
+    import ctypes as C
+    n = 1 << 26
+    a = torch.empty(n, dtype=torch.uint32, device=dev)
+    b = torch.empty(n, dtype=torch.uint32, device=dev)
+    c = torch.empty(n, dtype=torch.uint32, device=dev)
+    m.synth_fill(a, 42, 1, 0, 2013265921)
+    m.synth_fill(b, 42, 2, 0, 2013265921)
+    ctx = m.ctx_init(2013265921)
+    for threads in (256, 512):
+        for ctas in (2, 4, 8):
+            for unroll in (1, 2, 4, 8):
+                for variant in (0, 1):
+                    if variant == 1 and ctas != 4:
+                        continue
+                    cfg = m.Launch(threads=threads, ctas_per_sm=ctas, unroll=unroll, variant=variant)
+                    med, best = timeit(lambda: lib().mb_triad(c.data_ptr(), a.data_ptr(), b.data_ptr(), n,
+                                                              C.byref(cfg), s.cuda_stream))
+                    out(what="triad", threads=threads, ctas=ctas, unroll=unroll, variant=variant,
+                        us=med * 1e6, gbs=12 * n / med / 1e9, gbs_best=12 * n / best / 1e9)
+                    med, best = timeit(lambda: m.mul_vec(ctx, a, b, out=c, cfg=cfg))
+                    out(what="mul_vec", threads=threads, ctas=ctas, unroll=unroll, variant=variant,
+                        us=med * 1e6, gbs=12 * n / med / 1e9, gbs_best=12 * n / best / 1e9,
+                        gmulmod=n / med / 1e9)
+    cfg = m.Launch()
+    med, best = timeit(lambda: lib().mb_copy(c.data_ptr(), a.data_ptr(), n, C.byref(cfg), s.cuda_stream))
+    out(what="copy", us=med * 1e6, gbs=8 * n / med / 1e9)
+    med, best = timeit(lambda: c.copy_(a))
+    out(what="torch_copy", us=med * 1e6, gbs=8 * n / med / 1e9)
+    med, best = timeit(lambda: m.to_mont(ctx, a, out=c))
+    out(what="to_mont", us=med * 1e6, gbs=8 * n / med / 1e9)
+    med, best = timeit(lambda: m.from_mont(ctx, a, out=c))
+    out(what="from_mont", us=med * 1e6, gbs=8 * n / med / 1e9)
+    acc = torch.zeros(1, dtype=torch.int64, device=dev)
+    med, best = timeit(lambda: m.checksum(ctx, a, acc=acc))
+    out(what="checksum", us=med * 1e6, gbs=4 * n / med / 1e9)
+
+if args.what in ("all", "tw"):
+    P = 2013265921
+    ctx = m.ctx_init(P)
+    batch, L = 4096, 1 << 14
+    x = torch.empty(batch * L, dtype=torch.uint32, device=dev)
+    m.synth_fill(x, 42, 5, 0, P)
+    x = x.view(batch, L)
+    o = torch.empty_like(x)
+    tw = m.twiddle_table(ctx, 1657000625, L)
+    for variant in (0, 1):
+        for ctas in (1, 2, 3, 4):
+            for unroll in (2, 4, 8):
+                for chunk in (4096, 16384):
+                    for threads in (256, 512):
+                        cfg = m.Launch(threads=threads, ctas_per_sm=ctas, unroll=unroll, variant=variant,
+                                       chunk=chunk)
+                        try:
+                            med, best = timeit(lambda: m.mul_twiddle(ctx, x, tw, out=o, cfg=cfg))
+                        except m.MontError as e:
+                            out(what="twiddle", err=str(e), ctas=ctas, chunk=chunk)
+                            continue
+                        out(what="twiddle", variant=variant, ctas=ctas, unroll=unroll, chunk=chunk,
+                            threads=threads, us=med * 1e6, gbs=8 * batch * L / med / 1e9,
+                            gmulmod=batch * L / med / 1e9)
+
+if args.what in ("all", "pow"):
+    P = 469762049
+    ctx = m.ctx_init(P)
+    n = 1 << 24
+    base = torch.empty(n, dtype=torch.uint32, device=dev)
+    e = torch.empty(n, dtype=torch.uint32, device=dev)
+    o = torch.empty(n, dtype=torch.uint32, device=dev)
+    m.synth_fill(base, 42, 3, 0, P, mode=1)
+    m.synth_fill(e, 42, 4, 0, P, mode=2)
+    pc = e.cpu().numpy()
+    import numpy as np
+    useful = int(31 * n + np.unpackbits(pc.view(np.uint8)).sum())
+    for variant in (0, 1, 2):
+        for ctas in (2, 4, 8, 16):
+            cfg = m.Launch(variant=variant, ctas_per_sm=ctas)
+            med, best = timeit(lambda: m.pow_vec(ctx, base, e, out=o, cfg=cfg), reps=10)
+            out(what="pow", variant=variant, ctas=ctas, us=med * 1e6, useful_mulmods=useful,
+                tmulmod=useful / med / 1e12)

@@ -1,0 +1,111 @@
+"""CPU-only checks of the C-ABI library: it loads, exports every symbol include/*.h
+declares, and its host-side logic (context precompute, argument validation)
+behaves as documented.  No kernel is launched here."""
+import ctypes as C
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1609_00999_b200 as m
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADERS = sorted((ROOT / "include").glob("*.h"))
+
+
+def declared_functions():
+    names = []
+    for h in HEADERS:
+        text = h.read_text()
+        text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+        for mt in re.finditer(r"^\s*(?:const\s+)?[A-Za-z_][A-Za-z0-9_ ]*?[\s\*]+([A-Za-z_][A-Za-z0-9_]*)\s*\(",
+                              text, flags=re.M):
+            name = mt.group(1)
+            if name not in ("if", "while", "for", "sizeof", "return"):
+                names.append(name)
+    return sorted(set(names))
+
+
+def test_headers_declare_the_north_star_api():
+    names = declared_functions()
+    for required in ("mont_ctx_init", "to_mont", "from_mont", "mont_mul_vec", "mont_mul_twiddle",
+                     "mont_pow_vec", "mont_checksum", "mont_strerror"):
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = C.CDLL(str(m.LIB_PATH))
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+    # and the binding knows every one of them
+    assert set(declared_functions()) == set(m.SIGNATURES)
+
+
+def test_build_arch():
+    assert m.lib().mont_build_arch() == 100
+
+
+@pytest.mark.parametrize("P", list(range(3, 258, 2)) + [2013265921, 469762049, 998244353, 2147483647,
+                                                         1073741827, 65537, 12289])
+def test_ctx_matches_oracle(P):
+    """Newton-lifted P' (library) vs extended Euclid (oracle), plus r1, r2."""
+    c = m.ctx_init(P)
+    o = oracle.ctx(P)
+    assert (c.p, c.pneg, c.r1, c.r2) == (o.P, o.Pprime, o.r1, o.r2)
+
+
+def test_ctx_random_odd_moduli():
+    rng = np.random.default_rng(11)
+    for P in rng.integers(3, 1 << 31, 2000):
+        P = int(P) | 1
+        if P >= 1 << 31:
+            continue
+        c = m.ctx_init(P)
+        assert (c.p * c.pneg) % (1 << 32) == (1 << 32) - 1
+        assert c.r1 == (1 << 32) % P and c.r2 == (1 << 64) % P
+
+
+@pytest.mark.parametrize("P", [0, 1, 2, 4, 1 << 30, 1 << 31, (1 << 31) + 1, 0xFFFFFFFF])
+def test_ctx_rejects(P):
+    with pytest.raises(m.MontError) as e:
+        m.ctx_init(P)
+    assert e.value.status == 1
+
+
+def test_null_ctx_and_strerror():
+    L = m.lib()
+    assert L.mont_ctx_init(None, 17) == 2
+    for s in range(5):
+        assert L.mont_strerror(s)
+    assert L.mont_strerror(99) == b"unknown status"
+
+
+def test_validation_without_launch():
+    """Synchronous validation paths return before touching CUDA (safe without a GPU)."""
+    L = m.lib()
+    ctx = m.ctx_init(2013265921)
+    bad = m.Ctx(2013265921, 1, 0, 0)           # pneg wrong: not from mont_ctx_init
+    pc = C.byref(ctx)
+    assert L.mont_mul_vec(pc, None, None, None, 0, None) == 0          # n == 0: OK, no launch
+    assert L.mont_mul_vec(pc, None, None, None, 5, None) == 2          # NULL with n > 0
+    assert L.mont_mul_vec(C.byref(bad), None, None, None, 5, None) == 1
+    assert L.mont_mul_vec(None, None, None, None, 5, None) == 2
+    assert L.mont_mul_vec(pc, 0x1002, 0x2000, 0x3000, 5, None) == 2   # not 4-byte aligned
+    assert L.to_mont(pc, None, None, 0, None) == 0
+    assert L.from_mont(pc, None, None, 3, None) == 2
+    assert L.mont_pow_vec(pc, None, None, None, 0, None) == 0
+    assert L.mont_pow_vec(pc, None, None, None, 1, None) == 2
+    assert L.mont_mul_twiddle(pc, None, None, None, 0, 16, None) == 0  # batch == 0
+    assert L.mont_mul_twiddle(pc, 0x1000, 0x2000, 0x3000, 4, 0, None) == 2  # len == 0
+    assert L.mont_mul_twiddle(pc, 0x1000, 0x2000, 0x3000, 1 << 40, 1 << 40, None) == 2  # overflow
+    assert L.mont_checksum(pc, None, None, 0, None) == 0
+    assert L.mont_checksum(pc, 0x1004, 0x2000, 8, None) == 2           # acc not 8-byte aligned
+    assert L.mont_twiddle_table(pc, None, 5, 0, None) == 0
+    cfg = m.Launch(threads=100)
+    assert L.mont_mul_vec_ex(pc, 0x1000, 0x2000, 0x3000, 8, C.byref(cfg), None) == 2  # threads % 32
+    cfg = m.Launch(unroll=3)
+    assert L.mont_mul_vec_ex(pc, 0x1000, 0x2000, 0x3000, 8, C.byref(cfg), None) == 2
+    assert L.synth_fill(None, 4, 1, 1, 0, 17, 0, 0, None) == 2
+    assert L.synth_fill(0x1000, 4, 1, 1, 0, 17, 7, 0, None) == 2

@@ -1,0 +1,289 @@
+"""GPU parity: every kernel through the C ABI vs the CPU oracle, bit-exact.
+
+Sizes span several tiles and ragged tails; edge cases cover n = 0..9,
+misaligned (4/8/12-byte offset) operands, mixed alignments, in-place calls,
+the fixed-index edge values of configs[0] and the specials of configs[1].
+Full-size configs are in tests/test_gpu_fullsize.py.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+PRIMES = (2013265921, 469762049, 998244353)
+ODD_SMALL = (3, 5, 17, 97, 257, 65537, 12289, 2147483647, 1073741827)
+
+
+@pytest.fixture(scope="module")
+def m():
+    import paper_1609_00999_b200 as mod
+    return mod
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def offset_view(x: np.ndarray, off: int):
+    """Device tensor holding x starting `off` uint32 elements into a fresh allocation."""
+    buf = torch.empty(x.size + 8, dtype=torch.uint32, device="cuda")
+    v = buf[off:off + x.size]
+    v.copy_(dev(x))
+    return v
+
+
+# ------------------------------------------------------------------ mul_vec
+
+@pytest.mark.parametrize("P", PRIMES)
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 7, 8, 9, 31, 33, 1000, 4099, 65536, 262147, 1 << 20 | 5])
+def test_mul_vec_parity(m, P, n):
+    a, b = synth.c2_inputs(P, 0, n)
+    ctx = m.ctx_init(P)
+    c = m.mul_vec(ctx, dev(a), dev(b))
+    assert np.array_equal(host(c), oracle.mont_mul(P, a, b))
+
+
+def test_mul_vec_c1_config(m):
+    P = 2013265921
+    a, b = synth.c1_inputs(P)
+    c = host(m.mul_vec(m.ctx_init(P), dev(a), dev(b)))
+    ref = oracle.mont_mul(P, a, b)
+    assert np.array_equal(c, ref)
+    assert oracle.checksum(P, c) == oracle.checksum(P, ref)
+
+
+@pytest.mark.parametrize("P", ODD_SMALL)
+def test_mul_vec_other_moduli(m, P):
+    rng = np.random.default_rng(P)
+    n = 100_003
+    a = rng.integers(0, P, n, dtype=np.uint64).astype(np.uint32)
+    b = rng.integers(0, P, n, dtype=np.uint64).astype(np.uint32)
+    a[:3] = [0, P - 1, P - 1]
+    b[:3] = [P - 1, P - 1, 0]
+    c = m.mul_vec(m.ctx_init(P), dev(a), dev(b))
+    assert np.array_equal(host(c), oracle.mont_mul(P, a, b))
+
+
+@pytest.mark.parametrize("P", (3, 5, 7, 17, 97, 251, 257))
+def test_mul_vec_all_pairs_small(m, P):
+    g = np.arange(P, dtype=np.uint32)
+    a = np.repeat(g, P)
+    b = np.tile(g, P)
+    c = m.mul_vec(m.ctx_init(P), dev(a), dev(b))
+    assert np.array_equal(host(c), oracle.mont_mul(P, a, b))
+
+
+def test_mul_vec_one_operand_noncanonical(m):
+    """REDC needs only a*b < R P: any uint32 a with b < P is valid."""
+    P = 2013265921
+    rng = np.random.default_rng(12)
+    n = 50_001
+    a = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    b = rng.integers(0, P, n, dtype=np.uint64).astype(np.uint32)
+    a[:2] = [0xFFFFFFFF, 0xFFFFFFFF]
+    b[:2] = [P - 1, 0]
+    c = host(m.mul_vec(m.ctx_init(P), dev(a), dev(b)))
+    assert np.array_equal(c, oracle.mont_mul(P, a % np.uint32(P), b))
+
+
+@pytest.mark.parametrize("oa,ob,oc", [(1, 1, 1), (2, 2, 2), (3, 3, 3), (0, 1, 2), (1, 0, 0), (3, 0, 1), (0, 0, 3)])
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 5, 6, 9, 1023, 40_000 + 3])
+def test_mul_vec_alignment(m, oa, ob, oc, n):
+    P = 998244353
+    a, b = synth.c2_inputs(P, 7, n)
+    ta, tb = offset_view(a, oa), offset_view(b, ob)
+    buf = dev(np.full(n + 8, 0xDEADBEEF, dtype=np.uint32))
+    tc = buf[oc:oc + n]
+    m.mul_vec(m.ctx_init(P), ta, tb, out=tc)
+    full = host(buf)
+    assert np.array_equal(full[oc:oc + n], oracle.mont_mul(P, a, b))
+    # nothing outside [oc, oc+n) was written
+    assert np.all(full[:oc] == 0xDEADBEEF) and np.all(full[oc + n:] == 0xDEADBEEF)
+
+
+def test_mul_vec_in_place(m):
+    P = 469762049
+    a, b = synth.c2_inputs(P, 0, 100_001)
+    ta, tb = dev(a), dev(b)
+    m.mul_vec(m.ctx_init(P), ta, tb, out=ta)
+    assert np.array_equal(host(ta), oracle.mont_mul(P, a, b))
+    tb2 = dev(b)
+    m.mul_vec(m.ctx_init(P), dev(a), tb2, out=tb2)
+    assert np.array_equal(host(tb2), oracle.mont_mul(P, a, b))
+
+
+@pytest.mark.parametrize("threads,ctas,unroll,variant", [(32, 1, 1, 0), (128, 2, 2, 0), (256, 8, 8, 0),
+                                                         (512, 4, 4, 1), (512, 1, 8, 1), (64, 32, 4, 0)])
+def test_mul_vec_launch_configs(m, threads, ctas, unroll, variant):
+    P = 2013265921
+    a, b = synth.c2_inputs(P, 0, 300_007)
+    cfg = m.Launch(threads=threads, ctas_per_sm=ctas, unroll=unroll, variant=variant)
+    c = m.mul_vec(m.ctx_init(P), dev(a), dev(b), cfg=cfg)
+    assert np.array_equal(host(c), oracle.mont_mul(P, a, b))
+
+
+def test_mul_vec_empty(m):
+    e = torch.empty(0, dtype=torch.uint32, device="cuda")
+    assert m.mul_vec(m.ctx_init(17), e, e).numel() == 0
+
+
+# ------------------------------------------------------------- to/from_mont
+
+@pytest.mark.parametrize("P", PRIMES + (3, 17, 2147483647))
+@pytest.mark.parametrize("n", [1, 3, 4, 5, 4096 + 3, 1 << 20])
+def test_to_from_mont_parity(m, P, n):
+    x = synth.uniform(42, 9, P, 0, n)
+    ctx = m.ctx_init(P)
+    tm = m.to_mont(ctx, dev(x))
+    assert np.array_equal(host(tm), oracle.to_mont(P, x))
+    fm = m.from_mont(ctx, dev(x))
+    assert np.array_equal(host(fm), oracle.from_mont(P, x))
+    assert np.array_equal(host(m.from_mont(ctx, tm)), x)
+
+
+def test_to_from_mont_noncanonical_input(m):
+    P = 2013265921
+    rng = np.random.default_rng(13)
+    x = rng.integers(0, 1 << 32, 10_001, dtype=np.uint64).astype(np.uint32)
+    x[:2] = [0xFFFFFFFF, P]
+    ctx = m.ctx_init(P)
+    assert np.array_equal(host(m.to_mont(ctx, dev(x))), oracle.to_mont(P, x))
+    assert np.array_equal(host(m.from_mont(ctx, dev(x))), oracle.from_mont(P, x))
+
+
+@pytest.mark.parametrize("off_in,off_out", [(1, 1), (1, 2), (3, 0), (2, 2)])
+def test_to_mont_alignment_in_place(m, off_in, off_out):
+    P = 469762049
+    x = synth.uniform(42, 9, P, 0, 1001)
+    ti = offset_view(x, off_in)
+    to = offset_view(np.zeros_like(x), off_out)
+    ctx = m.ctx_init(P)
+    m.to_mont(ctx, ti, out=to)
+    assert np.array_equal(host(to), oracle.to_mont(P, x))
+    m.from_mont(ctx, to, out=to)
+    assert np.array_equal(host(to), x)
+
+
+# --------------------------------------------------------------------- pow
+
+@pytest.mark.parametrize("P", PRIMES + (17, 257, 2147483647, 3))
+@pytest.mark.parametrize("variant", [0, 1, 2])
+def test_pow_parity(m, P, variant):
+    n = 20_003
+    base = synth.uniform(42, synth.STREAM_BASE, P, 0, n, low=1) if P > 3 else \
+        np.random.default_rng(0).integers(0, 3, n).astype(np.uint32)
+    exp = synth.exponents(42, synth.STREAM_EXP, 0, n)
+    base[:6] = [0, 0, 1, P - 1, P - 1, 2 % P]
+    exp[:6] = [0, 7, 0, 0, (1 << 31) - 1, 0x7FFFFFFF]
+    cfg = m.Launch(variant=variant)
+    out = m.pow_vec(m.ctx_init(P), dev(base), dev(exp), cfg=cfg)
+    assert np.array_equal(host(out), oracle.power(P, base, exp))
+
+
+def test_pow_full_32bit_exponents_and_big_bases(m):
+    """Header contract: any uint32 base (reduced mod P) and full 32-bit exponents."""
+    P = 998244353
+    rng = np.random.default_rng(14)
+    n = 9_999
+    base = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    exp = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    exp[:3] = [0xFFFFFFFF, 1 << 31, 0]
+    ref = np.array([pow(int(b), int(e), P) for b, e in zip(base, exp)], dtype=np.uint32)
+    for variant in (0, 1, 2):
+        out = m.pow_vec(m.ctx_init(P), dev(base), dev(exp), cfg=m.Launch(variant=variant))
+        assert np.array_equal(host(out), ref)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6, 7, 1000, 1 << 16 | 3])
+def test_pow_ragged_and_misaligned(m, n):
+    P = 469762049
+    base, exp = synth.c4_inputs(P, 5, n)
+    ref = oracle.power(P, base, exp)
+    ctx = m.ctx_init(P)
+    assert np.array_equal(host(m.pow_vec(ctx, dev(base), dev(exp))), ref)
+    tb, te = offset_view(base, 1), offset_view(exp, 1)
+    to = offset_view(np.zeros_like(base), 1)
+    m.pow_vec(ctx, tb, te, out=to)
+    assert np.array_equal(host(to), ref)
+    tb, te = offset_view(base, 1), offset_view(exp, 2)
+    assert np.array_equal(host(m.pow_vec(ctx, tb, te)), ref)
+
+
+# ----------------------------------------------------------------- twiddle
+
+@pytest.mark.parametrize("L", [4, 16, 1000, 1024, 4096, 16384, 16388, 65536])
+def test_twiddle_table_parity(m, L):
+    P = 2013265921
+    order = 1 << 14
+    w = oracle.root_of_unity(P, synth.G11_GENERATOR, order)
+    tw = m.twiddle_table(m.ctx_init(P), w, L)
+    assert np.array_equal(host(tw), oracle.twiddle_table(P, w, L))
+
+
+@pytest.mark.parametrize("batch,L", [(1, 4), (3, 8), (5, 1000), (17, 1024), (7, 16384), (3, 16388), (2, 40000),
+                                     (1000, 64), (33, 4100)])
+@pytest.mark.parametrize("variant", [0, 1])
+def test_twiddle_parity(m, batch, L, variant):
+    P = 2013265921
+    x = synth.c3_x(P, batch=batch, length=L)
+    rng = np.random.default_rng(L)
+    tw = rng.integers(0, P, L, dtype=np.uint64).astype(np.uint32)
+    out = m.mul_twiddle(m.ctx_init(P), dev(x), dev(tw), cfg=m.Launch(variant=variant))
+    assert np.array_equal(host(out), oracle.twiddle(P, x, tw))
+
+
+@pytest.mark.parametrize("batch,L", [(3, 5), (4, 7), (2, 1001), (9, 3)])
+def test_twiddle_ragged_len(m, batch, L):
+    P = 998244353
+    x = synth.c3_x(P, batch=batch, length=L)
+    tw = synth.uniform(42, 11, P, 0, L)
+    out = m.mul_twiddle(m.ctx_init(P), dev(x), dev(tw))
+    assert np.array_equal(host(out), oracle.twiddle(P, x, tw))
+
+
+@pytest.mark.parametrize("chunk,ctas,unroll,threads", [(4, 1, 1, 32), (1024, 2, 2, 128), (4096, 8, 8, 512),
+                                                       (16384, 3, 4, 512), (36, 3, 4, 256)])
+def test_twiddle_launch_configs(m, chunk, ctas, unroll, threads):
+    P = 469762049
+    batch, L = 37, 8192
+    x = synth.c3_x(P, batch=batch, length=L)
+    tw = synth.uniform(42, 11, P, 0, L)
+    cfg = m.Launch(threads=threads, ctas_per_sm=ctas, unroll=unroll, chunk=chunk)
+    out = m.mul_twiddle(m.ctx_init(P), dev(x), dev(tw), cfg=cfg)
+    assert np.array_equal(host(out), oracle.twiddle(P, x, tw))
+
+
+def test_twiddle_misaligned_and_in_place(m):
+    P = 2013265921
+    batch, L = 6, 1024
+    x = synth.c3_x(P, batch=batch, length=L)
+    tw = synth.uniform(42, 11, P, 0, L)
+    ref = oracle.twiddle(P, x, tw)
+    ctx = m.ctx_init(P)
+    tx = offset_view(x.reshape(-1), 1).view(batch, L)
+    ttw = offset_view(tw, 3)
+    assert np.array_equal(host(m.mul_twiddle(ctx, tx, ttw)), ref)
+    tx = dev(x)
+    m.mul_twiddle(ctx, tx, dev(tw), out=tx)
+    assert np.array_equal(host(tx), ref)
+
+
+# ---------------------------------------------------------------- checksum
+
+@pytest.mark.parametrize("n", [1, 3, 4, 5, 1000, 65536 + 7, 1 << 22])
+@pytest.mark.parametrize("off", [0, 1, 2, 3])
+def test_checksum(m, n, off):
+    P = 2013265921
+    x = synth.uniform(42, 1, P, 0, n)
+    acc = m.checksum(m.ctx_init(P), offset_view(x, off))
+    torch.cuda.synchronize()
+    assert int(acc.item()) == oracle.raw_sum(x)
