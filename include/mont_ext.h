@@ -20,10 +20,16 @@ extern "C" {
  *   ctas_per_sm: CTAs per SM for the persistent grid (grid = SMs * ctas_per_sm)
  *   unroll    : 128-bit chunks per thread per loop trip (1, 2, 4 or 8)
  *   variant   : kernel variant (kernel-specific; 0 = default).
- *                 mont_mul_vec_ex : 0 = LDG.128 grid-stride, 1 = flat grid
- *                                   (one trip per thread, no loop)
- *                 mont_pow_vec_ex : 0 = 2-bit fixed window, 1 = binary
- *                                   ladder with selects, 2 = 3-bit window
+ *                 mont_mul_vec_ex, mb_triad, mb_copy : 0 = flat grid (one
+ *                                   tile of threads*unroll uint4 per CTA),
+ *                                   1 = persistent grid-stride over tiles
+ *                                   with grid = SMs * ctas_per_sm
+ *                 mont_pow_vec_ex : 0 = 2-bit fixed window, table in
+ *                                   registers; 1 = binary ladder with
+ *                                   selects; 2 = 3-bit window, registers;
+ *                                   3 = 2-bit window, table in shared memory;
+ *                                   4 = 3-bit window, shared memory.
+ *                                   ctas_per_sm = 0 selects a flat grid.
  *                 mont_mul_twiddle_ex : 0 = bulk-copy (TMA) staged table,
  *                                   1 = table read through L1/L2 (no smem)
  *   chunk     : mont_mul_twiddle_ex only: table columns staged per CTA
@@ -62,12 +68,14 @@ mont_status_t synth_fill(uint32_t *out, size_t n, uint64_t seed, uint32_t stream
  * mb_triad: c[i] = a[i] ^ b[i] over n uint32 with the same launch shape as
  *   mont_mul_vec: 12 bytes per element, the achievable 2-read/1-write HBM rate.
  * mb_copy: out[i] = in[i], 8 bytes per element.
- * mb_imad: every thread runs `iters` trips of 8 independent dependency chains
- *   of one integer-multiply instruction kind (0 = IMAD mul.lo, 1 = IMAD.HI
- *   mul.hi, 2 = IMAD.WIDE mul.wide, 3 = one signed Montgomery product:
- *   mul.lo, mul.hi, mul.lo, mul.hi, sub), writing one word per thread to
- *   sink[]; the caller times it and divides the executed count by time.
- *   grid = SMs * ctas_per_sm (cfg may be NULL). */
+ * mb_imad: every thread runs `iters` trips of 8 ops on each of 8 independent
+ *   dependency chains of one kind (0 = IMAD mul.lo, 1 = IMAD.HI mul.hi,
+ *   2 = IMAD.WIDE mad.wide, 3 = the library's signed chain REDC, 4 = its
+ *   canonical REDC, 5 = REDC from mul.lo/mul.hi, 6 = REDC with an IMAD.HI
+ *   64-bit addend), writing one word per thread to sink[] (which must hold
+ *   SMs * ctas_per_sm * 256 words); the caller times it and divides the
+ *   executed count (threads * iters * 64) by the time.
+ *   grid = SMs * ctas_per_sm, 256 threads (cfg may be NULL: 8 CTAs/SM). */
 mont_status_t mb_triad(uint32_t *c, const uint32_t *a, const uint32_t *b, size_t n,
                        const mont_launch_t *cfg, cudaStream_t stream);
 mont_status_t mb_copy(uint32_t *out, const uint32_t *in, size_t n, const mont_launch_t *cfg,

@@ -9,7 +9,7 @@
 
 namespace mont {
 
-inline Ctx to_dev(const mont_ctx_t *c) { return Ctx{c->p, c->pneg, c->r1, c->r2}; }
+inline Ctx to_dev(const mont_ctx_t *c) { return Ctx{c->p, 0u - c->pneg, c->r1, c->r2}; }
 
 // a context is usable if it came from mont_ctx_init: odd p in [3, 2^31) and
 // p * pneg = -1 (mod 2^32).  Cheap, catches uninitialised structs.

@@ -21,16 +21,16 @@
 namespace mont {
 
 struct OpMul {
-    uint32_t p, pneg;
-    __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return redc(a, b, p, pneg); }
+    uint32_t p, pinv;
+    __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return redc(a, b, p, pinv); }
 };
 struct OpTo {
-    uint32_t p, pneg, r2;
-    __device__ __forceinline__ uint32_t operator()(uint32_t x) const { return redc(x, r2, p, pneg); }
+    uint32_t p, pinv, r2;
+    __device__ __forceinline__ uint32_t operator()(uint32_t x) const { return redc(x, r2, p, pinv); }
 };
 struct OpFrom {
-    uint32_t p, pneg;
-    __device__ __forceinline__ uint32_t operator()(uint32_t x) const { return redc1(x, p, pneg); }
+    uint32_t p, pinv;
+    __device__ __forceinline__ uint32_t operator()(uint32_t x) const { return redc1(x, p, pinv); }
 };
 struct OpXor {  // triad microbenchmark: no modular math
     __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a ^ b; }
@@ -192,7 +192,7 @@ static mont_status_t launch_map2(const Op &op, uint32_t *c, const uint32_t *a, c
     const int sms = sm_count();
     if (sms <= 0) return MONT_ECUDA;
     const uintptr_t pa = (uintptr_t)a, pb = (uintptr_t)b, pc = (uintptr_t)c;
-    const bool flat = L.variant == 1;
+    const bool flat = L.variant == 0;
     if (same_mod16(pa, pb) && same_mod16(pa, pc)) {
         const uint32_t head = head_elems(pa, n);
         const size_t n4 = (n - head) / 4;
@@ -235,7 +235,7 @@ static mont_status_t launch_map1(const Op &op, uint32_t *out, const uint32_t *in
         const size_t n4 = (n - head) / 4;
         const uint32_t tail = (uint32_t)((n - head) % 4);
         const size_t tile = (size_t)L.unroll * L.threads;
-        size_t grid = L.variant == 1 ? (n4 + tile - 1) / tile : (size_t)sms * L.ctas_per_sm;
+        size_t grid = L.variant == 0 ? (n4 + tile - 1) / tile : (size_t)sms * L.ctas_per_sm;
         const size_t need = (n4 + tile - 1) / tile;
         if (grid > need) grid = need;
         if (grid == 0) grid = 1;
@@ -261,9 +261,12 @@ static mont_status_t launch_map1(const Op &op, uint32_t *out, const uint32_t *in
     return launch_status();
 }
 
-// defaults chosen by the sweep recorded in DESIGN.md §6
-static const Launch kMulVecDefault{512, 4, 4, 0, 0};
-static const Launch kMap1Default{512, 4, 4, 0, 0};
+// Defaults from the B200 sweep recorded in DESIGN.md §6: a flat grid (variant
+// 0, one tile of `threads` uint4 per CTA, ~65k CTAs at 2^26) beats every
+// persistent grid-stride shape by ~10 % -- the block scheduler balances the
+// slow and fast SMs dynamically, a static round-robin deal does not.
+static const Launch kMulVecDefault{256, 4, 1, 0, 0};
+static const Launch kMap1Default{256, 4, 1, 0, 0};
 
 }  // namespace mont
 
@@ -276,7 +279,7 @@ extern "C" mont_status_t mont_mul_vec_ex(const mont_ctx_t *ctx, uint32_t *c, con
     if (!a || !b || !c || ((uintptr_t)a | (uintptr_t)b | (uintptr_t)c) & 3u) return MONT_EINVAL_ARG;
     const Launch L = resolve(cfg, kMulVecDefault);
     if (!launch_ok(L)) return MONT_EINVAL_ARG;
-    return launch_map2(OpMul{ctx->p, ctx->pneg}, c, a, b, n, L, stream);
+    return launch_map2(OpMul{ctx->p, 0u - ctx->pneg}, c, a, b, n, L, stream);
 }
 
 extern "C" mont_status_t mont_mul_vec(const mont_ctx_t *ctx, uint32_t *c, const uint32_t *a, const uint32_t *b,
@@ -289,7 +292,7 @@ extern "C" mont_status_t to_mont(const mont_ctx_t *ctx, uint32_t *out, const uin
     if (!ctx_ok(ctx)) return ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
     if (n == 0) return MONT_OK;
     if (!in || !out || ((uintptr_t)in | (uintptr_t)out) & 3u) return MONT_EINVAL_ARG;
-    return launch_map1(OpTo{ctx->p, ctx->pneg, ctx->r2}, out, in, n, kMap1Default, stream);
+    return launch_map1(OpTo{ctx->p, 0u - ctx->pneg, ctx->r2}, out, in, n, kMap1Default, stream);
 }
 
 extern "C" mont_status_t from_mont(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *in, size_t n,
@@ -297,7 +300,7 @@ extern "C" mont_status_t from_mont(const mont_ctx_t *ctx, uint32_t *out, const u
     if (!ctx_ok(ctx)) return ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
     if (n == 0) return MONT_OK;
     if (!in || !out || ((uintptr_t)in | (uintptr_t)out) & 3u) return MONT_EINVAL_ARG;
-    return launch_map1(OpFrom{ctx->p, ctx->pneg}, out, in, n, kMap1Default, stream);
+    return launch_map1(OpFrom{ctx->p, 0u - ctx->pneg}, out, in, n, kMap1Default, stream);
 }
 
 extern "C" mont_status_t mont_checksum(const mont_ctx_t *ctx, unsigned long long *acc, const uint32_t *x, size_t n,
@@ -310,12 +313,11 @@ extern "C" mont_status_t mont_checksum(const mont_ctx_t *ctx, unsigned long long
     const uint32_t head = head_elems((uintptr_t)x, n);
     const size_t n4 = (n - head) / 4;
     const uint32_t tail = (uint32_t)((n - head) % 4);
-    const int threads = 512;
+    const int threads = 256;
     const size_t tile = 4 * (size_t)threads;
-    size_t grid = (size_t)sms * 4;
-    const size_t need = (n4 + tile - 1) / tile;
-    if (grid > need) grid = need;
+    size_t grid = (n4 + tile - 1) / tile;  // flat grid
     if (grid == 0) grid = 1;
+    if (grid > 0x7fffffff) grid = 0x7fffffff;
     k_sum<4><<<(unsigned)grid, threads, 0, stream>>>(acc, x, head, n4, tail);
     return launch_status();
 }

@@ -19,13 +19,13 @@ __device__ __forceinline__ void op(uint32_t &x, uint64_t &w, uint32_t c, int32_t
     } else if (KIND == 2) {
         asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(w) : "r"(x), "r"(c));
     } else if (KIND == 3) {
-        x = (uint32_t)sredc_hl((int32_t)x, (int32_t)x, p, pinv);
+        x = (uint32_t)sredc((int32_t)x, (int32_t)x, p, pinv);           // library chain form
     } else if (KIND == 4) {
-        x = redc_hl(x, x, (uint32_t)p, 0u - (uint32_t)pinv);
+        x = redc(x, x, (uint32_t)p, (uint32_t)pinv);                    // library canonical form
     } else if (KIND == 5) {
-        x = (uint32_t)sredc((int32_t)x, (int32_t)x, -p, pinv);
+        x = (uint32_t)sredc_mulhi((int32_t)x, (int32_t)x, p, pinv);     // mul.hi reference
     } else {
-        x = redc(x, x, (uint32_t)p, 0u - (uint32_t)pinv);
+        x = (uint32_t)sredc_hiadd((int32_t)x, (int32_t)x, -p, pinv);    // IMAD.HI 64-bit addend
     }
 }
 

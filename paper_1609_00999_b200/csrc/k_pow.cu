@@ -25,131 +25,125 @@
 namespace mont {
 
 struct PowParams {
-    int32_t p, negp, pinv;  // negp = -P, pinv = P^-1 mod 2^32 = -pneg
-    uint32_t pneg, r1, r2;
+    int32_t p, pinv;  // pinv = P^-1 mod 2^32 = -pneg
+    uint32_t r1, r2;
 };
 
-// ---- one lane's ladder, written for L lanes in lock-step so the compiler
-// interleaves the L independent dependency chains.
-template <int L>
-__device__ __forceinline__ void pow_window2(const PowParams &q, const uint32_t (&base)[L], const uint32_t (&e)[L],
-                                            uint32_t (&out)[L]) {
-    int32_t t1[L], t2[L], t3[L], acc[L];
-    const int32_t one = (int32_t)q.r1;
+// x-bar = to_mont(base) = REDC(base, R^2 mod P): canonical, valid for any uint32 base
+__device__ __forceinline__ int32_t pow_entry(const PowParams &q, uint32_t base) {
+    return (int32_t)redc(base, q.r2, (uint32_t)q.p, (uint32_t)q.pinv);
+}
+// out = from_mont(acc) canonical
+__device__ __forceinline__ uint32_t pow_exit(const PowParams &q, int32_t acc) {
+    return canon(sredc1(acc, q.p, q.pinv), q.p);
+}
+
+// ---- W-bit fixed-window ladder over the 32 exponent bits, L lanes in
+// lock-step (the compiler interleaves the L independent chains).  The first
+// window takes the top (32 mod W, or W) bits and needs no squaring.  Table
+// x^0..x^(2^W - 1) in Montgomery form, held in registers (multiplier picked by
+// a select tree on the ALU pipe) or, with SMEM, in a per-thread slice of
+// shared memory (one LDS per window on the LSU pipe).
+template <int W, int L, bool SMEM>
+__device__ __forceinline__ void pow_window(const PowParams &q, const uint32_t (&base)[L], const uint32_t (&e)[L],
+                                           uint32_t (&out)[L], int32_t *s_tab) {
+    constexpr int K = 1 << W;
+    constexpr int TOP = (32 % W) ? (32 % W) : W;  // bits in the first window
+    int32_t t[L][SMEM ? 2 : K], acc[L];
+    const uint32_t bd = blockDim.x;
 #pragma unroll
     for (int l = 0; l < L; ++l) {
-        t1[l] = (int32_t)redc(base[l], q.r2, (uint32_t)q.p, q.pneg);  // x-bar, canonical
-        t2[l] = sredc(t1[l], t1[l], q.negp, q.pinv);
-        t3[l] = sredc(t2[l], t1[l], q.negp, q.pinv);
-        const uint32_t d = e[l] >> 30;
-        acc[l] = d == 0 ? one : d == 1 ? t1[l] : d == 2 ? t2[l] : t3[l];
+        int32_t x = pow_entry(q, base[l]);
+        int32_t prev = (int32_t)q.r1;
+        int32_t first = prev;
+        const uint32_t d0 = e[l] >> (32 - TOP);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int32_t v = k == 0 ? (int32_t)q.r1 : k == 1 ? x : sredc(prev, x, q.p, q.pinv);
+            if (SMEM) s_tab[(k * L + l) * bd + threadIdx.x] = v;
+            else t[l][k] = v;
+            if (k < (1 << TOP)) first = (d0 == (uint32_t)k) ? v : first;
+            prev = v;
+        }
+        acc[l] = first;
     }
-#pragma unroll 1
-    for (int sh = 28; sh >= 0; sh -= 2) {
+#pragma unroll
+    for (int sh = 32 - TOP - W; sh >= 0; sh -= W) {
 #pragma unroll
         for (int l = 0; l < L; ++l) {
-            int32_t a = sredc(acc[l], acc[l], q.negp, q.pinv);
-            a = sredc(a, a, q.negp, q.pinv);
-            const uint32_t d = (e[l] >> sh) & 3u;
-            const int32_t lo = (d & 1u) ? t1[l] : one;
-            const int32_t hi = (d & 1u) ? t3[l] : t2[l];
-            acc[l] = sredc(a, (d & 2u) ? hi : lo, q.negp, q.pinv);
+            int32_t a = acc[l];
+#pragma unroll
+            for (int r = 0; r < W; ++r) a = sredc(a, a, q.p, q.pinv);
+            const uint32_t d = (e[l] >> sh) & (uint32_t)(K - 1);
+            int32_t mlt;
+            if (SMEM) {
+                mlt = s_tab[(d * L + l) * bd + threadIdx.x];
+            } else if (W == 2) {
+                const int32_t lo = (d & 1u) ? t[l][1] : t[l][0];
+                const int32_t hi = (d & 1u) ? t[l][3] : t[l][2];
+                mlt = (d & 2u) ? hi : lo;
+            } else {
+                int32_t cur = t[l][0];
+#pragma unroll
+                for (int k = 1; k < K; ++k) cur = (d == (uint32_t)k) ? t[l][k] : cur;
+                mlt = cur;
+            }
+            acc[l] = sredc(a, mlt, q.p, q.pinv);
         }
     }
 #pragma unroll
-    for (int l = 0; l < L; ++l) {
-        // from_mont: REDC(acc * 1) in signed form, then canonicalise
-        out[l] = canon(sredc1(acc[l], q.negp, q.pinv), q.p);
-    }
+    for (int l = 0; l < L; ++l) out[l] = pow_exit(q, acc[l]);
 }
 
-template <int L>
-__device__ __forceinline__ void pow_window3(const PowParams &q, const uint32_t (&base)[L], const uint32_t (&e)[L],
-                                            uint32_t (&out)[L]) {
-    int32_t t[L][8], acc[L];
-#pragma unroll
-    for (int l = 0; l < L; ++l) {
-        t[l][0] = (int32_t)q.r1;
-        t[l][1] = (int32_t)redc(base[l], q.r2, (uint32_t)q.p, q.pneg);
-#pragma unroll
-        for (int k = 2; k < 8; ++k) t[l][k] = sredc(t[l][k - 1], t[l][1], q.negp, q.pinv);
-        const uint32_t d = e[l] >> 30;  // top 2 bits
-        const int32_t s01 = (d & 1u) ? t[l][1] : t[l][0];
-        const int32_t s23 = (d & 1u) ? t[l][3] : t[l][2];
-        acc[l] = (d & 2u) ? s23 : s01;
-    }
-#pragma unroll 1
-    for (int sh = 27; sh >= 0; sh -= 3) {
-#pragma unroll
-        for (int l = 0; l < L; ++l) {
-            int32_t a = sredc(acc[l], acc[l], q.negp, q.pinv);
-            a = sredc(a, a, q.negp, q.pinv);
-            a = sredc(a, a, q.negp, q.pinv);
-            const uint32_t d = (e[l] >> sh) & 7u;
-            const bool b0 = d & 1u, b1 = d & 2u, b2 = d & 4u;
-            const int32_t s01 = b0 ? t[l][1] : t[l][0];
-            const int32_t s23 = b0 ? t[l][3] : t[l][2];
-            const int32_t s45 = b0 ? t[l][5] : t[l][4];
-            const int32_t s67 = b0 ? t[l][7] : t[l][6];
-            const int32_t s03 = b1 ? s23 : s01;
-            const int32_t s47 = b1 ? s67 : s45;
-            acc[l] = sredc(a, b2 ? s47 : s03, q.negp, q.pinv);
-        }
-    }
-#pragma unroll
-    for (int l = 0; l < L; ++l) {
-        out[l] = canon(sredc1(acc[l], q.negp, q.pinv), q.p);
-    }
-}
-
+// binary ladder with selects: 32 squarings + 32 multiplies, reference point
 template <int L>
 __device__ __forceinline__ void pow_binary(const PowParams &q, const uint32_t (&base)[L], const uint32_t (&e)[L],
                                            uint32_t (&out)[L]) {
     int32_t x[L], acc[L];
 #pragma unroll
     for (int l = 0; l < L; ++l) {
-        x[l] = (int32_t)redc(base[l], q.r2, (uint32_t)q.p, q.pneg);
+        x[l] = pow_entry(q, base[l]);
         acc[l] = (int32_t)q.r1;
     }
-#pragma unroll 1
+#pragma unroll 4
     for (int sh = 31; sh >= 0; --sh) {
 #pragma unroll
         for (int l = 0; l < L; ++l) {
-            int32_t a = sredc(acc[l], acc[l], q.negp, q.pinv);
-            int32_t m = sredc(a, x[l], q.negp, q.pinv);
-            acc[l] = ((e[l] >> sh) & 1u) ? m : a;
+            const int32_t a = sredc(acc[l], acc[l], q.p, q.pinv);
+            const int32_t mm = sredc(a, x[l], q.p, q.pinv);
+            acc[l] = ((e[l] >> sh) & 1u) ? mm : a;
         }
     }
 #pragma unroll
-    for (int l = 0; l < L; ++l) {
-        out[l] = canon(sredc1(acc[l], q.negp, q.pinv), q.p);
-    }
+    for (int l = 0; l < L; ++l) out[l] = pow_exit(q, acc[l]);
+}
+
+// variant: 0 = 2-bit window, registers; 1 = binary; 2 = 3-bit window, registers;
+//          3 = 2-bit window, smem table; 4 = 3-bit window, smem table
+template <int V, int L>
+__device__ __forceinline__ void pow_lanes(const PowParams &q, const uint32_t (&b)[L], const uint32_t (&e)[L],
+                                          uint32_t (&o)[L], int32_t *s_tab) {
+    if (V == 0) pow_window<2, L, false>(q, b, e, o, s_tab);
+    else if (V == 1) pow_binary<L>(q, b, e, o);
+    else if (V == 2) pow_window<3, L, false>(q, b, e, o, s_tab);
+    else if (V == 3) pow_window<2, L, true>(q, b, e, o, s_tab);
+    else pow_window<3, L, true>(q, b, e, o, s_tab);
 }
 
 template <int V>
-__device__ __forceinline__ void pow_lanes(const PowParams &q, const uint32_t (&b)[4], const uint32_t (&e)[4],
-                                          uint32_t (&o)[4]) {
-    if (V == 0) pow_window2<4>(q, b, e, o);
-    else if (V == 1) pow_binary<4>(q, b, e, o);
-    else pow_window3<4>(q, b, e, o);
-}
+constexpr int pow_smem_words() { return V == 3 ? 4 * 4 : V == 4 ? 8 * 4 : 0; }  // per thread, 4 lanes
 
-template <int V>
-__device__ __forceinline__ uint32_t pow_one(const PowParams &q, uint32_t b, uint32_t e) {
-    uint32_t bb[1] = {b}, ee[1] = {e}, oo[1];
-    if (V == 0) pow_window2<1>(q, bb, ee, oo);
-    else if (V == 1) pow_binary<1>(q, bb, ee, oo);
-    else pow_window3<1>(q, bb, ee, oo);
-    return oo[0];
-}
-
-// head/tail scalars by CTA 0; vector body over n4 uint4 chunks (grid-stride)
+// Vector body over n4 uint4 chunks; head/tail scalars by CTA 0 (1 lane each,
+// using the same table slice layout with L = 4 so the smem footprint matches).
 template <int V>
 __global__ void __launch_bounds__(256) k_pow(PowParams q, uint32_t *out, const uint32_t *base, const uint32_t *exp,
                                               uint32_t head, size_t n4, uint32_t tail) {
+    extern __shared__ int32_t s_tab[];
     if (blockIdx.x == 0 && threadIdx.x < head + tail) {
         size_t i = threadIdx.x < head ? threadIdx.x : head + 4 * n4 + (threadIdx.x - head);
-        out[i] = pow_one<V>(q, base[i], exp[i]);
+        uint32_t b[4] = {base[i], 0u, 0u, 0u}, e[4] = {exp[i], 0u, 0u, 0u}, o[4];
+        pow_lanes<V, 4>(q, b, e, o, s_tab);
+        out[i] = o[0];
     }
     const uint4 *b4 = reinterpret_cast<const uint4 *>(base + head);
     const uint4 *e4 = reinterpret_cast<const uint4 *>(exp + head);
@@ -157,7 +151,7 @@ __global__ void __launch_bounds__(256) k_pow(PowParams q, uint32_t *out, const u
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
         const uint4 bv = ld_stream(b4 + i), ev = ld_stream(e4 + i);
         uint32_t b[4] = {bv.x, bv.y, bv.z, bv.w}, e[4] = {ev.x, ev.y, ev.z, ev.w}, o[4];
-        pow_lanes<V>(q, b, e, o);
+        pow_lanes<V, 4>(q, b, e, o, s_tab);
         st_stream(o4 + i, make_uint4(o[0], o[1], o[2], o[3]));
     }
 }
@@ -165,25 +159,56 @@ __global__ void __launch_bounds__(256) k_pow(PowParams q, uint32_t *out, const u
 template <int V>
 __global__ void __launch_bounds__(256) k_pow_scalar(PowParams q, uint32_t *out, const uint32_t *base,
                                                      const uint32_t *exp, size_t n) {
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        out[i] = pow_one<V>(q, base[i], exp[i]);
+    extern __shared__ int32_t s_tab[];
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        uint32_t b[4] = {base[i], 0u, 0u, 0u}, e[4] = {exp[i], 0u, 0u, 0u}, o[4];
+        pow_lanes<V, 4>(q, b, e, o, s_tab);
+        out[i] = o[0];
+    }
 }
 
 // tw[j] = to_mont(w^j): binary ladder on the bits of j, canonical output
 __global__ void __launch_bounds__(256) k_twiddle_table(Ctx c, uint32_t *tw, uint32_t w, size_t len) {
     for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += (size_t)gridDim.x * blockDim.x) {
-        const uint32_t x = redc(w, c.r2, c.p, c.pneg);
+        const uint32_t x = redc(w, c.r2, c.p, c.pinv);
         uint32_t acc = c.r1;
         unsigned long long e = j;
         for (int sh = 63 - __clzll(e | 1ull); sh >= 0; --sh) {
-            acc = redc(acc, acc, c.p, c.pneg);
-            if ((e >> sh) & 1ull) acc = redc(acc, x, c.p, c.pneg);
+            acc = redc(acc, acc, c.p, c.pinv);
+            if ((e >> sh) & 1ull) acc = redc(acc, x, c.p, c.pinv);
         }
         tw[j] = acc;
     }
 }
 
-static const Launch kPowDefault{256, 8, 1, 0, 0};
+template <int V>
+static mont_status_t launch_pow(const PowParams &q, uint32_t *out, const uint32_t *base, const uint32_t *exp,
+                                size_t n, int ctas_per_sm, int sms, cudaStream_t stream) {
+    const int threads = 256;
+    const size_t smem = (size_t)pow_smem_words<V>() * threads * 4;
+    const uintptr_t pb = (uintptr_t)base, pe = (uintptr_t)exp, po = (uintptr_t)out;
+    if (same_mod16(pb, pe) && same_mod16(pb, po)) {
+        const uint32_t head = head_elems(pb, n);
+        const size_t n4 = (n - head) / 4;
+        const uint32_t tail = (uint32_t)((n - head) % 4);
+        const size_t need = (n4 + threads - 1) / threads;
+        size_t grid = ctas_per_sm > 0 ? (size_t)sms * ctas_per_sm : need;  // 0 = flat grid
+        if (grid > need) grid = need;
+        if (grid == 0) grid = 1;
+        if (grid > 0x7fffffff) grid = 0x7fffffff;
+        k_pow<V><<<(unsigned)grid, threads, smem, stream>>>(q, out, base, exp, head, n4, tail);
+    } else {
+        const size_t need = (n + threads - 1) / threads;
+        size_t grid = ctas_per_sm > 0 ? (size_t)sms * ctas_per_sm : need;
+        if (grid > need) grid = need;
+        if (grid > 0x7fffffff) grid = 0x7fffffff;
+        k_pow_scalar<V><<<(unsigned)grid, threads, smem, stream>>>(q, out, base, exp, n);
+    }
+    return launch_status();
+}
+
+// ctas_per_sm = 0: flat grid (one uint4 of work per thread)
+static const Launch kPowDefault{256, 0, 1, 0, 0};
 
 }  // namespace mont
 
@@ -196,36 +221,17 @@ extern "C" mont_status_t mont_pow_vec_ex(const mont_ctx_t *ctx, uint32_t *out, c
     if (n == 0) return MONT_OK;
     if (!out || !base || !exp || ((uintptr_t)out | (uintptr_t)base | (uintptr_t)exp) & 3u) return MONT_EINVAL_ARG;
     Launch L = resolve(cfg, kPowDefault);
-    if (L.threads != 256 || L.variant < 0 || L.variant > 2) return MONT_EINVAL_ARG;
+    if (L.threads != 256 || L.variant < 0 || L.variant > 4 || L.ctas_per_sm < 0) return MONT_EINVAL_ARG;
     const int sms = sm_count();
     if (sms <= 0) return MONT_ECUDA;
-    PowParams q{(int32_t)ctx->p, -(int32_t)ctx->p, (int32_t)(0u - ctx->pneg), ctx->pneg, ctx->r1, ctx->r2};
-    const uintptr_t pb = (uintptr_t)base, pe = (uintptr_t)exp, po = (uintptr_t)out;
-    const int threads = 256;
-    if (same_mod16(pb, pe) && same_mod16(pb, po)) {
-        const uint32_t head = head_elems(pb, n);
-        const size_t n4 = (n - head) / 4;
-        const uint32_t tail = (uint32_t)((n - head) % 4);
-        size_t grid = (size_t)sms * L.ctas_per_sm;
-        const size_t need = (n4 + threads - 1) / threads;
-        if (grid > need) grid = need;
-        if (grid == 0) grid = 1;
-        switch (L.variant) {
-            case 0: k_pow<0><<<(unsigned)grid, threads, 0, stream>>>(q, out, base, exp, head, n4, tail); break;
-            case 1: k_pow<1><<<(unsigned)grid, threads, 0, stream>>>(q, out, base, exp, head, n4, tail); break;
-            default: k_pow<2><<<(unsigned)grid, threads, 0, stream>>>(q, out, base, exp, head, n4, tail); break;
-        }
-    } else {
-        size_t grid = (size_t)sms * L.ctas_per_sm;
-        const size_t need = (n + threads - 1) / threads;
-        if (grid > need) grid = need;
-        switch (L.variant) {
-            case 0: k_pow_scalar<0><<<(unsigned)grid, threads, 0, stream>>>(q, out, base, exp, n); break;
-            case 1: k_pow_scalar<1><<<(unsigned)grid, threads, 0, stream>>>(q, out, base, exp, n); break;
-            default: k_pow_scalar<2><<<(unsigned)grid, threads, 0, stream>>>(q, out, base, exp, n); break;
-        }
+    const PowParams q{(int32_t)ctx->p, (int32_t)(0u - ctx->pneg), ctx->r1, ctx->r2};
+    switch (L.variant) {
+        case 0: return launch_pow<0>(q, out, base, exp, n, L.ctas_per_sm, sms, stream);
+        case 1: return launch_pow<1>(q, out, base, exp, n, L.ctas_per_sm, sms, stream);
+        case 2: return launch_pow<2>(q, out, base, exp, n, L.ctas_per_sm, sms, stream);
+        case 3: return launch_pow<3>(q, out, base, exp, n, L.ctas_per_sm, sms, stream);
+        default: return launch_pow<4>(q, out, base, exp, n, L.ctas_per_sm, sms, stream);
     }
-    return launch_status();
 }
 
 extern "C" mont_status_t mont_pow_vec(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *base,

@@ -54,9 +54,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
     } while (!done);
 }
 
-__device__ __forceinline__ uint4 redc4(const uint4 &x, const uint4 &t, uint32_t p, uint32_t pneg) {
-    return make_uint4(redc(x.x, t.x, p, pneg), redc(x.y, t.y, p, pneg), redc(x.z, t.z, p, pneg),
-                      redc(x.w, t.w, p, pneg));
+__device__ __forceinline__ uint4 redc4(const uint4 &x, const uint4 &t, uint32_t p, uint32_t pinv) {
+    return make_uint4(redc(x.x, t.x, p, pinv), redc(x.y, t.y, p, pinv), redc(x.z, t.z, p, pinv),
+                      redc(x.w, t.w, p, pinv));
 }
 
 // Vector path: len % 4 == 0, x/out/tw 16-byte aligned.  TMA = stage the table
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(512) k_twiddle(Ctx c, uint32_t *out, const uin
         for (int k = 0; k < U; ++k) {
             if (ok[k]) {
                 const uint4 t = TMA ? s_tw[cc[k]] : __ldg(t4 + cc[k]);
-                st_stream(o4 + idx[k], redc4(v[k], t, c.p, c.pneg));
+                st_stream(o4 + idx[k], redc4(v[k], t, c.p, c.pinv));
             }
         }
     }
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(256) k_twiddle_scalar(Ctx c, uint32_t *out, co
         const uint32_t *xr = x + r * len;
         uint32_t *orow = out + r * len;
         for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += (size_t)gridDim.x * blockDim.x)
-            st_stream1(orow + j, redc(ld_stream1(xr + j), __ldg(tw + j), c.p, c.pneg));
+            st_stream1(orow + j, redc(ld_stream1(xr + j), __ldg(tw + j), c.p, c.pinv));
     }
 }
 

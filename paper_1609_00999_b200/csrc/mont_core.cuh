@@ -29,8 +29,8 @@
 
 namespace mont {
 
-struct Ctx {  // mirrors mont_ctx_t (by value in kernel params)
-    uint32_t p, pneg, r1, r2;
+struct Ctx {  // device view of mont_ctx_t (by value in kernel params); pinv = -pneg
+    uint32_t p, pinv, r1, r2;
 };
 
 __device__ __forceinline__ uint32_t umin(uint32_t x, uint32_t y) { return x < y ? x : y; }
@@ -50,53 +50,63 @@ __device__ __forceinline__ int64_t mul_wide_s32(int32_t a, int32_t b) {
     asm("mul.wide.s32 %0, %1, %2;" : "=l"(r) : "r"(a), "r"(b));
     return r;
 }
+__device__ __forceinline__ uint32_t hi32(uint64_t x) { return (uint32_t)(x >> 32); }
+__device__ __forceinline__ int32_t hi32s(int64_t x) { return (int32_t)(x >> 32); }
 
-__device__ __forceinline__ uint32_t redc(uint32_t a, uint32_t b, uint32_t p, uint32_t pneg) {
-    const uint64_t T = mul_wide_u32(a, b);                       // IMAD.WIDE.U32
-    const uint32_t m = (uint32_t)T * pneg;                       // IMAD
-    const uint32_t t = (uint32_t)(((uint64_t)m * p + T) >> 32);  // IMAD.HI.U32, 64-bit addend
-    return umin(t, t - p);
+// Measured on B200 (scripts/probe.py): IMAD and IMAD.WIDE issue
+// at 64 lanes/clk/SM but IMAD.HI at only 32.  So the high halves are taken
+// from IMAD.WIDE results, never from mul.hi, and the REDC is written in the
+// "subtract" form, which needs no carry:
+//   T = a b (IMAD.WIDE);  m = lo(T) P^-1 mod 2^32 (IMAD);  M = m P (IMAD.WIDE)
+//   lo(M) = lo(T) exactly, so (T - M) / 2^32 = hi(T) - hi(M)  (IADD3), in (-P, P)
+// = 3 full-rate FMAHeavy ops + 1 ALU op.  It is Alg. 2 with m' = -m:
+// t' = (T - m'P)/R = (T + mP)/R - P, i.e. the paper's t shifted by -P, so the
+// final "if t >= P then t - P" becomes "if t' < 0 then t' + P".
+// pinv = P^-1 mod 2^32 = -P' (reading G2).
+
+// canonical REDC: a*b < 2^32 P required; returns [0, P).  2 ALU ops
+// (IADD3 + VIADDMNMX for the sign fix-up).
+__device__ __forceinline__ uint32_t redc(uint32_t a, uint32_t b, uint32_t p, uint32_t pinv) {
+    const uint64_t T = mul_wide_u32(a, b);
+    const uint32_t m = (uint32_t)T * pinv;
+    const uint64_t M = mul_wide_u32(m, p);
+    const uint32_t t = hi32(T) - hi32(M);  // in (-P, P) as a signed value
+    return umin(t, t + p);                 // t < 0 (wrapped) -> t + P
 }
 
-// "hi/lo" form with mul.lo / mul.hi only (kept for the microbenchmark and as
-// the literal reading of the three multiplications): 4 FMAHeavy ops.
-__device__ __forceinline__ uint32_t redc_hl(uint32_t a, uint32_t b, uint32_t p, uint32_t pneg) {
-    uint32_t lo = a * b;
-    uint32_t hi = __umulhi(a, b);
-    uint32_t m = lo * pneg;
-    uint32_t t = __umulhi(m, p) + hi + (lo != 0u ? 1u : 0u);
-    return umin(t, t - p);
+// REDC(x * 1) = x R^-1 mod P (A10): T = x, hi(T) = 0
+__device__ __forceinline__ uint32_t redc1(uint32_t x, uint32_t p, uint32_t pinv) {
+    const uint32_t m = x * pinv;
+    const uint32_t t = 0u - hi32(mul_wide_u32(m, p));
+    return umin(t, t + p);
 }
 
-// REDC(x * 1) = x R^-1 mod P: T = x, so only m and (x + m P) >> 32 (A10)
-__device__ __forceinline__ uint32_t redc1(uint32_t x, uint32_t p, uint32_t pneg) {
-    const uint32_t m = x * pneg;
-    const uint32_t t = (uint32_t)(((uint64_t)m * p + x) >> 32);
-    return umin(t, t - p);
+// signed lazy form for chains: |a|, |b| < P  ->  result in (-P, P),
+// congruent to a b R^-1 (mod P).  |T - M| < 2^31 P + 2^31 P, so |t| < P.
+__device__ __forceinline__ int32_t sredc(int32_t a, int32_t b, int32_t p, int32_t pinv) {
+    const int64_t T = mul_wide_s32(a, b);
+    const int32_t m = (int32_t)T * pinv;
+    return hi32s(T) - hi32s(mul_wide_s32(m, p));
 }
 
-// signed lazy form: |a|,|b| < P  ->  result in (-P, P), congruent to a b R^-1.
-// negp = -P, pinv = P^-1 mod 2^32.  T - m P = 0 (mod 2^32) exactly, so the
-// arithmetic shift of the IMAD.WIDE result is the exact division by R.
-// 3 FMAHeavy ops, no ALU op.
-__device__ __forceinline__ int32_t sredc(int32_t a, int32_t b, int32_t negp, int32_t pinv) {
-    const int64_t T = mul_wide_s32(a, b);                       // IMAD.WIDE
-    const int32_t m = (int32_t)T * pinv;                        // IMAD
-    return (int32_t)(((int64_t)m * negp + T) >> 32);            // IMAD.HI, 64-bit addend
+// signed REDC(x * 1) for |x| < P -> (-P, P)
+__device__ __forceinline__ int32_t sredc1(int32_t x, int32_t p, int32_t pinv) {
+    const int32_t m = x * pinv;
+    return (x >> 31) - hi32s(mul_wide_s32(m, p));
 }
 
-// signed hi/lo form (4 FMAHeavy ops + 1 ALU op), microbenchmark reference
-__device__ __forceinline__ int32_t sredc_hl(int32_t a, int32_t b, int32_t p, int32_t pinv) {
+// Reference forms kept for the K8 microbenchmark only (k_micro.cu):
+// mul.hi-based (IMAD.HI, half rate) and the IMAD.HI-with-64-bit-addend form.
+__device__ __forceinline__ int32_t sredc_mulhi(int32_t a, int32_t b, int32_t p, int32_t pinv) {
     int32_t lo = a * b;
     int32_t hi = __mulhi(a, b);
     int32_t m = lo * pinv;
     return hi - __mulhi(m, p);
 }
-
-// signed REDC(x * 1) for |x| < P -> (-P, P)
-__device__ __forceinline__ int32_t sredc1(int32_t x, int32_t negp, int32_t pinv) {
-    const int32_t m = x * pinv;
-    return (int32_t)(((int64_t)m * negp + (int64_t)x) >> 32);
+__device__ __forceinline__ int32_t sredc_hiadd(int32_t a, int32_t b, int32_t negp, int32_t pinv) {
+    const int64_t T = mul_wide_s32(a, b);
+    const int32_t m = (int32_t)T * pinv;
+    return (int32_t)(((int64_t)m * negp + T) >> 32);
 }
 
 // (-P, P) -> [0, P)
