@@ -47,7 +47,7 @@ def lib():
 if args.what in ("all", "imad"):
     import ctypes as C
     sink = torch.empty(sms * 32 * 256, dtype=torch.uint32, device=dev)
-    names = {0: "IMAD", 1: "IMAD.HI", 2: "IMAD.WIDE", 3: "sredc_hl", 4: "redc_hl", 5: "sredc_wide", 6: "redc_wide"}
+    names = {0: "IMAD", 1: "IMAD.HI", 2: "IMAD.WIDE", 3: "sredc", 4: "redc", 5: "sredc_mulhi", 6: "sredc_hiadd"}
     for kind in range(7):
         for ctas in (4, 8):
             iters = 2000
@@ -72,11 +72,11 @@ if args.what in ("all", "hbm"):
     m.synth_fill(a, 42, 1, 0, 2013265921)
     m.synth_fill(b, 42, 2, 0, 2013265921)
     ctx = m.ctx_init(2013265921)
-    for threads in (256, 512):
-        for ctas in (2, 4, 8):
-            for unroll in (1, 2, 4, 8):
+    for threads in (128, 256, 512):
+        for ctas in (4, 8):
+            for unroll in (1, 2, 4):
                 for variant in (0, 1):
-                    if variant == 1 and ctas != 4:
+                    if variant == 0 and ctas != 4:
                         continue
                     cfg = m.Launch(threads=threads, ctas_per_sm=ctas, unroll=unroll, variant=variant)
                     med, best = timeit(lambda: lib().mb_triad(c.data_ptr(), a.data_ptr(), b.data_ptr(), n,
@@ -110,9 +110,9 @@ if args.what in ("all", "tw"):
     o = torch.empty_like(x)
     tw = m.twiddle_table(ctx, 1657000625, L)
     for variant in (0, 1):
-        for ctas in (1, 2, 3, 4):
-            for unroll in (2, 4, 8):
-                for chunk in (4096, 16384):
+        for ctas in (3, 8, 16, 32, 64):
+            for unroll in (1, 2, 4):
+                for chunk in (2048, 4096, 16384):
                     for threads in (256, 512):
                         cfg = m.Launch(threads=threads, ctas_per_sm=ctas, unroll=unroll, variant=variant,
                                        chunk=chunk)
@@ -137,8 +137,8 @@ if args.what in ("all", "pow"):
     pc = e.cpu().numpy()
     import numpy as np
     useful = int(31 * n + np.unpackbits(pc.view(np.uint8)).sum())
-    for variant in (0, 1, 2):
-        for ctas in (2, 4, 8, 16):
+    for variant in (0, 1, 2, 3, 4):
+        for ctas in (0, 8, 16):
             cfg = m.Launch(variant=variant, ctas_per_sm=ctas)
             med, best = timeit(lambda: m.pow_vec(ctx, base, e, out=o, cfg=cfg), reps=10)
             out(what="pow", variant=variant, ctas=ctas, us=med * 1e6, useful_mulmods=useful,
