@@ -33,7 +33,7 @@ extern "C" {
  *                 mont_mul_twiddle_ex : 0 = bulk-copy (TMA) staged table,
  *                                   1 = table read through L1/L2 (no smem)
  *   chunk     : mont_mul_twiddle_ex only: table columns staged per CTA
- *               (multiple of 4; 0 = min(len, 16384)).                       */
+ *               (multiple of 4; 0 = min(len, 4096)).                       */
 typedef struct mont_launch {
     int threads;
     int ctas_per_sm;

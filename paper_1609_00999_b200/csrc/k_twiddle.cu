@@ -140,7 +140,10 @@ __global__ void __launch_bounds__(256) k_twiddle_scalar(Ctx c, uint32_t *out, co
     }
 }
 
-static const Launch kTwDefault{512, 3, 4, 0, 16384};
+// B200 sweep: many small CTAs (target 64 per SM, a few rows each)
+// balance like a flat grid; a 4096-column (16 KiB) staged chunk keeps the
+// table re-read from L2 at 1/4 of the x stream per row block.
+static const Launch kTwDefault{256, 64, 4, 0, 4096};
 
 template <int U, bool TMA>
 static mont_status_t launch_tw(const Ctx &c, uint32_t *out, const uint32_t *x, const uint32_t *tw, size_t batch,
