@@ -176,8 +176,9 @@ class Workload:
             back = torch.empty(N_C2, **u32)
             self.outputs.append(back)
             self.abar, self.back = abar, back
-            L.append(("to_mont", lambda: m.to_mont(self.ctx[P0], a0, out=abar), 8 * N_C2, N_C2, "hbm"))
-            L.append(("from_mont", lambda: m.from_mont(self.ctx[P0], abar, out=back), 8 * N_C2, N_C2, "hbm"))
+            L.append(("to_mont", lambda a0=a0, abar=abar: m.to_mont(self.ctx[P0], a0, out=abar), 8 * N_C2, N_C2, "hbm"))
+            L.append(("from_mont", lambda abar=abar, back=back: m.from_mont(self.ctx[P0], abar, out=back), 8 * N_C2, N_C2,
+                      "hbm"))
         if kind in ("step", "c3"):
             x = torch.empty(TW_BATCH * TW_LEN, **u32)
             m.synth_fill(x, SEED, 5, rank * TW_BATCH * TW_LEN, P0, 0, False)
@@ -188,7 +189,7 @@ class Workload:
             self.tw_x, self.tw, self.tw_out, self.w = x, tw, o, w
             self.inputs += [x]
             self.outputs.append(o)
-            L.append(("mont_mul_twiddle", lambda: m.mul_twiddle(self.ctx[P0], x, tw, out=o),
+            L.append(("mont_mul_twiddle", lambda x=x, tw=tw, o=o: m.mul_twiddle(self.ctx[P0], x, tw, out=o),
                       8 * TW_BATCH * TW_LEN, TW_BATCH * TW_LEN, "hbm"))
             self.config.update({"c3_batch": TW_BATCH, "c3_len": TW_LEN})
         if kind in ("step", "c4"):
@@ -202,7 +203,8 @@ class Workload:
             self.pow_bufs = (base, e, o)
             self.inputs += [base, e]
             self.outputs.append(o)
-            L.append(("mont_pow_vec", lambda: m.pow_vec(self.ctx[P1], base, e, out=o), 12 * N_C4, ladder, "imad"))
+            L.append(("mont_pow_vec", lambda base=base, e=e, o=o: m.pow_vec(self.ctx[P1], base, e, out=o), 12 * N_C4,
+                      ladder, "imad"))
             self.config.update({"c4_n": N_C4, "c4_ladder_mulmods": ladder})
         if kind in ("step", "c2"):
             for si, P in enumerate(PRIMES):
@@ -221,8 +223,8 @@ class Workload:
             self.c5 = (a, b, c)
             self.inputs += [a, b]
             self.outputs.append(c)
-            L.append(("mont_mul_vec[c5]", lambda: m.mul_vec(self.ctx[P0], a, b, out=c), 12 * n, n, "hbm"))
-            L.append(("mont_checksum[c5]", lambda: m.checksum(self.ctx[P0], c, acc=self.acc[0:1]), 4 * n, 0, "hbm"))
+            L.append(("mont_mul_vec[c5]", lambda a=a, b=b, c=c: m.mul_vec(self.ctx[P0], a, b, out=c), 12 * n, n, "hbm"))
+            L.append(("mont_checksum[c5]", lambda c=c: m.checksum(self.ctx[P0], c, acc=self.acc[0:1]), 4 * n, 0, "hbm"))
             self.config.update({"c5_n_total": N_C5, "c5_n_rank": n})
         torch.cuda.synchronize()
 
