@@ -8,14 +8,15 @@ One "step" (default workload) is one pass of the whole hot path of
 SURVEY.md §8(a) (rows A1-A11) over one batch of synthetic input, per rank:
 
   A1   mont_ctx_init for the three config primes (host)
-  A7   mont_mul_vec   configs[1]: n = 2^26 pairs with 1 % specials, for each of
-                      P in {2013265921, 469762049, 998244353}      (3 launches)
+  A7   mont_mul_vec_checksum  configs[1]: n = 2^26 pairs with 1 % specials, for
+                      each of P in {2013265921, 469762049, 998244353}, with the
+                      A11 checksum partial fused into the same pass (3 launches)
   A2   to_mont        the P0 operand a (2^26)                      (1 launch)
   A10  from_mont      back again (2^26)                            (1 launch)
   A8   mont_mul_twiddle configs[2]: 4096 x 2^14 against tw[j] = to_mont(w^j)
   A9   mont_pow_vec   configs[3]: 2^24 bases/exponents, P = 469762049
-  A11  mont_checksum  sum of each C2 output (3 launches); the cross-rank
-                      NCCL all-reduce of the partials runs once, after timing
+  A11  the cross-rank NCCL all-reduce of the checksum partials runs once,
+                      after timing
 
 metric/unit are BASELINE.json's: useful Montgomery products per second
 (Gmulmod/s) of the whole job: C2 3*2^26 + to/from 2*2^26 + C3 2^26 + C4
@@ -167,7 +168,10 @@ class Workload:
                 self.c2[P] = (a, b, c)
                 self.inputs += [a, b]
                 self.outputs.append(c)
-                L.append((f"mont_mul_vec[P={P}]", (lambda ctx=self.ctx[P], a=a, b=b, c=c: m.mul_vec(ctx, a, b, out=c)),
+                # A7 + A11 fused: c = REDC(a, b) and the checksum partial in one pass
+                L.append((f"mont_mul_vec_checksum[P={P}]",
+                          (lambda ctx=self.ctx[P], a=a, b=b, c=c, si=si:
+                           m.mul_vec_checksum(ctx, a, b, out=c, acc=self.acc[si:si + 1])),
                           12 * N_C2, N_C2, "hbm"))
             self.config.update({"c2_n": N_C2, "c2_primes": list(PRIMES)})
         if kind == "step":
@@ -206,12 +210,6 @@ class Workload:
             L.append(("mont_pow_vec", lambda base=base, e=e, o=o: m.pow_vec(self.ctx[P1], base, e, out=o), 12 * N_C4,
                       ladder, "imad"))
             self.config.update({"c4_n": N_C4, "c4_ladder_mulmods": ladder})
-        if kind in ("step", "c2"):
-            for si, P in enumerate(PRIMES):
-                c = self.c2[P][2]
-                L.append((f"mont_checksum[P={P}]",
-                          (lambda ctx=self.ctx[P], c=c, si=si: m.checksum(ctx, c, acc=self.acc[si:si + 1])),
-                          4 * N_C2, 0, "hbm"))
         if kind == "c5":
             n = N_C5 // world
             lo = (rank * N_C5) // world
@@ -223,8 +221,9 @@ class Workload:
             self.c5 = (a, b, c)
             self.inputs += [a, b]
             self.outputs.append(c)
-            L.append(("mont_mul_vec[c5]", lambda a=a, b=b, c=c: m.mul_vec(self.ctx[P0], a, b, out=c), 12 * n, n, "hbm"))
-            L.append(("mont_checksum[c5]", lambda c=c: m.checksum(self.ctx[P0], c, acc=self.acc[0:1]), 4 * n, 0, "hbm"))
+            L.append(("mont_mul_vec_checksum[c5]",
+                      lambda a=a, b=b, c=c: m.mul_vec_checksum(self.ctx[P0], a, b, out=c, acc=self.acc[0:1]),
+                      12 * n, n, "hbm"))
             self.config.update({"c5_n_total": N_C5, "c5_n_rank": n})
         torch.cuda.synchronize()
 
@@ -500,7 +499,7 @@ def main():
     if wl.kind in ("step", "c2", "c5"):
         wl.acc.zero_()
         for name, fn, *_ in wl.launches:
-            if name.startswith("mont_checksum"):
+            if name.startswith("mont_mul_vec_checksum"):
                 fn()
         torch.cuda.synchronize()
         local = [int(v) for v in wl.acc.tolist()]
@@ -555,7 +554,7 @@ def main():
         "higher_is_better": True, "scaling": "weak" if wl.kind != "c5" else "strong",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded SplitMix64 counter generator, device-side)",
         "config": {"workload": {"step": "one pass of SURVEY §8(a) A1-A11: configs[1] mul_vec x3 primes + to/from_mont + "
-                                         "configs[2] twiddle + configs[3] pow + checksums",
+                                         "configs[2] twiddle + configs[3] pow (checksum fused into mul_vec)",
                                 "c2": "configs[1] mul_vec x3 primes + checksums", "c3": "configs[2] twiddle",
                                 "c4": "configs[3] pow", "c5": "configs[4] sharded mul_vec n=2^31 + checksum"}[wl.kind],
                    "parallelism": f"dp{world} (contiguous global-index slices, no data-path collective)",

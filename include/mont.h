@@ -6,9 +6,10 @@
  * Arithmetic.  R = 2^32 and P is an odd modulus 3 <= P < 2^31 (DESIGN.md
  * reading G16; primality is not required, REDC needs only gcd(R, P) = 1,
  * PAPER.md:89).  REDC(a, b) = a*b*R^-1 mod P, computed with the paper's three
- * integer multiplications (Alg. 2 at PAPER.md:95-99) as
- * mul.lo/mul.hi on the integer-multiply (FMAHeavy) pipe, and returned in the
- * canonical range [0, P).
+ * integer multiplications (Alg. 2 at PAPER.md:95-99) on the
+ * integer-multiply (FMAHeavy) pipe -- T = a*b and m*P as 32x32->64 IMAD.WIDE,
+ * the short product m as one IMAD -- and returned in the canonical range
+ * [0, P).
  *
  * Conventions shared by every entry point below:
  *   - Array pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors),
@@ -119,6 +120,13 @@ mont_status_t mont_pow_vec(const mont_ctx_t *ctx, uint32_t *out, const uint32_t 
  * on the host or after the cross-rank all-reduce.  4 bytes per element. */
 mont_status_t mont_checksum(const mont_ctx_t *ctx, unsigned long long *acc, const uint32_t *x,
                             size_t n, cudaStream_t stream);
+
+/* Fused A7 + A11: c[i] = REDC(a[i], b[i]) exactly as mont_mul_vec, and
+ * *acc += sum_i c[i] (64-bit, device pointer, caller zeroes it) in the same
+ * pass, so the checksum of configs[4] costs no second read of c.  One 64-bit
+ * atomic per CTA.  Same argument rules as mont_mul_vec and mont_checksum. */
+mont_status_t mont_mul_vec_checksum(const mont_ctx_t *ctx, uint32_t *c, const uint32_t *a, const uint32_t *b,
+                                    size_t n, unsigned long long *acc, cudaStream_t stream);
 
 /* tw[j] = to_mont(w^j mod P) for j < len: the Montgomery-form twiddle table of
  * BASELINE configs[2] (w a root of unity mod P).  Each element is an

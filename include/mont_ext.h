@@ -20,7 +20,8 @@ extern "C" {
  *   ctas_per_sm: CTAs per SM for the persistent grid (grid = SMs * ctas_per_sm)
  *   unroll    : 128-bit chunks per thread per loop trip (1, 2, 4 or 8)
  *   variant   : kernel variant (kernel-specific; 0 = default).
- *                 mont_mul_vec_ex, mb_triad, mb_copy : 0 = flat grid (one
+ *                 mont_mul_vec_ex, mont_mul_vec_checksum_ex, to_mont_ex,
+ *                 from_mont_ex, mb_triad, mb_copy : 0 = flat grid (one
  *                                   tile of threads*unroll uint4 per CTA),
  *                                   1 = persistent grid-stride over tiles
  *                                   with grid = SMs * ctas_per_sm
@@ -44,6 +45,13 @@ typedef struct mont_launch {
 
 mont_status_t mont_mul_vec_ex(const mont_ctx_t *ctx, uint32_t *c, const uint32_t *a, const uint32_t *b,
                               size_t n, const mont_launch_t *cfg, cudaStream_t stream);
+mont_status_t mont_mul_vec_checksum_ex(const mont_ctx_t *ctx, uint32_t *c, const uint32_t *a,
+                                       const uint32_t *b, size_t n, unsigned long long *acc,
+                                       const mont_launch_t *cfg, cudaStream_t stream);
+mont_status_t to_mont_ex(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *in, size_t n,
+                         const mont_launch_t *cfg, cudaStream_t stream);
+mont_status_t from_mont_ex(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *in, size_t n,
+                           const mont_launch_t *cfg, cudaStream_t stream);
 mont_status_t mont_mul_twiddle_ex(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *x,
                                   const uint32_t *tw, size_t batch, size_t len,
                                   const mont_launch_t *cfg, cudaStream_t stream);

@@ -21,7 +21,7 @@ _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "libmont.so"
 
 __all__ = [
-    "Ctx", "MontError", "ctx_init", "to_mont", "from_mont", "mul_vec", "mul_twiddle", "pow_vec",
+    "Ctx", "MontError", "ctx_init", "to_mont", "from_mont", "mul_vec", "mul_vec_checksum", "mul_twiddle", "pow_vec",
     "checksum", "twiddle_table", "synth_fill", "Launch", "lib", "LIB_PATH",
 ]
 
@@ -62,6 +62,10 @@ SIGNATURES = {
     "mont_pow_vec": (C.c_int, [_CTX, _P, _P, _P, _S, _P]),
     "mont_checksum": (C.c_int, [_CTX, _P, _P, _S, _P]),
     "mont_twiddle_table": (C.c_int, [_CTX, _P, C.c_uint32, _S, _P]),
+    "mont_mul_vec_checksum": (C.c_int, [_CTX, _P, _P, _P, _S, _P, _P]),
+    "mont_mul_vec_checksum_ex": (C.c_int, [_CTX, _P, _P, _P, _S, _P, _LAUNCH, _P]),
+    "to_mont_ex": (C.c_int, [_CTX, _P, _P, _S, _LAUNCH, _P]),
+    "from_mont_ex": (C.c_int, [_CTX, _P, _P, _S, _LAUNCH, _P]),
     "mont_strerror": (C.c_char_p, [C.c_int]),
     "mont_build_arch": (C.c_int, []),
     "mont_mul_vec_ex": (C.c_int, [_CTX, _P, _P, _P, _S, _LAUNCH, _P]),
@@ -170,17 +174,44 @@ def mul_vec(ctx: Ctx, a, b, out=None, stream=None, cfg: Launch | None = None):
     return out
 
 
-def to_mont(ctx: Ctx, x, out=None, stream=None):
+def mul_vec_checksum(ctx: Ctx, a, b, out=None, acc=None, stream=None, cfg: Launch | None = None):
+    """c = mul_vec(a, b) and acc += sum(c) in one pass (mont_mul_vec_checksum); returns (c, acc)."""
+    torch = _torch()
+    _dev_u32(a, "a"), _dev_u32(b, "b")
+    if a.numel() != b.numel():
+        raise ValueError("a and b differ in length")
+    out = _out_like(out, a)
+    if acc is None:
+        acc = torch.zeros(1, dtype=torch.int64, device=a.device)
+    s = _stream_handle(stream)
+    if cfg is None:
+        _check(lib().mont_mul_vec_checksum(C.byref(ctx), _ptr(out), _ptr(a), _ptr(b), a.numel(), _ptr(acc), s),
+               "mont_mul_vec_checksum")
+    else:
+        _check(lib().mont_mul_vec_checksum_ex(C.byref(ctx), _ptr(out), _ptr(a), _ptr(b), a.numel(), _ptr(acc),
+                                              C.byref(cfg), s), "mont_mul_vec_checksum_ex")
+    return out, acc
+
+
+def to_mont(ctx: Ctx, x, out=None, stream=None, cfg: Launch | None = None):
     _dev_u32(x, "x")
     out = _out_like(out, x)
-    _check(lib().to_mont(C.byref(ctx), _ptr(out), _ptr(x), x.numel(), _stream_handle(stream)), "to_mont")
+    s = _stream_handle(stream)
+    if cfg is None:
+        _check(lib().to_mont(C.byref(ctx), _ptr(out), _ptr(x), x.numel(), s), "to_mont")
+    else:
+        _check(lib().to_mont_ex(C.byref(ctx), _ptr(out), _ptr(x), x.numel(), C.byref(cfg), s), "to_mont_ex")
     return out
 
 
-def from_mont(ctx: Ctx, x, out=None, stream=None):
+def from_mont(ctx: Ctx, x, out=None, stream=None, cfg: Launch | None = None):
     _dev_u32(x, "x")
     out = _out_like(out, x)
-    _check(lib().from_mont(C.byref(ctx), _ptr(out), _ptr(x), x.numel(), _stream_handle(stream)), "from_mont")
+    s = _stream_handle(stream)
+    if cfg is None:
+        _check(lib().from_mont(C.byref(ctx), _ptr(out), _ptr(x), x.numel(), s), "from_mont")
+    else:
+        _check(lib().from_mont_ex(C.byref(ctx), _ptr(out), _ptr(x), x.numel(), C.byref(cfg), s), "from_mont_ex")
     return out
 
 

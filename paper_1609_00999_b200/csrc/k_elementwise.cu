@@ -48,15 +48,46 @@ __device__ __forceinline__ uint4 apply4(const Op &op, const uint4 &a) {
     return make_uint4(op(a.x), op(a.y), op(a.z), op(a.w));
 }
 
+// ------------------------------------------------------------ block reduce
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// adds the CTA's total of s into *acc with one 64-bit atomic
+__device__ __forceinline__ void block_sum_to(unsigned long long *acc, unsigned long long s) {
+    __shared__ unsigned long long warp_part[32];
+    s = warp_sum(s);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) warp_part[wid] = s;
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = (blockDim.x + 31) >> 5;
+        s = lane < nw ? warp_part[lane] : 0ull;
+        s = warp_sum(s);
+        if (lane == 0 && s) atomicAdd(acc, s);
+    }
+}
+
+__device__ __forceinline__ unsigned long long sum4(const uint4 &v) {
+    return (unsigned long long)v.x + v.y + (unsigned long long)v.z + v.w;
+}
+
 // ---------------------------------------------------------------- binary map
 // Vector body over n4 chunks of a4/b4/c4 (16-byte aligned), plus `head`
 // scalar elements before it and `tail` after it, handled by CTA 0.
-template <int U, class Op>
+// SUM: also add the sum of every output word into *acc (A7 fused with the
+// A11 checksum: saves re-reading c, 4 B/elem).
+template <int U, class Op, bool SUM>
 __global__ void __launch_bounds__(512) k_map2(Op op, uint32_t *c, const uint32_t *a, const uint32_t *b,
-                                                uint32_t head, size_t n4, uint32_t tail) {
+                                                uint32_t head, size_t n4, uint32_t tail, unsigned long long *acc) {
+    unsigned long long s = 0;
     if (blockIdx.x == 0 && threadIdx.x < head + tail) {
         size_t i = threadIdx.x < head ? threadIdx.x : head + 4 * n4 + (threadIdx.x - head);
-        c[i] = op(a[i], b[i]);
+        const uint32_t r = op(a[i], b[i]);
+        c[i] = r;
+        s += r;
     }
     const uint4 *a4 = reinterpret_cast<const uint4 *>(a + head);
     const uint4 *b4 = reinterpret_cast<const uint4 *>(b + head);
@@ -72,18 +103,27 @@ __global__ void __launch_bounds__(512) k_map2(Op op, uint32_t *c, const uint32_t
 #pragma unroll
         for (int k = 0; k < U; ++k) vb[k] = ld_stream(b4 + base + (size_t)k * blockDim.x);
 #pragma unroll
-        for (int k = 0; k < U; ++k) st_stream(c4 + base + (size_t)k * blockDim.x, apply4(op, va[k], vb[k]));
+        for (int k = 0; k < U; ++k) {
+            const uint4 r = apply4(op, va[k], vb[k]);
+            st_stream(c4 + base + (size_t)k * blockDim.x, r);
+            if (SUM) s += sum4(r);
+        }
     }
     if (t == ntiles_full) {  // the one partial tile, owned by exactly one CTA
-        for (size_t i = t * tile + threadIdx.x; i < n4; i += blockDim.x)
-            st_stream(c4 + i, apply4(op, ld_stream(a4 + i), ld_stream(b4 + i)));
+        for (size_t i = t * tile + threadIdx.x; i < n4; i += blockDim.x) {
+            const uint4 r = apply4(op, ld_stream(a4 + i), ld_stream(b4 + i));
+            st_stream(c4 + i, r);
+            if (SUM) s += sum4(r);
+        }
     }
+    if (SUM) block_sum_to(acc, s);
 }
 
 // 32-bit path for operands that do not share an address mod 16
-template <int U, class Op>
+template <int U, class Op, bool SUM>
 __global__ void __launch_bounds__(512) k_map2_scalar(Op op, uint32_t *c, const uint32_t *a, const uint32_t *b,
-                                                       size_t n) {
+                                                       size_t n, unsigned long long *acc) {
+    unsigned long long s = 0;
     const size_t tile = (size_t)U * blockDim.x;
     for (size_t t0 = (size_t)blockIdx.x * tile; t0 < n; t0 += (size_t)gridDim.x * tile) {
         uint32_t va[U], vb[U];
@@ -96,9 +136,14 @@ __global__ void __launch_bounds__(512) k_map2_scalar(Op op, uint32_t *c, const u
 #pragma unroll
         for (int k = 0; k < U; ++k) {
             size_t i = t0 + (size_t)k * blockDim.x + threadIdx.x;
-            if (i < n) st_stream1(c + i, op(va[k], vb[k]));
+            if (i < n) {
+                const uint32_t r = op(va[k], vb[k]);
+                st_stream1(c + i, r);
+                if (SUM) s += r;
+            }
         }
     }
+    if (SUM) block_sum_to(acc, s);
 }
 
 // ----------------------------------------------------------------- unary map
@@ -146,12 +191,6 @@ __global__ void __launch_bounds__(512) k_map1_scalar(Op op, uint32_t *out, const
 }
 
 // ------------------------------------------------------------------ checksum
-__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    return v;
-}
-
 template <int U>
 __global__ void __launch_bounds__(512) k_sum(unsigned long long *acc, const uint32_t *x, uint32_t head, size_t n4,
                                                uint32_t tail) {
@@ -166,29 +205,16 @@ __global__ void __launch_bounds__(512) k_sum(unsigned long long *acc, const uint
 #pragma unroll
         for (int k = 0; k < U; ++k) {
             size_t i = t0 + (size_t)k * blockDim.x + threadIdx.x;
-            if (i < n4) {
-                uint4 v = ld_stream(x4 + i);
-                s += (unsigned long long)v.x + v.y + (unsigned long long)v.z + v.w;
-            }
+            if (i < n4) s += sum4(ld_stream(x4 + i));
         }
     }
-    __shared__ unsigned long long warp_part[32];
-    s = warp_sum(s);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (lane == 0) warp_part[wid] = s;
-    __syncthreads();
-    if (wid == 0) {
-        const int nw = (blockDim.x + 31) >> 5;
-        s = lane < nw ? warp_part[lane] : 0ull;
-        s = warp_sum(s);
-        if (lane == 0 && s) atomicAdd(acc, s);
-    }
+    block_sum_to(acc, s);
 }
 
 // ------------------------------------------------------------------- helpers
-template <class Op>
+template <bool SUM, class Op>
 static mont_status_t launch_map2(const Op &op, uint32_t *c, const uint32_t *a, const uint32_t *b, size_t n,
-                                 const Launch &L, cudaStream_t s) {
+                                 const Launch &L, cudaStream_t s, unsigned long long *acc = nullptr) {
     const int sms = sm_count();
     if (sms <= 0) return MONT_ECUDA;
     const uintptr_t pa = (uintptr_t)a, pb = (uintptr_t)b, pc = (uintptr_t)c;
@@ -204,10 +230,10 @@ static mont_status_t launch_map2(const Op &op, uint32_t *c, const uint32_t *a, c
         if (grid == 0) grid = 1;
         if (grid > 0x7fffffff) return MONT_EUNSUPPORTED;
         switch (L.unroll) {
-            case 1: k_map2<1><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, head, n4, tail); break;
-            case 2: k_map2<2><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, head, n4, tail); break;
-            case 4: k_map2<4><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, head, n4, tail); break;
-            default: k_map2<8><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, head, n4, tail); break;
+            case 1: k_map2<1, Op, SUM><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, head, n4, tail, acc); break;
+            case 2: k_map2<2, Op, SUM><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, head, n4, tail, acc); break;
+            case 4: k_map2<4, Op, SUM><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, head, n4, tail, acc); break;
+            default: k_map2<8, Op, SUM><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, head, n4, tail, acc); break;
         }
     } else {
         const size_t tile = (size_t)L.unroll * L.threads;
@@ -215,10 +241,10 @@ static mont_status_t launch_map2(const Op &op, uint32_t *c, const uint32_t *a, c
         const size_t need = (n + tile - 1) / tile;
         if (grid > need) grid = need;
         switch (L.unroll) {
-            case 1: k_map2_scalar<1><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, n); break;
-            case 2: k_map2_scalar<2><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, n); break;
-            case 4: k_map2_scalar<4><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, n); break;
-            default: k_map2_scalar<8><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, n); break;
+            case 1: k_map2_scalar<1, Op, SUM><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, n, acc); break;
+            case 2: k_map2_scalar<2, Op, SUM><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, n, acc); break;
+            case 4: k_map2_scalar<4, Op, SUM><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, n, acc); break;
+            default: k_map2_scalar<8, Op, SUM><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, n, acc); break;
         }
     }
     return launch_status();
@@ -266,7 +292,9 @@ static mont_status_t launch_map1(const Op &op, uint32_t *out, const uint32_t *in
 // persistent grid-stride shape by ~10 % -- the block scheduler balances the
 // slow and fast SMs dynamically, a static round-robin deal does not.
 static const Launch kMulVecDefault{256, 4, 1, 0, 0};
-static const Launch kMap1Default{256, 4, 1, 0, 0};
+static const Launch kMap1Default{256, 4, 2, 0, 0};
+// fused checksum: 4 uint4 per thread keeps the per-CTA atomic count at n / 4096
+static const Launch kMulVecSumDefault{256, 4, 4, 0, 0};
 
 }  // namespace mont
 
@@ -279,7 +307,7 @@ extern "C" mont_status_t mont_mul_vec_ex(const mont_ctx_t *ctx, uint32_t *c, con
     if (!a || !b || !c || ((uintptr_t)a | (uintptr_t)b | (uintptr_t)c) & 3u) return MONT_EINVAL_ARG;
     const Launch L = resolve(cfg, kMulVecDefault);
     if (!launch_ok(L)) return MONT_EINVAL_ARG;
-    return launch_map2(OpMul{ctx->p, 0u - ctx->pneg}, c, a, b, n, L, stream);
+    return launch_map2<false>(OpMul{ctx->p, 0u - ctx->pneg}, c, a, b, n, L, stream);
 }
 
 extern "C" mont_status_t mont_mul_vec(const mont_ctx_t *ctx, uint32_t *c, const uint32_t *a, const uint32_t *b,
@@ -287,20 +315,52 @@ extern "C" mont_status_t mont_mul_vec(const mont_ctx_t *ctx, uint32_t *c, const 
     return mont_mul_vec_ex(ctx, c, a, b, n, nullptr, stream);
 }
 
-extern "C" mont_status_t to_mont(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *in, size_t n,
-                                 cudaStream_t stream) {
+extern "C" mont_status_t mont_mul_vec_checksum_ex(const mont_ctx_t *ctx, uint32_t *c, const uint32_t *a,
+                                                  const uint32_t *b, size_t n, unsigned long long *acc,
+                                                  const mont_launch_t *cfg, cudaStream_t stream) {
+    if (!ctx_ok(ctx)) return ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
+    if (n == 0) return MONT_OK;
+    if (!a || !b || !c || !acc || ((uintptr_t)a | (uintptr_t)b | (uintptr_t)c) & 3u || ((uintptr_t)acc & 7u))
+        return MONT_EINVAL_ARG;
+    const Launch L = resolve(cfg, kMulVecSumDefault);
+    if (!launch_ok(L)) return MONT_EINVAL_ARG;
+    return launch_map2<true>(OpMul{ctx->p, 0u - ctx->pneg}, c, a, b, n, L, stream, acc);
+}
+
+extern "C" mont_status_t mont_mul_vec_checksum(const mont_ctx_t *ctx, uint32_t *c, const uint32_t *a,
+                                               const uint32_t *b, size_t n, unsigned long long *acc,
+                                               cudaStream_t stream) {
+    return mont_mul_vec_checksum_ex(ctx, c, a, b, n, acc, nullptr, stream);
+}
+
+extern "C" mont_status_t to_mont_ex(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *in, size_t n,
+                                    const mont_launch_t *cfg, cudaStream_t stream) {
     if (!ctx_ok(ctx)) return ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
     if (n == 0) return MONT_OK;
     if (!in || !out || ((uintptr_t)in | (uintptr_t)out) & 3u) return MONT_EINVAL_ARG;
-    return launch_map1(OpTo{ctx->p, 0u - ctx->pneg, ctx->r2}, out, in, n, kMap1Default, stream);
+    const Launch L = resolve(cfg, kMap1Default);
+    if (!launch_ok(L)) return MONT_EINVAL_ARG;
+    return launch_map1(OpTo{ctx->p, 0u - ctx->pneg, ctx->r2}, out, in, n, L, stream);
+}
+
+extern "C" mont_status_t to_mont(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *in, size_t n,
+                                 cudaStream_t stream) {
+    return to_mont_ex(ctx, out, in, n, nullptr, stream);
+}
+
+extern "C" mont_status_t from_mont_ex(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *in, size_t n,
+                                      const mont_launch_t *cfg, cudaStream_t stream) {
+    if (!ctx_ok(ctx)) return ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
+    if (n == 0) return MONT_OK;
+    if (!in || !out || ((uintptr_t)in | (uintptr_t)out) & 3u) return MONT_EINVAL_ARG;
+    const Launch L = resolve(cfg, kMap1Default);
+    if (!launch_ok(L)) return MONT_EINVAL_ARG;
+    return launch_map1(OpFrom{ctx->p, 0u - ctx->pneg}, out, in, n, L, stream);
 }
 
 extern "C" mont_status_t from_mont(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *in, size_t n,
                                    cudaStream_t stream) {
-    if (!ctx_ok(ctx)) return ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
-    if (n == 0) return MONT_OK;
-    if (!in || !out || ((uintptr_t)in | (uintptr_t)out) & 3u) return MONT_EINVAL_ARG;
-    return launch_map1(OpFrom{ctx->p, 0u - ctx->pneg}, out, in, n, kMap1Default, stream);
+    return from_mont_ex(ctx, out, in, n, nullptr, stream);
 }
 
 extern "C" mont_status_t mont_checksum(const mont_ctx_t *ctx, unsigned long long *acc, const uint32_t *x, size_t n,
@@ -328,7 +388,7 @@ extern "C" mont_status_t mb_triad(uint32_t *c, const uint32_t *a, const uint32_t
     if (!a || !b || !c) return MONT_EINVAL_ARG;
     const Launch L = resolve(cfg, kMulVecDefault);
     if (!launch_ok(L)) return MONT_EINVAL_ARG;
-    return launch_map2(OpXor{}, c, a, b, n, L, stream);
+    return launch_map2<false>(OpXor{}, c, a, b, n, L, stream);
 }
 
 extern "C" mont_status_t mb_copy(uint32_t *out, const uint32_t *in, size_t n, const mont_launch_t *cfg,

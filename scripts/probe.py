@@ -87,6 +87,16 @@ if args.what in ("all", "hbm"):
                     out(what="mul_vec", threads=threads, ctas=ctas, unroll=unroll, variant=variant,
                         us=med * 1e6, gbs=12 * n / med / 1e9, gbs_best=12 * n / best / 1e9,
                         gmulmod=n / med / 1e9)
+    acc = torch.zeros(1, dtype=torch.int64, device=dev)
+    for threads in (256, 512):
+        for unroll in (1, 2, 4, 8):
+            cfg = m.Launch(threads=threads, unroll=unroll)
+            med, best = timeit(lambda: m.mul_vec_checksum(ctx, a, b, out=c, acc=acc, cfg=cfg))
+            out(what="mul_vec_checksum", threads=threads, unroll=unroll, us=med * 1e6, gbs=12 * n / med / 1e9)
+            med, best = timeit(lambda: m.to_mont(ctx, a, out=c, cfg=cfg))
+            out(what="to_mont_cfg", threads=threads, unroll=unroll, us=med * 1e6, gbs=8 * n / med / 1e9)
+            med, best = timeit(lambda: lib().mb_copy(c.data_ptr(), a.data_ptr(), n, C.byref(cfg), s.cuda_stream))
+            out(what="copy_cfg", threads=threads, unroll=unroll, us=med * 1e6, gbs=8 * n / med / 1e9)
     cfg = m.Launch()
     med, best = timeit(lambda: lib().mb_copy(c.data_ptr(), a.data_ptr(), n, C.byref(cfg), s.cuda_stream))
     out(what="copy", us=med * 1e6, gbs=8 * n / med / 1e9)

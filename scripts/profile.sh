@@ -9,7 +9,7 @@ CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --soak 0"
 $CMD > $OUT/plain_small.log 2>&1 || { echo "plain small bench failed"; tail -20 $OUT/plain_small.log; exit 1; }
 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
 echo "launch list rc=$?"
-for K in k_map2 k_pow k_twiddle k_map1 k_sum; do
-  ncu --set full --clock-control none --import-source on -k regex:"^${K}" -s 6 -c 1 -o $OUT/prof_${K} $CMD > $OUT/ncu_${K}.log 2>&1
+for K in k_map2 k_pow k_twiddle k_map1; do
+  ncu --set full --clock-control none --import-source on -k regex:"^${K}" -s 3 -c 1 -o $OUT/prof_${K} $CMD > $OUT/ncu_${K}.log 2>&1
   echo "ncu full ${K} rc=$?"
 done

@@ -287,3 +287,44 @@ def test_checksum(m, n, off):
     acc = m.checksum(m.ctx_init(P), offset_view(x, off))
     torch.cuda.synchronize()
     assert int(acc.item()) == oracle.raw_sum(x)
+
+
+# ------------------------------------------------------- fused mul + checksum
+
+@pytest.mark.parametrize("n", [1, 3, 5, 4096, 65536 + 5, 1 << 20 | 3])
+@pytest.mark.parametrize("off", [0, 1])
+def test_mul_vec_checksum_fused(m, n, off):
+    P = 2013265921
+    a, b = synth.c5_inputs(P, 1000, n)
+    ref = oracle.mont_mul(P, a, b)
+    ctx = m.ctx_init(P)
+    ta, tb = offset_view(a, off), offset_view(b, off)
+    tc = offset_view(np.zeros_like(a), off)
+    c, acc = m.mul_vec_checksum(ctx, ta, tb, out=tc)
+    assert np.array_equal(host(c), ref)
+    assert int(acc.item()) == oracle.raw_sum(ref)
+    # accumulates across calls; misaligned operands take the 32-bit path
+    tb2 = offset_view(b, (off + 1) % 4)
+    m.mul_vec_checksum(ctx, ta, tb2, acc=acc)
+    assert int(acc.item()) == 2 * oracle.raw_sum(ref)
+
+
+@pytest.mark.parametrize("threads,unroll,variant", [(256, 1, 0), (512, 4, 0), (128, 2, 1), (256, 8, 1)])
+def test_mul_vec_checksum_configs(m, threads, unroll, variant):
+    P = 998244353
+    a, b = synth.c2_inputs(P, 0, 300_001)
+    ref = oracle.mont_mul(P, a, b)
+    cfg = m.Launch(threads=threads, unroll=unroll, variant=variant, ctas_per_sm=4)
+    c, acc = m.mul_vec_checksum(m.ctx_init(P), dev(a), dev(b), cfg=cfg)
+    assert np.array_equal(host(c), ref) and int(acc.item()) == oracle.raw_sum(ref)
+
+
+@pytest.mark.parametrize("unroll,threads,variant", [(1, 256, 0), (2, 256, 0), (4, 512, 0), (2, 128, 1)])
+def test_to_from_mont_configs(m, unroll, threads, variant):
+    P = 469762049
+    x = synth.uniform(42, 9, P, 0, 123_457)
+    cfg = m.Launch(threads=threads, unroll=unroll, variant=variant, ctas_per_sm=4)
+    ctx = m.ctx_init(P)
+    tm = m.to_mont(ctx, dev(x), cfg=cfg)
+    assert np.array_equal(host(tm), oracle.to_mont(P, x))
+    assert np.array_equal(host(m.from_mont(ctx, tm, cfg=cfg)), x)
