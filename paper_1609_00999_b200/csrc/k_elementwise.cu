@@ -292,9 +292,9 @@ static mont_status_t launch_map1(const Op &op, uint32_t *out, const uint32_t *in
 // persistent grid-stride shape by ~10 % -- the block scheduler balances the
 // slow and fast SMs dynamically, a static round-robin deal does not.
 static const Launch kMulVecDefault{256, 4, 1, 0, 0};
-static const Launch kMap1Default{256, 4, 2, 0, 0};
-// fused checksum: 4 uint4 per thread keeps the per-CTA atomic count at n / 4096
-static const Launch kMulVecSumDefault{256, 4, 4, 0, 0};
+static const Launch kMap1Default{512, 4, 2, 0, 0};
+// fused checksum: 2 uint4 per thread x 512 threads -> one atomic per 4096 words
+static const Launch kMulVecSumDefault{512, 4, 2, 0, 0};
 
 }  // namespace mont
 
