@@ -450,7 +450,8 @@ def ncu_traffic(name: str):
         return None
     try:
         d = json.loads(p.read_text())
-        return d.get("traffic_bytes_per_launch", {}).get(name)
+        v = d.get("traffic_bytes_per_launch", {}).get(name.split("[")[0])
+        return int(v) if v is not None else None
     except Exception:
         return None
 
