@@ -29,7 +29,11 @@ extern "C" {
  *                                   registers; 1 = binary ladder with
  *                                   selects; 2 = 3-bit window, registers;
  *                                   3 = 2-bit window, table in shared memory;
- *                                   4 = 3-bit window, shared memory.
+ *                                   4 = 3-bit window, shared memory;
+ *                                   5/6/7/8 = 2-bit window with 3/2/1/0 of
+ *                                   each 4 lanes on the IMAD pipe and the
+ *                                   rest as FP64 Barrett products on the
+ *                                   FP64 pipe.
  *                                   ctas_per_sm = 0 selects a flat grid.
  *                 mont_mul_twiddle_ex : 0 = bulk-copy (TMA) staged table,
  *                                   1 = table read through L1/L2 (no smem)
@@ -80,7 +84,8 @@ mont_status_t synth_fill(uint32_t *out, size_t n, uint64_t seed, uint32_t stream
  *   dependency chains of one kind (0 = IMAD mul.lo, 1 = IMAD.HI mul.hi,
  *   2 = IMAD.WIDE mad.wide, 3 = the library's signed chain REDC, 4 = its
  *   canonical REDC, 5 = REDC from mul.lo/mul.hi, 6 = REDC with an IMAD.HI
- *   64-bit addend), writing one word per thread to sink[] (which must hold
+ *   64-bit addend, 7 = DFMA, 8 = the FP64 Barrett product, 9 = IADD,
+ *   10 = LOP3, 11 = 3 Montgomery : 1 FP64 chains, 12 = 1 : 1), writing one word per thread to sink[] (which must hold
  *   SMs * ctas_per_sm * 256 words); the caller times it and divides the
  *   executed count (threads * iters * 64) by the time.
  *   grid = SMs * ctas_per_sm, 256 threads (cfg may be NULL: 8 CTAs/SM). */

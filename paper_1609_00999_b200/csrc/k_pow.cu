@@ -27,6 +27,7 @@ namespace mont {
 struct PowParams {
     int32_t p, pinv;  // pinv = P^-1 mod 2^32 = -pneg
     uint32_t r1, r2;
+    double pd, pdinv;  // P and fl(1/P) for the FP64 lanes
 };
 
 // x-bar = to_mont(base) = REDC(base, R^2 mod P): canonical, valid for any uint32 base
@@ -118,8 +119,73 @@ __device__ __forceinline__ void pow_binary(const PowParams &q, const uint32_t (&
     for (int l = 0; l < L; ++l) out[l] = pow_exit(q, acc[l]);
 }
 
+// ---- hybrid 2-bit window: of the 4 lanes of a uint4, NI run the integer
+// Montgomery ladder on the IMAD (FMAHeavy) pipe and 4 - NI run the same
+// ladder as FP64 Barrett products (mont_core.cuh fmulmod) on the otherwise
+// idle FP64 pipe, on plain residues (no residue-class conversion needed).
+// Both instruction streams interleave in one thread, so the two multiplier
+// arrays of the SM work at once.  Results are identical: both compute
+// base^exp mod P exactly and canonicalise.
+template <int NI>
+__device__ __forceinline__ void pow_hybrid(const PowParams &q, const uint32_t (&base)[4], const uint32_t (&e)[4],
+                                           uint32_t (&out)[4]) {
+    constexpr int NF = 4 - NI;
+    int32_t ti[NI > 0 ? NI : 1][4], ai[NI > 0 ? NI : 1];
+    double tf[NF > 0 ? NF : 1][4], af[NF > 0 ? NF : 1];
+#pragma unroll
+    for (int l = 0; l < NI; ++l) {
+        const int32_t x = pow_entry(q, base[l]);
+        ti[l][0] = (int32_t)q.r1;
+        ti[l][1] = x;
+        ti[l][2] = sredc(x, x, q.p, q.pinv);
+        ti[l][3] = sredc(ti[l][2], x, q.p, q.pinv);
+        const uint32_t d0 = e[l] >> 30;
+        ai[l] = (d0 & 2u) ? ((d0 & 1u) ? ti[l][3] : ti[l][2]) : ((d0 & 1u) ? ti[l][1] : ti[l][0]);
+    }
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+        const double x = fmulmod((double)base[NI + f], 1.0, q.pd, q.pdinv);  // base mod P, in (-P/2, P/2]
+        tf[f][0] = 1.0;
+        tf[f][1] = x;
+        tf[f][2] = fmulmod(x, x, q.pd, q.pdinv);
+        tf[f][3] = fmulmod(tf[f][2], x, q.pd, q.pdinv);
+        const uint32_t d0 = e[NI + f] >> 30;
+        af[f] = (d0 & 2u) ? ((d0 & 1u) ? tf[f][3] : tf[f][2]) : ((d0 & 1u) ? tf[f][1] : tf[f][0]);
+    }
+#pragma unroll
+    for (int sh = 28; sh >= 0; sh -= 2) {
+#pragma unroll
+        for (int l = 0; l < NI; ++l) {
+            int32_t a = sredc(ai[l], ai[l], q.p, q.pinv);
+            a = sredc(a, a, q.p, q.pinv);
+            const uint32_t d = (e[l] >> sh) & 3u;
+            const int32_t lo = (d & 1u) ? ti[l][1] : ti[l][0];
+            const int32_t hi = (d & 1u) ? ti[l][3] : ti[l][2];
+            ai[l] = sredc(a, (d & 2u) ? hi : lo, q.p, q.pinv);
+        }
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            double a = fmulmod(af[f], af[f], q.pd, q.pdinv);
+            a = fmulmod(a, a, q.pd, q.pdinv);
+            const uint32_t d = (e[NI + f] >> sh) & 3u;
+            const double lo = (d & 1u) ? tf[f][1] : tf[f][0];
+            const double hi = (d & 1u) ? tf[f][3] : tf[f][2];
+            af[f] = fmulmod(a, (d & 2u) ? hi : lo, q.pd, q.pdinv);
+        }
+    }
+#pragma unroll
+    for (int l = 0; l < NI; ++l) out[l] = pow_exit(q, ai[l]);
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+        const double r = af[f] < 0.0 ? af[f] + q.pd : af[f];
+        out[NI + f] = (uint32_t)__double2uint_rn(r);
+    }
+}
+
 // variant: 0 = 2-bit window, registers; 1 = binary; 2 = 3-bit window, registers;
-//          3 = 2-bit window, smem table; 4 = 3-bit window, smem table
+//          3 = 2-bit window, smem table; 4 = 3-bit window, smem table;
+//          5/6/7/8 = hybrid 2-bit window with 3/2/1/0 of 4 lanes on the IMAD
+//          pipe and the rest on the FP64 pipe
 template <int V, int L>
 __device__ __forceinline__ void pow_lanes(const PowParams &q, const uint32_t (&b)[L], const uint32_t (&e)[L],
                                           uint32_t (&o)[L], int32_t *s_tab) {
@@ -127,7 +193,8 @@ __device__ __forceinline__ void pow_lanes(const PowParams &q, const uint32_t (&b
     else if (V == 1) pow_binary<L>(q, b, e, o);
     else if (V == 2) pow_window<3, L, false>(q, b, e, o, s_tab);
     else if (V == 3) pow_window<2, L, true>(q, b, e, o, s_tab);
-    else pow_window<3, L, true>(q, b, e, o, s_tab);
+    else if (V == 4) pow_window<3, L, true>(q, b, e, o, s_tab);
+    else pow_hybrid<8 - V>(q, b, e, o);
 }
 
 template <int V>
@@ -221,16 +288,20 @@ extern "C" mont_status_t mont_pow_vec_ex(const mont_ctx_t *ctx, uint32_t *out, c
     if (n == 0) return MONT_OK;
     if (!out || !base || !exp || ((uintptr_t)out | (uintptr_t)base | (uintptr_t)exp) & 3u) return MONT_EINVAL_ARG;
     Launch L = resolve(cfg, kPowDefault);
-    if (L.threads != 256 || L.variant < 0 || L.variant > 4 || L.ctas_per_sm < 0) return MONT_EINVAL_ARG;
+    if (L.threads != 256 || L.variant < 0 || L.variant > 8 || L.ctas_per_sm < 0) return MONT_EINVAL_ARG;
     const int sms = sm_count();
     if (sms <= 0) return MONT_ECUDA;
-    const PowParams q{(int32_t)ctx->p, (int32_t)(0u - ctx->pneg), ctx->r1, ctx->r2};
+    const PowParams q{(int32_t)ctx->p, (int32_t)(0u - ctx->pneg), ctx->r1, ctx->r2, (double)ctx->p, 1.0 / (double)ctx->p};
     switch (L.variant) {
         case 0: return launch_pow<0>(q, out, base, exp, n, L.ctas_per_sm, sms, stream);
         case 1: return launch_pow<1>(q, out, base, exp, n, L.ctas_per_sm, sms, stream);
         case 2: return launch_pow<2>(q, out, base, exp, n, L.ctas_per_sm, sms, stream);
         case 3: return launch_pow<3>(q, out, base, exp, n, L.ctas_per_sm, sms, stream);
-        default: return launch_pow<4>(q, out, base, exp, n, L.ctas_per_sm, sms, stream);
+        case 4: return launch_pow<4>(q, out, base, exp, n, L.ctas_per_sm, sms, stream);
+        case 5: return launch_pow<5>(q, out, base, exp, n, L.ctas_per_sm, sms, stream);
+        case 6: return launch_pow<6>(q, out, base, exp, n, L.ctas_per_sm, sms, stream);
+        case 7: return launch_pow<7>(q, out, base, exp, n, L.ctas_per_sm, sms, stream);
+        default: return launch_pow<8>(q, out, base, exp, n, L.ctas_per_sm, sms, stream);
     }
 }
 

@@ -139,3 +139,24 @@ __device__ __forceinline__ void st_stream1(uint32_t *p, uint32_t v) {
 }
 
 }  // namespace mont
+
+namespace mont {
+
+// ---- FP64 reduction (Barrett, Alg. 1, with a floating
+// reciprocal instead of the integer P' = floor(2^2k / P)).  Plain residues
+// held as doubles in (-P, P):
+//   h = fl(a b); l = fma(a, b, -h)       a b = h + l exactly (FMA error term)
+//   q = rint(h / P)                       fma(h, 1/P, 1.5*2^52) - 1.5*2^52
+//   r = fma(-q, P, h) + l                 = a b - q P exactly (|.| < 2^53)
+// |a b / P - q| <= 1/2 + 2^-21, so |r| < P(1/2 + 2^-21): the chain needs no
+// correction.  6 FP64-pipe instructions, no integer pipe use: this is the
+// second multiplier array of the SM, idle in the IMAD-only ladder.
+__device__ __forceinline__ double fmulmod(double a, double b, double P, double Pinv) {
+    const double M = 6755399441055744.0;  // 1.5 * 2^52
+    const double h = a * b;
+    const double l = fma(a, b, -h);
+    const double q = fma(h, Pinv, M) - M;
+    return fma(-q, P, h) + l;
+}
+
+}  // namespace mont

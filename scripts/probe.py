@@ -47,8 +47,9 @@ def lib():
 if args.what in ("all", "imad"):
     import ctypes as C
     sink = torch.empty(sms * 32 * 256, dtype=torch.uint32, device=dev)
-    names = {0: "IMAD", 1: "IMAD.HI", 2: "IMAD.WIDE", 3: "sredc", 4: "redc", 5: "sredc_mulhi", 6: "sredc_hiadd"}
-    for kind in range(7):
+    names = {0: "IMAD", 1: "IMAD.HI", 2: "IMAD.WIDE(hoisted)", 3: "sredc", 4: "redc", 5: "sredc_mulhi",
+             6: "sredc_hiadd", 7: "DFMA", 8: "fmulmod", 9: "IADD", 10: "LOP3", 11: "mix3:1", 12: "mix1:1"}
+    for kind in range(13):
         for ctas in (4, 8):
             iters = 2000
             nthr = C.c_ulonglong(0)
@@ -147,8 +148,8 @@ if args.what in ("all", "pow"):
     pc = e.cpu().numpy()
     import numpy as np
     useful = int(31 * n + np.unpackbits(pc.view(np.uint8)).sum())
-    for variant in (0, 1, 2, 3, 4):
-        for ctas in (0, 8, 16):
+    for variant in (0, 2, 5, 6, 7, 8):
+        for ctas in (0,):
             cfg = m.Launch(variant=variant, ctas_per_sm=ctas)
             med, best = timeit(lambda: m.pow_vec(ctx, base, e, out=o, cfg=cfg), reps=10)
             out(what="pow", variant=variant, ctas=ctas, us=med * 1e6, useful_mulmods=useful,

@@ -176,7 +176,7 @@ def test_to_mont_alignment_in_place(m, off_in, off_out):
 # --------------------------------------------------------------------- pow
 
 @pytest.mark.parametrize("P", PRIMES + (17, 257, 2147483647, 3))
-@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("variant", list(range(9)))
 def test_pow_parity(m, P, variant):
     n = 20_003
     base = synth.uniform(42, synth.STREAM_BASE, P, 0, n, low=1) if P > 3 else \
@@ -198,24 +198,26 @@ def test_pow_full_32bit_exponents_and_big_bases(m):
     exp = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
     exp[:3] = [0xFFFFFFFF, 1 << 31, 0]
     ref = np.array([pow(int(b), int(e), P) for b, e in zip(base, exp)], dtype=np.uint32)
-    for variant in (0, 1, 2):
+    for variant in range(9):
         out = m.pow_vec(m.ctx_init(P), dev(base), dev(exp), cfg=m.Launch(variant=variant))
-        assert np.array_equal(host(out), ref)
+        assert np.array_equal(host(out), ref), variant
 
 
 @pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6, 7, 1000, 1 << 16 | 3])
-def test_pow_ragged_and_misaligned(m, n):
+@pytest.mark.parametrize("variant", [0, 5, 6])
+def test_pow_ragged_and_misaligned(m, n, variant):
     P = 469762049
     base, exp = synth.c4_inputs(P, 5, n)
     ref = oracle.power(P, base, exp)
     ctx = m.ctx_init(P)
-    assert np.array_equal(host(m.pow_vec(ctx, dev(base), dev(exp))), ref)
+    cfg = m.Launch(variant=variant)
+    assert np.array_equal(host(m.pow_vec(ctx, dev(base), dev(exp), cfg=cfg)), ref)
     tb, te = offset_view(base, 1), offset_view(exp, 1)
     to = offset_view(np.zeros_like(base), 1)
-    m.pow_vec(ctx, tb, te, out=to)
+    m.pow_vec(ctx, tb, te, out=to, cfg=cfg)
     assert np.array_equal(host(to), ref)
     tb, te = offset_view(base, 1), offset_view(exp, 2)
-    assert np.array_equal(host(m.pow_vec(ctx, tb, te)), ref)
+    assert np.array_equal(host(m.pow_vec(ctx, tb, te, cfg=cfg)), ref)
 
 
 # ----------------------------------------------------------------- twiddle
