@@ -1,0 +1,67 @@
+/*
+ * mont_host.h -- host-buffer entry points of libmont.so (the end-to-end path).
+ *
+ * Same operations as mont.h, but every array is in HOST memory.  The library
+ * streams the arrays through a caller-supplied device workspace in chunks with
+ * a 3-stage pipeline: the host->device copy of chunk i+1, the kernel on chunk i
+ * and the device->host copy of chunk i-1 run concurrently on three internal
+ * streams (two copy engines + the SMs), so a call costs ~max(bytes in, bytes
+ * out) / PCIe bandwidth instead of their sum.  Host memory must be page-locked
+ * (cudaHostAlloc / torch pin_memory) for the copies to overlap; pageable memory
+ * works but serialises.
+ *
+ * Ordering: the pipeline starts after all work previously enqueued on `stream`
+ * and `stream` waits for its completion, so the call is asynchronous like the
+ * device-pointer forms: outputs (and *acc_host) are valid once `stream` has
+ * synchronised.  Several calls may run concurrently on different streams if
+ * each has its own workspace.  The library creates and releases its internal
+ * streams/events per call; it allocates no memory.
+ *
+ * Workspace: `ws` is a device buffer of `ws_bytes`; the chunk size is derived
+ * from it (3 slots of in+out buffers).  It must hold at least
+ * mont_host_min_workspace(op) bytes.  Errors as in mont.h; MONT_EINVAL_ARG for a
+ * too-small or misaligned (16 B) workspace.
+ */
+#ifndef MONT_HOST_H_
+#define MONT_HOST_H_
+
+#include "mont.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum mont_host_op {
+    MONT_HOST_MUL_VEC = 0,      /* 2 in, 1 out (+ optional checksum)          */
+    MONT_HOST_TO_MONT = 1,      /* 1 in, 1 out                                */
+    MONT_HOST_FROM_MONT = 2,    /* 1 in, 1 out                                */
+    MONT_HOST_POW_VEC = 3,      /* 2 in, 1 out                                */
+    MONT_HOST_TWIDDLE = 4       /* 1 in, 1 out (+ the table, copied once)     */
+} mont_host_op_t;
+
+/* Smallest workspace (bytes) accepted for `op`; len = twiddle row length
+ * (ignored otherwise). */
+size_t mont_host_min_workspace(mont_host_op_t op, size_t len);
+
+/* c = REDC(a, b) elementwise (mont_mul_vec); if acc_host != NULL also
+ * *acc_host = sum_i c[i] (64-bit, overwritten, not accumulated). */
+mont_status_t mont_mul_vec_host(const mont_ctx_t *ctx, uint32_t *c_host, const uint32_t *a_host,
+                                const uint32_t *b_host, size_t n, unsigned long long *acc_host, void *ws,
+                                size_t ws_bytes, cudaStream_t stream);
+mont_status_t to_mont_host(const mont_ctx_t *ctx, uint32_t *out_host, const uint32_t *in_host, size_t n,
+                           void *ws, size_t ws_bytes, cudaStream_t stream);
+mont_status_t from_mont_host(const mont_ctx_t *ctx, uint32_t *out_host, const uint32_t *in_host, size_t n,
+                             void *ws, size_t ws_bytes, cudaStream_t stream);
+mont_status_t mont_pow_vec_host(const mont_ctx_t *ctx, uint32_t *out_host, const uint32_t *base_host,
+                                const uint32_t *exp_host, size_t n, void *ws, size_t ws_bytes,
+                                cudaStream_t stream);
+/* chunks are whole rows; the len-word table tw_host is copied once */
+mont_status_t mont_mul_twiddle_host(const mont_ctx_t *ctx, uint32_t *out_host, const uint32_t *x_host,
+                                    const uint32_t *tw_host, size_t batch, size_t len, void *ws,
+                                    size_t ws_bytes, cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MONT_HOST_H_ */

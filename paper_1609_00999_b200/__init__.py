@@ -76,7 +76,16 @@ SIGNATURES = {
     "mb_copy": (C.c_int, [_P, _P, _S, _LAUNCH, _P]),
     "mb_imad": (C.c_int, [_P, C.c_int, C.c_int, _LAUNCH, _P, C.POINTER(C.c_ulonglong)]),
     "mont_sm_count": (C.c_int, []),
+    # include/mont_host.h
+    "mont_host_min_workspace": (C.c_size_t, [C.c_int, C.c_size_t]),
+    "mont_mul_vec_host": (C.c_int, [_CTX, _P, _P, _P, _S, _P, _P, _S, _P]),
+    "to_mont_host": (C.c_int, [_CTX, _P, _P, _S, _P, _S, _P]),
+    "from_mont_host": (C.c_int, [_CTX, _P, _P, _S, _P, _S, _P]),
+    "mont_pow_vec_host": (C.c_int, [_CTX, _P, _P, _P, _S, _P, _S, _P]),
+    "mont_mul_twiddle_host": (C.c_int, [_CTX, _P, _P, _P, _S, _S, _P, _S, _P]),
 }
+
+HOST_OPS = {"mul_vec": 0, "to_mont": 1, "from_mont": 2, "pow_vec": 3, "twiddle": 4}
 
 
 def lib():
@@ -277,6 +286,64 @@ def synth_fill(out, seed: int, stream_id: int, start: int, p: int, mode: int = 0
     _check(lib().synth_fill(_ptr(out), out.numel(), seed, stream_id, start, p, mode, int(bool(specials)),
                             _stream_handle(stream)), "synth_fill")
     return out
+
+
+# ----------------------------------------------------- host-buffer forms (e2e)
+
+def _host_u32(t, name):
+    torch = _torch()
+    if not isinstance(t, torch.Tensor) or t.is_cuda:
+        raise TypeError(f"{name} must be a CPU (ideally pinned) torch tensor")
+    if t.dtype not in (torch.uint32, torch.int32) or not t.is_contiguous():
+        raise TypeError(f"{name} must be a contiguous uint32 CPU tensor")
+    return t
+
+
+def host_workspace(op: str, length: int = 0, min_bytes: int = 256 << 20, device="cuda"):
+    """A device workspace for the host-buffer forms (include/mont_host.h)."""
+    torch = _torch()
+    need = int(lib().mont_host_min_workspace(HOST_OPS[op], length))
+    return torch.empty(max(need, min_bytes), dtype=torch.uint8, device=device)
+
+
+def mul_vec_host(ctx: Ctx, a, b, out, ws, want_checksum: bool = False, stream=None):
+    """out = REDC(a, b) for HOST tensors, streamed through device workspace `ws`.
+    Returns a pinned int64 scalar tensor holding sum(out) if want_checksum (valid after sync)."""
+    torch = _torch()
+    for t, nme in ((a, "a"), (b, "b"), (out, "out")):
+        _host_u32(t, nme)
+    if not (a.numel() == b.numel() == out.numel()):
+        raise ValueError("length mismatch")
+    acc = torch.zeros(1, dtype=torch.int64, pin_memory=True) if want_checksum else None
+    _check(lib().mont_mul_vec_host(C.byref(ctx), _ptr(out), _ptr(a), _ptr(b), a.numel(),
+                                   _ptr(acc) if acc is not None else None, _ptr(ws), ws.numel(),
+                                   _stream_handle(stream)), "mont_mul_vec_host")
+    return acc
+
+
+def to_mont_host(ctx: Ctx, x, out, ws, stream=None):
+    _host_u32(x, "x"), _host_u32(out, "out")
+    _check(lib().to_mont_host(C.byref(ctx), _ptr(out), _ptr(x), x.numel(), _ptr(ws), ws.numel(),
+                              _stream_handle(stream)), "to_mont_host")
+
+
+def from_mont_host(ctx: Ctx, x, out, ws, stream=None):
+    _host_u32(x, "x"), _host_u32(out, "out")
+    _check(lib().from_mont_host(C.byref(ctx), _ptr(out), _ptr(x), x.numel(), _ptr(ws), ws.numel(),
+                                _stream_handle(stream)), "from_mont_host")
+
+
+def pow_vec_host(ctx: Ctx, base, exp, out, ws, stream=None):
+    _host_u32(base, "base"), _host_u32(exp, "exp"), _host_u32(out, "out")
+    _check(lib().mont_pow_vec_host(C.byref(ctx), _ptr(out), _ptr(base), _ptr(exp), base.numel(), _ptr(ws),
+                                   ws.numel(), _stream_handle(stream)), "mont_pow_vec_host")
+
+
+def mul_twiddle_host(ctx: Ctx, x, tw, out, ws, stream=None):
+    _host_u32(x, "x"), _host_u32(tw, "tw"), _host_u32(out, "out")
+    batch, length = x.shape
+    _check(lib().mont_mul_twiddle_host(C.byref(ctx), _ptr(out), _ptr(x), _ptr(tw), batch, length, _ptr(ws),
+                                       ws.numel(), _stream_handle(stream)), "mont_mul_twiddle_host")
 
 
 def sm_count() -> int:

@@ -1,0 +1,179 @@
+"""Full-size parity at BASELINE.json's configs, in the launch configuration bench.py times
+(the library defaults), through the C ABI.
+
+Inputs are generated in HBM by the device generator (itself checked against synth/ in
+test_gpu_synth.py).  Checks: (1) sampled outputs against the oracle computed element by
+element from synth/ (the host generator) at the same indices; (2) properties that hold at any
+size, checked on every element with torch int64 arithmetic on the GPU (independent of our
+kernels): the Montgomery identity c*2^32 = a*b (mod P) with 0 <= c < P; (3) checksums against
+an independent torch reduction.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+P0, P1, P2 = synth.CONFIG_PRIMES
+SAMPLES = 20_000
+
+
+@pytest.fixture(scope="module")
+def m():
+    import paper_1609_00999_b200 as mod
+    return mod
+
+
+def i64(t):
+    return t.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+
+
+def identity_all(P, a, b, c, chunk=1 << 24):
+    for s in range(0, a.numel(), chunk):
+        aa, bb, cc = i64(a[s:s + chunk]), i64(b[s:s + chunk]), i64(c[s:s + chunk])
+        if not bool(((cc << 32) % P == (aa * bb) % P).all()) or not bool((cc < P).all()):
+            return False
+    return True
+
+
+def sample_idx(n, k=SAMPLES, seed=0):
+    rng = np.random.default_rng(seed)
+    idx = np.unique(np.concatenate([rng.integers(0, n, k), np.arange(8), np.arange(n - 8, n)]))
+    return idx.astype(np.int64)
+
+
+def gen(n, stream_id, P, mode=0, specials=False, start=0, m=None):
+    t = torch.empty(n, dtype=torch.uint32, device="cuda")
+    m.synth_fill(t, 42, stream_id, start, P, mode, specials)
+    return t
+
+
+@pytest.mark.parametrize("P", [P0, P1, P2])
+def test_c2_fullsize(m, P):
+    """configs[1]: n = 2^26, 1 % specials, fused mul+checksum (the bench launch)."""
+    n = 1 << 26
+    a = gen(n, 1, P, 0, True, m=m)
+    b = gen(n, 2, P, 0, True, m=m)
+    c, acc = m.mul_vec_checksum(m.ctx_init(P), a, b)
+    torch.cuda.synchronize()
+    idx = sample_idx(n)
+    ha, hb = synth.c2_inputs_at(P, idx.astype(np.uint64))
+    ref = oracle.mont_mul(P, ha, hb)
+    assert np.array_equal(c.cpu().numpy()[idx], ref)
+    assert identity_all(P, a, b, c)
+    assert int(acc.item()) == int(i64(c).sum().item())
+    # the plain mul_vec entry point gives the same array
+    c2 = m.mul_vec(m.ctx_init(P), a, b)
+    assert bool((c2.view(torch.int32) == c.view(torch.int32)).all())
+
+
+def test_c1_full(m):
+    """configs[0] exactly: full array vs the oracle, and its checksum."""
+    a, b = synth.c1_inputs(P0)
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    c, acc = m.mul_vec_checksum(m.ctx_init(P0), ta, tb)
+    ref = oracle.mont_mul(P0, a, b)
+    assert np.array_equal(c.cpu().numpy(), ref)
+    assert int(acc.item()) % P0 == oracle.checksum(P0, ref)
+    assert c[0].item() == 0 and c[1].item() == 0
+
+
+def test_c3_fullsize(m):
+    """configs[2]: 4096 x 2^14 against tw[j] = to_mont(w^j), w = 31^((P-1)/2^14)."""
+    batch, L = 4096, 1 << 14
+    x = gen(batch * L, 5, P0, m=m).view(batch, L)
+    w = oracle.root_of_unity(P0, synth.G11_GENERATOR, L)
+    tw_ref = oracle.twiddle_table(P0, w, L)
+    ctx = m.ctx_init(P0)
+    tw = m.twiddle_table(ctx, w, L)
+    assert np.array_equal(tw.cpu().numpy(), tw_ref)
+    out = m.mul_twiddle(ctx, x, tw)
+    torch.cuda.synchronize()
+    idx = sample_idx(batch * L)
+    hx = synth.uniform_at(42, 5, P0, idx.astype(np.uint64))
+    ref = oracle.mont_mul(P0, hx, tw_ref[idx % L])
+    assert np.array_equal(out.view(-1).cpu().numpy()[idx], ref)
+    # x * w^j in the plain domain for a few (r, j), via Python's pow
+    ho = out.cpu().numpy()
+    for r, j in [(0, 0), (0, 1), (4095, 16383), (77, 8192), (1234, 4321)]:
+        assert int(ho[r, j]) == (int(x[r, j].item()) * pow(w, j, P0)) % P0
+    twx = tw.view(torch.int32).view(1, -1).expand(512, -1).contiguous().view(torch.uint32).view(-1)
+    for r in range(0, batch, 512):
+        assert identity_all(P0, x[r:r + 512].reshape(-1), twx, out[r:r + 512].reshape(-1))
+
+
+def test_c4_fullsize(m):
+    """configs[3]: 2^24 bases in [1,P), 31-bit exponents, P = 469762049 (bench launch)."""
+    n = 1 << 24
+    base = gen(n, 3, P1, 1, m=m)
+    e = gen(n, 4, P1, 2, m=m)
+    out = m.pow_vec(m.ctx_init(P1), base, e)
+    torch.cuda.synchronize()
+    idx = sample_idx(n, 50_000)
+    hb = synth.uniform_at(42, 3, P1, idx.astype(np.uint64), low=1)
+    he = synth.exponents_at(42, 4, idx.astype(np.uint64))
+    assert np.array_equal(out.cpu().numpy()[idx], oracle.power(P1, hb, he))
+
+
+def test_to_from_fullsize(m):
+    n = 1 << 26
+    a = gen(n, 1, P0, 0, True, m=m)
+    ctx = m.ctx_init(P0)
+    abar = m.to_mont(ctx, a)
+    back = m.from_mont(ctx, abar)
+    torch.cuda.synchronize()
+    assert bool((back.view(torch.int32) == a.view(torch.int32)).all())
+    idx = sample_idx(n)
+    assert np.array_equal(abar.cpu().numpy()[idx], oracle.to_mont(P0, a.cpu().numpy()[idx]))
+    one = torch.ones(n, dtype=torch.int32, device="cuda").view(torch.uint32)
+    assert identity_all(P0, abar, one, a)
+
+
+@pytest.mark.parametrize("P", [P0, P1, P2])
+def test_exhaustive_closed_forms(m, P):
+    """All a in [0, P) against b in {0, 1, 1-bar, R^2 mod P, P-1} (SURVEY §8(c) pins), on the GPU."""
+    ctx = m.ctx_init(P)
+    chunk = 1 << 28
+    for s in range(0, P, chunk):
+        n = min(chunk, P - s)
+        a = torch.arange(s, s + n, dtype=torch.int64, device="cuda").to(torch.int32).view(torch.uint32)
+        full = lambda v: torch.full((n,), v, dtype=torch.int64, device="cuda").to(torch.int32).view(torch.uint32)
+        eq = lambda x, y: bool((x.view(torch.int32) == y.view(torch.int32)).all())
+        assert eq(m.mul_vec(ctx, a, full(ctx.r1)), a)                         # 1-bar is the identity
+        assert bool((m.mul_vec(ctx, a, full(0)).view(torch.int32) == 0).all())
+        assert eq(m.mul_vec(ctx, a, full(1)), m.from_mont(ctx, a))
+        tm = m.to_mont(ctx, a)
+        assert eq(m.mul_vec(ctx, a, full(ctx.r2)), tm)
+        assert eq(m.from_mont(ctx, tm), a)                                    # round trip, every x < P
+        neg = m.mul_vec(ctx, a, full(P - 1))                                  # -a R^-1
+        fa = i64(m.from_mont(ctx, a))
+        assert bool(((i64(neg) + fa) % P == 0).all())
+        del a, tm, neg, fa
+        torch.cuda.empty_cache()
+
+
+def test_c5_fullsize(m):
+    """configs[4] at W = 1: n = 2^31 (64-bit indexing), fused mul + checksum, P = 2013265921."""
+    n = 1 << 31
+    free, _ = torch.cuda.mem_get_info()
+    if free < 3 * 4 * n + (4 << 30):
+        pytest.skip("not enough device memory for 3 x 8 GiB")
+    a = gen(n, 1, P0, m=m)
+    b = gen(n, 2, P0, m=m)
+    c, acc = m.mul_vec_checksum(m.ctx_init(P0), a, b)
+    torch.cuda.synchronize()
+    idx = sample_idx(n)
+    ha, hb = synth.c5_inputs(P0, 0, 8)
+    assert np.array_equal(c[:8].cpu().numpy(), oracle.mont_mul(P0, ha, hb))
+    ia = torch.from_numpy(idx).cuda()
+    hs_a = synth.uniform_at(42, 1, P0, idx.astype(np.uint64))
+    hs_b = synth.uniform_at(42, 2, P0, idx.astype(np.uint64))
+    assert np.array_equal(c.view(torch.int32)[ia].cpu().numpy().view(np.uint32), oracle.mont_mul(P0, hs_a, hs_b))
+    assert identity_all(P0, a, b, c, chunk=1 << 26)
+    tot = 0
+    for s in range(0, n, 1 << 28):
+        tot += int(i64(c[s:s + (1 << 28)]).sum().item())
+    assert int(acc.item()) == tot
