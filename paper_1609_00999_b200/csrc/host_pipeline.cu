@@ -63,7 +63,7 @@ template <class Pre, class Launch, class Post>
 mont_status_t pipeline(int nin, const uint32_t *const *host_in, uint32_t *host_out, size_t units, size_t unit_words,
                        void *ws, size_t ws_bytes, size_t reserved, cudaStream_t user, Pre pre, Launch launch,
                        Post post) {
-    if (((uintptr_t)ws & 15u) || ws_bytes < reserved) return MONT_EINVAL_ARG;
+    if (((uintptr_t)ws & 15u) || ws_bytes < align_up(reserved) + kAlign) return MONT_EINVAL_ARG;
     const size_t nbuf = (size_t)nin + 1;
     const size_t per_unit = unit_words * 4;
     const size_t avail = ws_bytes - align_up(reserved);

@@ -154,3 +154,29 @@ if args.what in ("all", "pow"):
             med, best = timeit(lambda: m.pow_vec(ctx, base, e, out=o, cfg=cfg), reps=10)
             out(what="pow", variant=variant, ctas=ctas, us=med * 1e6, useful_mulmods=useful,
                 tmulmod=useful / med / 1e12)
+
+if args.what in ("pcie",):
+    n = 1 << 26   # 256 MiB
+    hs = [torch.empty(n, dtype=torch.uint32, pin_memory=True) for _ in range(2)]
+    ds = [torch.empty(n, dtype=torch.uint32, device=dev) for _ in range(2)]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    med, _ = timeit(lambda: ds[0].copy_(hs[0], non_blocking=True), reps=5)
+    out(what="h2d", gbs=4 * n / med / 1e9)
+    med, _ = timeit(lambda: hs[1].copy_(ds[1], non_blocking=True), reps=5)
+    out(what="d2h", gbs=4 * n / med / 1e9)
+
+    def both():
+        ev = torch.cuda.Event()
+        ev.record()
+        s1.wait_event(ev)
+        s2.wait_event(ev)
+        with torch.cuda.stream(s1):
+            ds[0].copy_(hs[0], non_blocking=True)
+        with torch.cuda.stream(s2):
+            hs[1].copy_(ds[1], non_blocking=True)
+        torch.cuda.current_stream().wait_stream(s1)
+        torch.cuda.current_stream().wait_stream(s2)
+    med, _ = timeit(both, reps=5)
+    out(what="h2d+d2h concurrent", gbs_each=4 * n / med / 1e9, gbs_total=8 * n / med / 1e9)
+    import subprocess
+    out(what="nvidia-smi topo", txt=subprocess.run(["nvidia-smi", "-q", "-d", "PCIE"], capture_output=True, text=True).stdout[-1500:])
