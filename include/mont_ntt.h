@@ -1,0 +1,40 @@
+/*
+ * mont_ntt.h -- number-theoretic transform on top of the Montgomery product
+ * (SURVEY.md §8(f) NEXT #1): the consumer of the paper's vectorised Montgomery
+ * multiplication, its "modular FFT" libraries.  Same
+ * conventions as mont.h (device pointers, asynchronous on `stream`, status
+ * codes, no global state, no allocation).
+ */
+#ifndef MONT_NTT_H_
+#define MONT_NTT_H_
+
+#include "mont.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* In-place batched NTT of `batch` rows of N = 2^log_n canonical residues
+ * (row r at data + r*N, natural order in and out):
+ *     X[k] = s * sum_{j<N} x[j] w^(j k)  mod P
+ * tw    : N/2 twiddles in Montgomery form, tw[j] = to_mont(w^j) (e.g. from
+ *         mont_twiddle_table(ctx, tw, w, N/2)), w a primitive N-th root of
+ *         unity mod P.  Passing the table of w^-1 gives the inverse transform.
+ * scale : the output factor s in Montgomery form (to_mont(s)); ctx->r1 means
+ *         s = 1 (no extra multiply); to_mont(N^-1) with the w^-1 table makes
+ *         the normalised inverse.
+ * Radix-2 Cooley-Tukey (decimation in time, bit-reversed load) with each
+ * butterfly u' = u + REDC(v, tw), v' = u - REDC(v, tw) on plain residues, mod
+ * add/sub by one conditional correction ("straightforward").  One
+ * CTA per row; the row lives in shared memory for all log_n stages, so HBM
+ * traffic is 8 bytes per element.  1 <= log_n <= 15 (N <= 32768 words = 128 KiB
+ * of shared memory), else MONT_EUNSUPPORTED.  data 4-byte aligned; tw, data
+ * device pointers; rows may not overlap. */
+mont_status_t mont_ntt(const mont_ctx_t *ctx, uint32_t *data, size_t batch, int log_n, const uint32_t *tw,
+                       uint32_t scale, cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MONT_NTT_H_ */

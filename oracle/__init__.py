@@ -79,6 +79,10 @@ def lib():
         L.oracle_fourier_redc.argtypes = [C.POINTER(Ctx), C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                           C.POINTER(C.c_int64), C.POINTER(C.c_uint64)]
         L.oracle_fourier_redc.restype = C.c_uint32
+        L.oracle_dft.argtypes = [C.c_uint32, C.c_uint32, _U32P, _U32P, C.c_size_t]
+        L.oracle_cyclic_conv.argtypes = [C.c_uint32, _U32P, _U32P, _U32P, C.c_size_t]
+        L.oracle_inverse.argtypes = [C.c_uint32, C.c_uint32]
+        L.oracle_inverse.restype = C.c_uint32
         L.oracle_mod_add.argtypes = [C.c_uint32] * 3
         L.oracle_mod_add.restype = C.c_uint32
         L.oracle_mod_sub.argtypes = [C.c_uint32] * 3
@@ -219,3 +223,26 @@ def mod_add(a: int, b: int, P: int) -> int:
 
 def mod_sub(a: int, b: int, P: int) -> int:
     return int(lib().oracle_mod_sub(a, b, P))
+
+
+# NTT by definition -----------------------------------
+
+def dft(P: int, w: int, x) -> np.ndarray:
+    """X[k] = sum_j x[j] w^(jk) mod P for each row of x (O(N^2) per row)."""
+    x = _u32(x)
+    rows = x.reshape(-1, x.shape[-1])
+    out = np.empty_like(rows)
+    for r in range(rows.shape[0]):
+        lib().oracle_dft(P, w, np.ascontiguousarray(rows[r]), out[r], rows.shape[1])
+    return out.reshape(x.shape)
+
+
+def cyclic_conv(P: int, a, b) -> np.ndarray:
+    a, b = _u32(a), _u32(b)
+    out = np.empty_like(a)
+    lib().oracle_cyclic_conv(P, a, b, out, a.size)
+    return out
+
+
+def inverse(x: int, P: int) -> int:
+    return int(lib().oracle_inverse(x, P))

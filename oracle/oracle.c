@@ -334,3 +334,47 @@ uint32_t oracle_fourier_redc(const oracle_ctx_t *c, uint32_t cc, uint32_t n, uin
 uint32_t oracle_mod_add(uint32_t a, uint32_t b, uint32_t P) { return (uint32_t)(((uint64_t)a + b) % P); }
 uint32_t oracle_mod_sub(uint32_t a, uint32_t b, uint32_t P)
 { return (uint32_t)(((uint64_t)a + P - (b % P)) % P); }
+
+/* ------------------------------------------------ NTT
+ *
+ * The number-theoretic transform the paper's generated modular FFT libraries
+ * compute, by DEFINITION: for a primitive N-th root of
+ * unity w mod P,
+ *     X[k] = sum_{j<N} x[j] * w^(j k)  mod P,    k < N            (O(N^2))
+ * and the cyclic convolution c[k] = sum_j a[j] b[(k - j) mod N] mod P, also by
+ * definition.  Powers w^e are taken from a table of w^0..w^(N-1) built by
+ * repeated naive multiplication; exponents are reduced mod N (w^N = 1). */
+void oracle_dft(uint32_t P, uint32_t w, const uint32_t *x, uint32_t *X, size_t N)
+{
+    uint32_t *pw = (uint32_t *)malloc(N * sizeof(uint32_t));
+    uint32_t acc = 1u % P;
+    for (size_t e = 0; e < N; ++e) { pw[e] = acc; acc = mulmod_naive(acc, w, P); }
+    for (size_t k = 0; k < N; ++k) {
+        uint64_t s = 0;
+        for (size_t j = 0; j < N; ++j) {
+            s += mulmod_naive(x[j] % P, pw[(j * k) % N], P);
+            s %= P;
+        }
+        X[k] = (uint32_t)s;
+    }
+    free(pw);
+}
+
+void oracle_cyclic_conv(uint32_t P, const uint32_t *a, const uint32_t *b, uint32_t *c, size_t N)
+{
+    for (size_t k = 0; k < N; ++k) {
+        uint64_t s = 0;
+        for (size_t j = 0; j < N; ++j) {
+            s += mulmod_naive(a[j] % P, b[(k + N - j) % N] % P, P);
+            s %= P;
+        }
+        c[k] = (uint32_t)s;
+    }
+}
+
+/* modular inverse by extended Euclid (P:89's tool), 0 if not invertible */
+uint32_t oracle_inverse(uint32_t x, uint32_t P)
+{
+    int64_t r = ext_euclid_inverse((int64_t)(x % P), (int64_t)P);
+    return r < 0 ? 0u : (uint32_t)r;
+}

@@ -85,6 +85,8 @@ SIGNATURES = {
     "mont_mul_twiddle_host": (C.c_int, [_CTX, _P, _P, _P, _S, _S, _P, _S, _P]),
 }
 
+SIGNATURES["mont_ntt"] = (C.c_int, [_CTX, _P, _S, C.c_int, _P, C.c_uint32, _P])
+
 HOST_OPS = {"mul_vec": 0, "to_mont": 1, "from_mont": 2, "pow_vec": 3, "twiddle": 4}
 
 
@@ -344,6 +346,21 @@ def mul_twiddle_host(ctx: Ctx, x, tw, out, ws, stream=None):
     batch, length = x.shape
     _check(lib().mont_mul_twiddle_host(C.byref(ctx), _ptr(out), _ptr(x), _ptr(tw), batch, length, _ptr(ws),
                                        ws.numel(), _stream_handle(stream)), "mont_mul_twiddle_host")
+
+
+def ntt(ctx: Ctx, data, tw, scale: int | None = None, stream=None):
+    """In-place batched NTT of the rows of `data` (batch, N), N = 2^k <= 32768 (include/mont_ntt.h).
+    tw: device table of N/2 Montgomery twiddles; scale: Montgomery form of the output factor."""
+    _dev_u32(data, "data"), _dev_u32(tw, "tw")
+    if data.dim() != 2:
+        raise ValueError("data must be (batch, N)")
+    batch, n = data.shape
+    log_n = n.bit_length() - 1
+    if n != 1 << log_n or tw.numel() < n // 2:
+        raise ValueError("N must be a power of two and tw must hold N/2 entries")
+    _check(lib().mont_ntt(C.byref(ctx), _ptr(data), batch, log_n, _ptr(tw), ctx.r1 if scale is None else scale,
+                          _stream_handle(stream)), "mont_ntt")
+    return data
 
 
 def sm_count() -> int:

@@ -1,0 +1,98 @@
+"""GPU NTT (include/mont_ntt.h) vs the oracle's definition-DFT, inverse and convolution."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+GEN = {2013265921: 31, 469762049: 3, 998244353: 3}
+
+
+@pytest.fixture(scope="module")
+def m():
+    import paper_1609_00999_b200 as mod
+    return mod
+
+
+def tables(m, P, N):
+    ctx = m.ctx_init(P)
+    w = oracle.root_of_unity(P, GEN[P], N)
+    winv = oracle.inverse(w, P)
+    half = max(1, N // 2)
+    tw = m.twiddle_table(ctx, w, half)
+    twi = m.twiddle_table(ctx, winv, half)
+    ninv_m = int(oracle.to_mont(P, np.array([oracle.inverse(N, P)], np.uint32))[0])
+    return ctx, w, winv, tw, twi, ninv_m
+
+
+@pytest.mark.parametrize("P", list(GEN))
+@pytest.mark.parametrize("log_n", [1, 2, 3, 5, 6, 8, 10, 11, 12])
+def test_ntt_vs_dft(m, P, log_n):
+    N = 1 << log_n
+    batch = 3
+    ctx, w, winv, tw, twi, ninv_m = tables(m, P, N)
+    x = synth.uniform(42, 21, P, 0, batch * N).reshape(batch, N)
+    x[0, :2] = [0, P - 1]
+    d = torch.from_numpy(x).cuda()
+    m.ntt(ctx, d, tw)
+    X = d.cpu().numpy()
+    assert np.array_equal(X, oracle.dft(P, w, x))
+    m.ntt(ctx, d, twi, scale=ninv_m)
+    assert np.array_equal(d.cpu().numpy(), x)
+
+
+@pytest.mark.parametrize("log_n", [13, 14, 15])
+def test_ntt_large_properties(m, log_n):
+    P = 998244353
+    N = 1 << log_n
+    ctx, w, winv, tw, twi, ninv_m = tables(m, P, N)
+    x = synth.uniform(42, 22, P, 0, 2 * N).reshape(2, N)
+    d = torch.from_numpy(x).cuda()
+    m.ntt(ctx, d, tw)
+    X = d.cpu().numpy()
+    xs = [int(v) for v in x[1]]
+    for k in (0, 1, 2, N // 2, N - 1, 12345 % N):
+        wk = pow(w, k, P)
+        acc, pw = 0, 1
+        for v in xs:
+            acc = (acc + v * pw) % P
+            pw = pw * wk % P
+        assert int(X[1, k]) == acc
+    m.ntt(ctx, d, twi, scale=ninv_m)
+    assert np.array_equal(d.cpu().numpy(), x)
+
+
+@pytest.mark.parametrize("log_n", [4, 9, 12])
+def test_ntt_convolution(m, log_n):
+    P = 2013265921
+    N = 1 << log_n
+    ctx, w, winv, tw, twi, ninv_m = tables(m, P, N)
+    a = synth.uniform(42, 23, P, 0, N)
+    b = synth.uniform(42, 24, P, 0, N)
+    da, db = torch.from_numpy(a.reshape(1, N)).cuda(), torch.from_numpy(b.reshape(1, N)).cuda()
+    m.ntt(ctx, da, tw)
+    m.ntt(ctx, db, tw)
+    # pointwise product of the transforms: REDC(A, to_mont(B)) = A B mod P, via the library
+    prod = m.mul_vec(ctx, da.view(-1), m.to_mont(ctx, db.view(-1))).view(1, N)
+    m.ntt(ctx, prod, twi, scale=ninv_m)
+    assert np.array_equal(prod.cpu().numpy().reshape(-1), oracle.cyclic_conv(P, a, b))
+
+
+def test_ntt_many_rows_and_validation(m):
+    P = 469762049
+    N = 1 << 10
+    ctx, w, winv, tw, twi, ninv_m = tables(m, P, N)
+    x = synth.uniform(42, 25, P, 0, 300 * N).reshape(300, N)
+    d = torch.from_numpy(x).cuda()
+    m.ntt(ctx, d, tw)
+    X = d.cpu().numpy()
+    for r in (0, 1, 150, 299):
+        assert np.array_equal(X[r], oracle.dft(P, w, x[r]))
+    import ctypes as C
+    L = m.lib()
+    assert L.mont_ntt(C.byref(ctx), d.data_ptr(), 1, 16, tw.data_ptr(), ctx.r1, None) == 4
+    assert L.mont_ntt(C.byref(ctx), d.data_ptr(), 1, 0, tw.data_ptr(), ctx.r1, None) == 4
+    assert L.mont_ntt(C.byref(ctx), d.data_ptr(), 0, 10, tw.data_ptr(), ctx.r1, None) == 0
+    assert L.mont_ntt(C.byref(ctx), d.data_ptr(), 1, 10, tw.data_ptr(), P, None) == 2

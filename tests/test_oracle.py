@@ -301,3 +301,50 @@ def test_alg3_fourier_redc(P, l):
         assert r3 == 0
         assert -(P - 1) <= traw <= 2 * (P - 1)                   # PAPER.md:117 (interval reading G7)
         assert (t * (1 << l) - a * b) % P == 0 and 0 <= t < P
+
+
+# ------------------------------------------------------------- NTT (NEXT #1)
+
+@pytest.mark.parametrize("P", CONFIG_PRIMES)
+@pytest.mark.parametrize("N", [1, 2, 4, 8, 64, 256])
+def test_dft_pins(P, N):
+    """Pins for the definition-DFT: delta -> ones, ones -> N e0, e1 -> powers of w, inverse round trip,
+    and the convolution theorem against the (independent) definition of cyclic convolution."""
+    w = oracle.root_of_unity(P, {2013265921: 31, 469762049: 3, 998244353: 3}[P], N)
+    assert pow(w, N, P) == 1 and (N == 1 or pow(w, N // 2, P) == P - 1)
+    e0 = np.zeros(N, np.uint32)
+    e0[0] = 1
+    assert np.all(oracle.dft(P, w, e0) == 1)
+    ones = np.ones(N, np.uint32)
+    ref = np.zeros(N, np.uint32)
+    ref[0] = N % P
+    assert np.array_equal(oracle.dft(P, w, ones), ref)
+    if N > 1:
+        e1 = np.zeros(N, np.uint32)
+        e1[1] = 1
+        assert [int(v) for v in oracle.dft(P, w, e1)] == [pow(w, k, P) for k in range(N)]
+    rng = np.random.default_rng(N)
+    x = rng.integers(0, P, N, dtype=np.uint64).astype(np.uint32)
+    X = oracle.dft(P, w, x)
+    winv = oracle.inverse(w, P)
+    assert (winv * w) % P == 1
+    ninv = oracle.inverse(N, P)
+    back = (oracle.dft(P, winv, X).astype(np.uint64) * ninv % P).astype(np.uint32)
+    assert np.array_equal(back, x)
+    a = rng.integers(0, P, N, dtype=np.uint64).astype(np.uint32)
+    b = rng.integers(0, P, N, dtype=np.uint64).astype(np.uint32)
+    prod = (oracle.dft(P, w, a).astype(np.uint64) * oracle.dft(P, w, b) % P).astype(np.uint32)
+    conv = (oracle.dft(P, winv, prod).astype(np.uint64) * ninv % P).astype(np.uint32)
+    assert np.array_equal(conv, oracle.cyclic_conv(P, a, b))
+
+
+def test_cyclic_conv_small_integers():
+    """Cyclic convolution of small integers equals numpy's exact integer convolution folded mod N."""
+    P, N = 998244353, 16
+    rng = np.random.default_rng(3)
+    a = rng.integers(0, 100, N).astype(np.uint32)
+    b = rng.integers(0, 100, N).astype(np.uint32)
+    full = np.convolve(a.astype(np.int64), b.astype(np.int64))
+    folded = full[:N].copy()
+    folded[:N - 1] += full[N:]
+    assert np.array_equal(oracle.cyclic_conv(P, a, b), folded.astype(np.uint32))
