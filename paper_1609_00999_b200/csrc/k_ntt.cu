@@ -55,6 +55,81 @@ __global__ void __launch_bounds__(1024) k_ntt_smem(Ctx c, uint32_t *data, int lo
     }
 }
 
+// ---- register-blocked radix-2 NTT: 32 elements per thread, 5 stages per
+// trip through shared memory.
+//
+// Thread t of a row owns, in trip g, the 32 elements whose index bits
+// [ws, ws+5) vary and whose other bits are fixed by t (ws = min(5g, log_n-5));
+// the 5 butterfly stages whose pair distance is one of those bits run entirely
+// in registers, so a row of N = 2^log_n crosses shared memory only
+// ceil(log_n / 5) + 1 times instead of log_n.  Shared memory addresses are
+// XOR-swizzled, a ^ (((a >> 5) ^ (a >> 10)) & 31): a bijection on [0, 2^15)
+// that makes every access pattern used here (coalesced natural order, the
+// bit-reversed scatter of the load, and each trip's gather) bank-conflict free
+// (checked exhaustively for log_n = 10..15 offline; scripts/ntt_swizzle.py).
+__device__ __forceinline__ uint32_t swz(uint32_t a) { return a ^ (((a >> 5) ^ (a >> 10)) & 31u); }
+
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) k_ntt_r32(Ctx c, uint32_t *data, size_t batch, int log_n,
+                                                      const uint32_t *__restrict__ tw, uint32_t scale) {
+    extern __shared__ uint32_t sm[];
+    const uint32_t N = 1u << log_n, T = N >> 5;
+    const uint32_t rl = threadIdx.x / T, t = threadIdx.x - rl * T;
+    const size_t row = (size_t)blockIdx.x * (blockDim.x / T) + rl;
+    const bool live = row < batch;
+    uint32_t *s = sm + (size_t)rl * N;
+    uint32_t *g = data + row * N;
+    uint32_t v[32];
+    if (live) {
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k) {
+            const uint32_t idx = t + (uint32_t)k * T;
+            s[swz(__brev(idx) >> (32 - log_n))] = ld_stream1(g + idx);
+        }
+    }
+    __syncthreads();
+    for (int s0 = 0; s0 < log_n; s0 += 5) {
+        const int ws = s0 < log_n - 5 ? s0 : log_n - 5;
+        const uint32_t tl = t & ((1u << ws) - 1u);
+        const uint32_t base = tl | ((t >> ws) << (ws + 5));
+#pragma unroll
+        for (int k = 0; k < 32; ++k) v[k] = s[swz(base | ((uint32_t)k << ws))];
+#pragma unroll
+        for (int lb = 0; lb < 5; ++lb) {
+            const int st = ws + lb + 1;  // stage: pair distance 2^(st-1)
+            if (st <= s0) continue;      // done by the previous trip (last, overlapping window)
+            const int tsh = log_n - st;
+            // the 2^lb distinct twiddles of this stage for this thread:
+            // index (i mod 2^(st-1)) << (log_n - st) with i = base | k0 << ws
+            uint32_t wv[16];
+#pragma unroll
+            for (int j = 0; j < (1 << lb); ++j) wv[j] = __ldg(tw + ((tl | ((uint32_t)j << ws)) << tsh));
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int k0 = ((q >> lb) << (lb + 1)) | (q & ((1 << lb) - 1));
+                const int k1 = k0 | (1 << lb);
+                const uint32_t w = wv[k0 & ((1 << lb) - 1)];
+                const uint32_t x1 = redc(v[k1], w, c.p, c.pinv);
+                const uint32_t u = v[k0];
+                v[k0] = mod_add(u, x1, c.p);
+                v[k1] = mod_sub(u, x1, c.p);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 32; ++k) s[swz(base | ((uint32_t)k << ws))] = v[k];
+        __syncthreads();
+    }
+    if (live) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            const uint32_t idx = t + (uint32_t)k * T;
+            uint32_t x = s[swz(idx)];
+            if (scale != c.r1) x = redc(x, scale, c.p, c.pinv);
+            st_stream1(g + idx, x);
+        }
+    }
+}
+
 }  // namespace mont
 
 using namespace mont;
@@ -67,6 +142,25 @@ extern "C" mont_status_t mont_ntt(const mont_ctx_t *ctx, uint32_t *data, size_t 
     if (!data || !tw || ((uintptr_t)data & 3u) || ((uintptr_t)tw & 3u) || scale >= ctx->p) return MONT_EINVAL_ARG;
     if (batch > 0x7fffffffu) return MONT_EUNSUPPORTED;
     const uint32_t N = 1u << log_n;
+    if (log_n >= 5) {
+        const uint32_t T = N >> 5;                       // threads per row
+        const uint32_t rpc = T >= 256 ? 1u : 256u / T;   // rows per CTA
+        const size_t smem = (size_t)rpc * N * 4;
+        const size_t grid = (batch + rpc - 1) / rpc;
+        if (grid > 0x7fffffffu) return MONT_EUNSUPPORTED;
+        if (rpc * T <= 512) {  // <= 512 threads: up to 128 registers, no spills
+            if (smem > 48 * 1024 && cudaFuncSetAttribute(k_ntt_r32<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         (int)smem) != cudaSuccess)
+                return MONT_ECUDA;
+            k_ntt_r32<512><<<(unsigned)grid, rpc * T, smem, stream>>>(to_dev(ctx), data, batch, log_n, tw, scale);
+        } else {
+            if (cudaFuncSetAttribute(k_ntt_r32<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+                cudaSuccess)
+                return MONT_ECUDA;
+            k_ntt_r32<1024><<<(unsigned)grid, rpc * T, smem, stream>>>(to_dev(ctx), data, batch, log_n, tw, scale);
+        }
+        return launch_status();
+    }
     int threads = (int)(N / 2 < 1024 ? N / 2 : 1024);
     if (threads < 32) threads = 32;
     const size_t smem = (size_t)N * 4;

@@ -180,3 +180,20 @@ if args.what in ("pcie",):
     out(what="h2d+d2h concurrent", gbs_each=4 * n / med / 1e9, gbs_total=8 * n / med / 1e9)
     import subprocess
     out(what="nvidia-smi topo", txt=subprocess.run(["nvidia-smi", "-q", "-d", "PCIE"], capture_output=True, text=True).stdout[-1500:])
+
+if args.what in ("ntt",):
+    P = 2013265921
+    ctx = m.ctx_init(P)
+    import numpy as np
+    for log_n in (10, 12, 13, 14, 15):
+        N = 1 << log_n
+        batch = (1 << 26) // N
+        w = pow(31, (P - 1) // N, P)
+        tw = m.twiddle_table(ctx, w, N // 2)
+        d = torch.empty(batch * N, dtype=torch.uint32, device=dev)
+        m.synth_fill(d, 42, 5, 0, P)
+        d = d.view(batch, N)
+        med, best = timeit(lambda: m.ntt(ctx, d, tw), reps=10)
+        redc = batch * (N // 2) * log_n
+        out(what="ntt", log_n=log_n, batch=batch, us=med * 1e6, gbs=8 * batch * N / med / 1e9,
+            tredc=redc / med / 1e12, frac_imad_floor=redc / med / (148 * 64 / 5 * 1.965e9))
