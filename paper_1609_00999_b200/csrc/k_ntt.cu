@@ -69,46 +69,51 @@ __global__ void __launch_bounds__(1024) k_ntt_smem(Ctx c, uint32_t *data, int lo
 // (checked exhaustively for log_n = 10..15 offline; scripts/ntt_swizzle.py).
 __device__ __forceinline__ uint32_t swz(uint32_t a) { return a ^ (((a >> 5) ^ (a >> 10)) & 31u); }
 
-template <int MAXT>
-__global__ void __launch_bounds__(MAXT, 1) k_ntt_r32(Ctx c, uint32_t *data, size_t batch, int log_n,
-                                                      const uint32_t *__restrict__ tw, uint32_t scale) {
+// LOG_N is a template parameter so every shift, window position and twiddle
+// stride is a compile-time constant.  Because the swizzle is linear over
+// GF(2) and the per-thread bits and the per-k bits of an index are disjoint,
+// swz(base | k << ws) = swz(base) ^ swz(k << ws): one LOP3 per shared-memory
+// access, and twiddle addresses become (per-thread base) + (constant offset).
+template <int LOG_N>
+__global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, 1)
+    k_ntt_r32(Ctx c, uint32_t *data, size_t batch, const uint32_t *__restrict__ tw, uint32_t scale) {
+    constexpr uint32_t N = 1u << LOG_N, T = N >> 5;
     extern __shared__ uint32_t sm[];
-    const uint32_t N = 1u << log_n, T = N >> 5;
-    const uint32_t rl = threadIdx.x / T, t = threadIdx.x - rl * T;
+    const uint32_t rl = threadIdx.x / T, t = threadIdx.x % T;
     const size_t row = (size_t)blockIdx.x * (blockDim.x / T) + rl;
     const bool live = row < batch;
     uint32_t *s = sm + (size_t)rl * N;
     uint32_t *g = data + row * N;
     uint32_t v[32];
     if (live) {
-#pragma unroll 8
-        for (int k = 0; k < 32; ++k) {
-            const uint32_t idx = t + (uint32_t)k * T;
-            s[swz(__brev(idx) >> (32 - log_n))] = ld_stream1(g + idx);
-        }
+        // element t + k T goes to bit-reversed position brev(t) | brev(k T)
+        const uint32_t bt = swz(__brev(t) >> (32 - LOG_N));
+#pragma unroll
+        for (int k = 0; k < 32; ++k) v[k] = ld_stream1(g + t + (uint32_t)k * T);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) s[bt ^ swz(__brev((uint32_t)k * T) >> (32 - LOG_N))] = v[k];
     }
     __syncthreads();
-    for (int s0 = 0; s0 < log_n; s0 += 5) {
-        const int ws = s0 < log_n - 5 ? s0 : log_n - 5;
+#pragma unroll
+    for (int s0 = 0; s0 < LOG_N; s0 += 5) {
+        const int ws = s0 < LOG_N - 5 ? s0 : LOG_N - 5;
         const uint32_t tl = t & ((1u << ws) - 1u);
         const uint32_t base = tl | ((t >> ws) << (ws + 5));
+        const uint32_t sb = swz(base);
 #pragma unroll
-        for (int k = 0; k < 32; ++k) v[k] = s[swz(base | ((uint32_t)k << ws))];
+        for (int k = 0; k < 32; ++k) v[k] = s[sb ^ swz((uint32_t)k << ws)];
 #pragma unroll
         for (int lb = 0; lb < 5; ++lb) {
             const int st = ws + lb + 1;  // stage: pair distance 2^(st-1)
             if (st <= s0) continue;      // done by the previous trip (last, overlapping window)
-            const int tsh = log_n - st;
-            // the 2^lb distinct twiddles of this stage for this thread:
-            // index (i mod 2^(st-1)) << (log_n - st) with i = base | k0 << ws
-            uint32_t wv[16];
-#pragma unroll
-            for (int j = 0; j < (1 << lb); ++j) wv[j] = __ldg(tw + ((tl | ((uint32_t)j << ws)) << tsh));
+            const int tsh = LOG_N - st;
+            // twiddle index (i mod 2^(st-1)) << (LOG_N - st) = (tl << tsh) + (j << (ws + tsh))
+            const uint32_t *twb = tw + (tl << tsh);
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
                 const int k0 = ((q >> lb) << (lb + 1)) | (q & ((1 << lb) - 1));
                 const int k1 = k0 | (1 << lb);
-                const uint32_t w = wv[k0 & ((1 << lb) - 1)];
+                const uint32_t w = __ldg(twb + ((uint32_t)(k0 & ((1 << lb) - 1)) << (ws + tsh)));
                 const uint32_t x1 = redc(v[k1], w, c.p, c.pinv);
                 const uint32_t u = v[k0];
                 v[k0] = mod_add(u, x1, c.p);
@@ -116,18 +121,33 @@ __global__ void __launch_bounds__(MAXT, 1) k_ntt_r32(Ctx c, uint32_t *data, size
             }
         }
 #pragma unroll
-        for (int k = 0; k < 32; ++k) s[swz(base | ((uint32_t)k << ws))] = v[k];
+        for (int k = 0; k < 32; ++k) s[sb ^ swz((uint32_t)k << ws)] = v[k];
         __syncthreads();
     }
     if (live) {
+        const uint32_t st0 = swz(t);
 #pragma unroll
         for (int k = 0; k < 32; ++k) {
-            const uint32_t idx = t + (uint32_t)k * T;
-            uint32_t x = s[swz(idx)];
+            uint32_t x = s[st0 ^ swz((uint32_t)k * T)];
             if (scale != c.r1) x = redc(x, scale, c.p, c.pinv);
-            st_stream1(g + idx, x);
+            st_stream1(g + t + (uint32_t)k * T, x);
         }
     }
+}
+
+template <int LOG_N>
+static mont_status_t launch_ntt_r32(const Ctx &c, uint32_t *data, size_t batch, const uint32_t *tw, uint32_t scale,
+                                    cudaStream_t stream) {
+    constexpr uint32_t N = 1u << LOG_N, T = N >> 5;
+    constexpr uint32_t rpc = T >= 256 ? 1u : 256u / T;  // rows per CTA
+    const size_t smem = (size_t)rpc * N * 4;
+    const size_t grid = (batch + rpc - 1) / rpc;
+    if (grid > 0x7fffffffu) return MONT_EUNSUPPORTED;
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(k_ntt_r32<LOG_N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return MONT_ECUDA;
+    k_ntt_r32<LOG_N><<<(unsigned)grid, rpc * T, smem, stream>>>(c, data, batch, tw, scale);
+    return launch_status();
 }
 
 }  // namespace mont
@@ -142,24 +162,19 @@ extern "C" mont_status_t mont_ntt(const mont_ctx_t *ctx, uint32_t *data, size_t 
     if (!data || !tw || ((uintptr_t)data & 3u) || ((uintptr_t)tw & 3u) || scale >= ctx->p) return MONT_EINVAL_ARG;
     if (batch > 0x7fffffffu) return MONT_EUNSUPPORTED;
     const uint32_t N = 1u << log_n;
-    if (log_n >= 5) {
-        const uint32_t T = N >> 5;                       // threads per row
-        const uint32_t rpc = T >= 256 ? 1u : 256u / T;   // rows per CTA
-        const size_t smem = (size_t)rpc * N * 4;
-        const size_t grid = (batch + rpc - 1) / rpc;
-        if (grid > 0x7fffffffu) return MONT_EUNSUPPORTED;
-        if (rpc * T <= 512) {  // <= 512 threads: up to 128 registers, no spills
-            if (smem > 48 * 1024 && cudaFuncSetAttribute(k_ntt_r32<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                         (int)smem) != cudaSuccess)
-                return MONT_ECUDA;
-            k_ntt_r32<512><<<(unsigned)grid, rpc * T, smem, stream>>>(to_dev(ctx), data, batch, log_n, tw, scale);
-        } else {
-            if (cudaFuncSetAttribute(k_ntt_r32<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-                cudaSuccess)
-                return MONT_ECUDA;
-            k_ntt_r32<1024><<<(unsigned)grid, rpc * T, smem, stream>>>(to_dev(ctx), data, batch, log_n, tw, scale);
-        }
-        return launch_status();
+    switch (log_n) {
+        case 5: return launch_ntt_r32<5>(to_dev(ctx), data, batch, tw, scale, stream);
+        case 6: return launch_ntt_r32<6>(to_dev(ctx), data, batch, tw, scale, stream);
+        case 7: return launch_ntt_r32<7>(to_dev(ctx), data, batch, tw, scale, stream);
+        case 8: return launch_ntt_r32<8>(to_dev(ctx), data, batch, tw, scale, stream);
+        case 9: return launch_ntt_r32<9>(to_dev(ctx), data, batch, tw, scale, stream);
+        case 10: return launch_ntt_r32<10>(to_dev(ctx), data, batch, tw, scale, stream);
+        case 11: return launch_ntt_r32<11>(to_dev(ctx), data, batch, tw, scale, stream);
+        case 12: return launch_ntt_r32<12>(to_dev(ctx), data, batch, tw, scale, stream);
+        case 13: return launch_ntt_r32<13>(to_dev(ctx), data, batch, tw, scale, stream);
+        case 14: return launch_ntt_r32<14>(to_dev(ctx), data, batch, tw, scale, stream);
+        case 15: return launch_ntt_r32<15>(to_dev(ctx), data, batch, tw, scale, stream);
+        default: break;
     }
     int threads = (int)(N / 2 < 1024 ? N / 2 : 1024);
     if (threads < 32) threads = 32;

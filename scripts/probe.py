@@ -15,6 +15,7 @@ import paper_1609_00999_b200 as m  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--what", default="all")
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--logn", type=int, default=0)
 args = ap.parse_args()
 
 dev = torch.device("cuda:0")
@@ -185,7 +186,7 @@ if args.what in ("ntt",):
     P = 2013265921
     ctx = m.ctx_init(P)
     import numpy as np
-    for log_n in (10, 12, 13, 14, 15):
+    for log_n in ((args.logn,) if args.logn else (10, 12, 13, 14, 15)):
         N = 1 << log_n
         batch = (1 << 26) // N
         w = pow(31, (P - 1) // N, P)
