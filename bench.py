@@ -62,11 +62,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="step", choices=["step", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="step", choices=["step", "c2", "c3", "c4", "c5", "ntt"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--soak", type=float, default=1.0, help="seconds of untimed steps before timing (clocks)")
+    ap.add_argument("--serial", action="store_true", help="report the serial (one-stream) step instead")
     return ap.parse_args()
 
 
@@ -210,6 +211,19 @@ class Workload:
             L.append(("mont_pow_vec", lambda base=base, e=e, o=o: m.pow_vec(self.ctx[P1], base, e, out=o), 12 * N_C4,
                       ladder, "imad"))
             self.config.update({"c4_n": N_C4, "c4_ladder_mulmods": ladder})
+        if kind == "ntt":
+            # forward NTT of the configs[2] batch (4096 rows of 2^14) over P0
+            x = torch.empty(TW_BATCH * TW_LEN, **u32)
+            m.synth_fill(x, SEED, 5, rank * TW_BATCH * TW_LEN, P0, 0, False)
+            x = x.view(TW_BATCH, TW_LEN)
+            w = pow(G11_GENERATOR, (P0 - 1) // TW_LEN, P0)
+            tw = m.twiddle_table(self.ctx[P0], w, TW_LEN // 2, device=dev)
+            self.ntt_x, self.ntt_x0, self.ntt_w, self.ntt_tw = x, x.clone(), w, tw
+            self.inputs += [x]
+            self.outputs.append(x)
+            redc = TW_BATCH * (TW_LEN // 2) * 14
+            L.append(("mont_ntt", lambda x=x, tw=tw: m.ntt(self.ctx[P0], x, tw), 8 * TW_BATCH * TW_LEN, redc, "imad"))
+            self.config.update({"ntt_batch": TW_BATCH, "ntt_n": TW_LEN, "ntt_redc_per_pass": redc})
         if kind == "c5":
             n = N_C5 // world
             lo = (rank * N_C5) // world
@@ -232,8 +246,32 @@ class Workload:
         return sum(x[3] for x in self.launches)
 
     def step(self):
+        """Serial step: every launch in order on the current stream."""
         for _, fn, *_ in self.launches:
             fn()
+
+    def step_concurrent(self):
+        """The step as the runtime schedules it: the HBM-bound launches (mul_vec x3,
+        to_mont -> from_mont, twiddle) in order on one stream and the FMAHeavy-bound
+        pow ladder on a second stream, so the integer-multiply pipes and HBM work at
+        the same time.  Both lanes are joined back into the current stream; the
+        launches are independent (disjoint outputs), so results are identical."""
+        torch = self.torch
+        cur = torch.cuda.current_stream()
+        if not hasattr(self, "_lanes"):
+            self._lanes = {"hbm": torch.cuda.Stream(), "imad": torch.cuda.Stream()}
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        for st in self._lanes.values():
+            st.wait_event(ev)
+        for lane in ("imad", "hbm"):
+            st = self._lanes[lane]
+            with torch.cuda.stream(st):
+                for _, fn, _, _, bound in self.launches:
+                    if bound == lane:
+                        fn()
+        for st in self._lanes.values():
+            cur.wait_stream(st)
 
     def h2d_bytes(self):
         return sum(t.numel() * 4 for t in self.inputs)
@@ -298,13 +336,40 @@ def verify(wl: Workload) -> dict:
     if hasattr(wl, "c5"):
         a, b, c = wl.c5
         checks["c5_identity"] = identity(P0, a, b, c)
+    if hasattr(wl, "ntt_x"):
+        x0 = wl.ntt_x0[7].cpu().numpy()
+        X = wl.ntt_x[7].cpu().numpy()
+        ok = True
+        for k in (0, 1, 4097, TW_LEN - 1):
+            wk, acc, pw = pow(wl.ntt_w, k, P0), 0, 1
+            for v in x0:
+                acc = (acc + int(v) * pw) % P0
+                pw = pw * wk % P0
+            ok &= int(X[k]) == acc
+        checks["ntt_sampled_dft"] = ok
+        wl.ntt_x.copy_(wl.ntt_x0)
     return checks
 
 
 # ----------------------------------------------------------- device timing
 
+def time_steps_concurrent(wl: Workload, K: int):
+    """K concurrent-schedule steps between CUDA events on the current stream (the
+    lanes are joined into it, so the events bracket all of each step's work)."""
+    torch = wl.torch
+    s = torch.cuda.current_stream()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(s)
+    for _ in range(K):
+        wl.step_concurrent()
+    end.record(s)
+    end.synchronize()
+    return start.elapsed_time(end)
+
+
 def time_steps(wl: Workload, K: int):
-    """K steps between CUDA events on the launching stream; per-launch events too."""
+    """K serial steps between CUDA events on the launching stream; per-launch events too."""
     torch = wl.torch
     s = torch.cuda.current_stream()
     nl = len(wl.launches)
@@ -524,15 +589,24 @@ def main():
     torch.cuda.synchronize()
     t_end = time.perf_counter() + args.soak
     while time.perf_counter() < t_end:
-        wl.step()
+        wl.step_concurrent()
         torch.cuda.synchronize()
     shard.barrier()
     torch.cuda.synchronize()
-    total_ms, per_ms = time_steps(wl, args.steps)
+    # per-kernel durations: a serial pass (each launch bracketed by events)
+    serial_ms, per_ms = time_steps(wl, args.steps)
+    for _ in range(3):
+        wl.step_concurrent()
+    torch.cuda.synchronize()
+    shard.barrier()
+    torch.cuda.synchronize()
+    # the reported number: K steps with the runtime's two-lane schedule
+    total_ms = time_steps_concurrent(wl, args.steps) if not args.serial else serial_ms
     torch.cuda.synchronize()
     shard.barrier()
     clocks = sampler.stop()
     total_ms = shard.max_over_ranks(total_ms)
+    serial_ms = shard.max_over_ranks(serial_ms)
     ms_per_step = total_ms / args.steps
     # checksum partials -> one NCCL all-reduce SUM (A11), outside the timed region
     if wl.kind in ("step", "c2", "c5"):
@@ -595,11 +669,15 @@ def main():
         "config": {"workload": {"step": "one pass of SURVEY §8(a) A1-A11: configs[1] mul_vec x3 primes + to/from_mont + "
                                          "configs[2] twiddle + configs[3] pow (checksum fused into mul_vec)",
                                 "c2": "configs[1] mul_vec x3 primes + checksums", "c3": "configs[2] twiddle",
-                                "c4": "configs[3] pow", "c5": "configs[4] sharded mul_vec n=2^31 + checksum"}[wl.kind],
+                                "c4": "configs[3] pow", "c5": "configs[4] sharded mul_vec n=2^31 + checksum",
+                                "ntt": "SURVEY 8(f) NEXT #1: in-place forward NTT of the configs[2] batch, 4096 x 2^14"}[wl.kind],
                    "parallelism": f"dp{world} (contiguous global-index slices, no data-path collective)",
                    "l2": "inputs larger than L2 (step working set ~3.3 GiB vs 126 MB L2)",
                    "mulmods_per_step_per_rank": wl.mulmods, **wl.config},
         "gpu_launches": len(wl.launches) * args.steps,
+        "schedule": ("serial, one stream" if args.serial else
+                     "two lanes: HBM-bound launches on one stream, the IMAD-bound pow on another"),
+        "ms_per_step_serial": round(serial_ms / args.steps, 5),
         "roofline": roof,
         "kernels": rooflines,
         "clocks": {k: clocks.get(k) for k in ("sm_mhz", "sm_max_mhz", "reasons", "samples", "samples_under_load")},

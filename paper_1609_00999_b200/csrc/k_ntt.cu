@@ -75,7 +75,7 @@ __device__ __forceinline__ uint32_t swz(uint32_t a) { return a ^ (((a >> 5) ^ (a
 // swz(base | k << ws) = swz(base) ^ swz(k << ws): one LOP3 per shared-memory
 // access, and twiddle addresses become (per-thread base) + (constant offset).
 template <int LOG_N>
-__global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, 1)
+__global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
     k_ntt_r32(Ctx c, uint32_t *data, size_t batch, const uint32_t *__restrict__ tw, uint32_t scale) {
     constexpr uint32_t N = 1u << LOG_N, T = N >> 5;
     extern __shared__ uint32_t sm[];
