@@ -54,6 +54,8 @@ N_C5 = 1 << 31
 SEED = 42
 METRIC = json.loads((ROOT / "BASELINE.json").read_text())["metric"]
 G11_GENERATOR = 31
+POW_CTAS = 0   # set from --pow-ctas
+LANE_ORDER = tuple(os.environ.get("MONT_LANE_ORDER", "imad,hbm").split(","))
 
 
 def parse():
@@ -68,6 +70,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--soak", type=float, default=1.0, help="seconds of untimed steps before timing (clocks)")
     ap.add_argument("--serial", action="store_true", help="report the serial (one-stream) step instead")
+    ap.add_argument("--pow-ctas", type=int, default=5, help="CTAs per SM of the persistent pow grid (0 = flat)")
     return ap.parse_args()
 
 
@@ -208,8 +211,11 @@ class Workload:
             self.pow_bufs = (base, e, o)
             self.inputs += [base, e]
             self.outputs.append(o)
-            L.append(("mont_pow_vec", lambda base=base, e=e, o=o: m.pow_vec(self.ctx[P1], base, e, out=o), 12 * N_C4,
-                      ladder, "imad"))
+            # in the two-lane schedule pow runs as a persistent grid of POW_CTAS CTAs per SM so it
+            # co-resides with the HBM-bound kernels instead of filling every SM first
+            pcfg = m.Launch(ctas_per_sm=POW_CTAS) if POW_CTAS > 0 else None
+            L.append(("mont_pow_vec", lambda base=base, e=e, o=o, pcfg=pcfg:
+                      m.pow_vec(self.ctx[P1], base, e, out=o, cfg=pcfg), 12 * N_C4, ladder, "imad"))
             self.config.update({"c4_n": N_C4, "c4_ladder_mulmods": ladder})
         if kind == "ntt":
             # forward NTT of the configs[2] batch (4096 rows of 2^14) over P0
@@ -264,7 +270,7 @@ class Workload:
         ev.record(cur)
         for st in self._lanes.values():
             st.wait_event(ev)
-        for lane in ("imad", "hbm"):
+        for lane in LANE_ORDER:
             st = self._lanes[lane]
             with torch.cuda.stream(st):
                 for _, fn, _, _, bound in self.launches:
@@ -561,6 +567,8 @@ def ncu_traffic(name: str):
 
 def main():
     args = parse()
+    global POW_CTAS
+    POW_CTAS = 0 if args.serial else args.pow_ctas
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
