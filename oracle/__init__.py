@@ -47,7 +47,9 @@ _U32P = np.ctypeslib.ndpointer(dtype=np.uint32, flags="C_CONTIGUOUS")
 def lib():
     global _lib
     if _lib is None:
-        L = C.CDLL(str(build()))
+        # test hook: tests/test_oracle_mutants.py points this at deliberately broken builds
+        override = os.environ.get("ORACLE_LIB_OVERRIDE")
+        L = C.CDLL(override if override else str(build()))
         L.oracle_ctx_l.argtypes = [C.POINTER(Ctx), C.c_uint32, C.c_uint32]
         L.oracle_ctx_l.restype = C.c_int
         L.oracle_mulmod.argtypes = [C.c_uint32] * 3
