@@ -330,3 +330,65 @@ def test_to_from_mont_configs(m, unroll, threads, variant):
     tm = m.to_mont(ctx, dev(x), cfg=cfg)
     assert np.array_equal(host(tm), oracle.to_mont(P, x))
     assert np.array_equal(host(m.from_mont(ctx, tm, cfg=cfg)), x)
+
+
+# ------------------------------------------- out-of-bounds guards (no sanitizer on this pool)
+
+GUARD = 64
+
+
+def guarded(n, off):
+    """A device buffer of n words at offset `off` inside GUARD canary words on each side."""
+    buf = dev(np.full(n + 2 * GUARD, 0xA5A5A5A5, dtype=np.uint32))
+    return buf, buf[GUARD + off:GUARD + off + n]
+
+
+def canaries_intact(buf, n, off):
+    h = host(buf)
+    return bool(np.all(h[:GUARD + off] == 0xA5A5A5A5) and np.all(h[GUARD + off + n:] == 0xA5A5A5A5))
+
+
+@pytest.mark.parametrize("n", [1, 3, 4, 5, 7, 33, 4099, 65537])
+@pytest.mark.parametrize("off", [0, 1, 2, 3])
+def test_guards_all_kernels(m, n, off):
+    P = 469762049
+    ctx = m.ctx_init(P)
+    a, b = synth.c2_inputs(P, 0, n)
+    for name, run, ref in [
+        ("mul_vec", lambda o: m.mul_vec(ctx, dev(a), dev(b), out=o), oracle.mont_mul(P, a, b)),
+        ("mul_vec_checksum", lambda o: m.mul_vec_checksum(ctx, dev(a), dev(b), out=o), oracle.mont_mul(P, a, b)),
+        ("to_mont", lambda o: m.to_mont(ctx, dev(a), out=o), oracle.to_mont(P, a)),
+        ("from_mont", lambda o: m.from_mont(ctx, dev(a), out=o), oracle.from_mont(P, a)),
+        ("pow_vec", lambda o: m.pow_vec(ctx, dev(a), dev(b), out=o), oracle.power(P, a, b)),
+    ]:
+        buf, o = guarded(n, off)
+        run(o)
+        assert np.array_equal(host(o), ref), name
+        assert canaries_intact(buf, n, off), name
+
+
+@pytest.mark.parametrize("batch,L,off", [(3, 1000, 1), (5, 16, 0), (2, 4100, 3), (9, 7, 2)])
+def test_guards_twiddle(m, batch, L, off):
+    P = 2013265921
+    x = synth.c3_x(P, batch=batch, length=L)
+    tw = synth.uniform(42, 11, P, 0, L)
+    buf, o = guarded(batch * L, off)
+    m.mul_twiddle(m.ctx_init(P), dev(x), dev(tw), out=o.view(batch, L))
+    assert np.array_equal(host(o).reshape(batch, L), oracle.twiddle(P, x, tw))
+    assert canaries_intact(buf, batch * L, off)
+
+
+@pytest.mark.parametrize("log_n", [1, 4, 5, 9, 12])
+@pytest.mark.parametrize("batch", [1, 3, 7])
+def test_guards_ntt(m, log_n, batch):
+    P = 998244353
+    N = 1 << log_n
+    ctx = m.ctx_init(P)
+    w = oracle.root_of_unity(P, 3, N)
+    tw = m.twiddle_table(ctx, w, max(1, N // 2))
+    x = synth.uniform(42, 26, P, 0, batch * N).reshape(batch, N)
+    buf, o = guarded(batch * N, 0)
+    o.copy_(dev(x.reshape(-1)))
+    m.ntt(ctx, o.view(batch, N), tw)
+    assert np.array_equal(host(o).reshape(batch, N), oracle.dft(P, w, x))
+    assert canaries_intact(buf, batch * N, 0)
