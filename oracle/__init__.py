@@ -64,6 +64,7 @@ def lib():
         L.oracle_pow1.restype = C.c_uint32
         L.oracle_mont_mul.argtypes = [C.POINTER(Ctx), _U32P, _U32P, _U32P, C.c_size_t, C.c_int]
         L.oracle_to_mont.argtypes = [C.POINTER(Ctx), _U32P, _U32P, C.c_size_t, C.c_int]
+        L.oracle_mulmod_vec.argtypes = [C.POINTER(Ctx), _U32P, _U32P, _U32P, C.c_size_t, C.c_int]
         L.oracle_from_mont.argtypes = [C.POINTER(Ctx), _U32P, _U32P, C.c_size_t, C.c_int]
         L.oracle_twiddle.argtypes = [C.POINTER(Ctx), _U32P, _U32P, _U32P, C.c_size_t, C.c_size_t, C.c_int]
         L.oracle_pow.argtypes = [C.POINTER(Ctx), _U32P, _U32P, _U32P, C.c_size_t, C.c_int]
@@ -116,6 +117,15 @@ def mont_mul(P: int, a, b, nthreads: int = 0) -> np.ndarray:
     out = np.empty_like(a)
     c = ctx(P)
     lib().oracle_mont_mul(C.byref(c), out.reshape(-1), a.reshape(-1), b.reshape(-1), a.size, nthreads)
+    return out
+
+
+def mulmod_vec(P: int, a, b, nthreads: int = 0) -> np.ndarray:
+    """c[i] = a[i] b[i] mod P (plain), by definition."""
+    a, b = _u32(a), _u32(b)
+    out = np.empty_like(a)
+    c = ctx(P)
+    lib().oracle_mulmod_vec(C.byref(c), out.reshape(-1), a.reshape(-1), b.reshape(-1), a.size, nthreads)
     return out
 
 

@@ -151,7 +151,7 @@ typedef struct {
     uint64_t sum;
 } job_t;
 
-enum { OP_MUL = 0, OP_TO = 1, OP_FROM = 2, OP_TW = 3, OP_POW = 4, OP_SUM = 5 };
+enum { OP_MUL = 0, OP_TO = 1, OP_FROM = 2, OP_TW = 3, OP_POW = 4, OP_SUM = 5, OP_MULMOD = 6 };
 
 static void *run_job(void *arg)
 {
@@ -173,6 +173,9 @@ static void *run_job(void *arg)
         break;
     case OP_POW:
         for (i = j->lo; i < j->hi; ++i) j->out[i] = oracle_pow1(c->P, j->a[i], j->b[i]);
+        break;
+    case OP_MULMOD:   /* plain a*b mod P by definition (the result Barrett, Alg. 1, reaches) */
+        for (i = j->lo; i < j->hi; ++i) j->out[i] = mulmod_naive(j->a[i] % c->P, j->b[i] % c->P, c->P);
         break;
     case OP_SUM: {
         uint64_t s = 0;
@@ -218,6 +221,10 @@ static uint64_t run_parallel(int op, const oracle_ctx_t *c, uint32_t *out, const
 void oracle_mont_mul(const oracle_ctx_t *c, uint32_t *out, const uint32_t *a, const uint32_t *b,
                      size_t n, int nthreads)
 { run_parallel(OP_MUL, c, out, a, b, n, 1, nthreads); }
+
+void oracle_mulmod_vec(const oracle_ctx_t *c, uint32_t *out, const uint32_t *a, const uint32_t *b, size_t n,
+                       int nthreads)
+{ run_parallel(OP_MULMOD, c, out, a, b, n, 1, nthreads); }
 
 void oracle_to_mont(const oracle_ctx_t *c, uint32_t *out, const uint32_t *x, size_t n, int nthreads)
 { run_parallel(OP_TO, c, out, x, NULL, n, 1, nthreads); }

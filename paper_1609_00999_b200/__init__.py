@@ -87,6 +87,19 @@ SIGNATURES = {
 
 SIGNATURES["mont_ntt"] = (C.c_int, [_CTX, _P, _S, C.c_int, _P, C.c_uint32, _P])
 
+
+class BarrettCtx(C.Structure):
+    """barrett_ctx_t (include/barrett.h): k = ceil(log2 P), P' = floor(2^2k / P)."""
+    _fields_ = [("p", C.c_uint32), ("k", C.c_uint32), ("pprime", C.c_uint32), ("pad", C.c_uint32)]
+
+
+_BCTX = C.POINTER(BarrettCtx)
+SIGNATURES.update({
+    "barrett_ctx_init": (C.c_int, [_BCTX, C.c_uint32]),
+    "barrett_mul_vec": (C.c_int, [_BCTX, _P, _P, _P, _S, _P]),
+    "barrett_pow_vec": (C.c_int, [_BCTX, _P, _P, _P, _S, _P]),
+})
+
 HOST_OPS = {"mul_vec": 0, "to_mont": 1, "from_mont": 2, "pow_vec": 3, "twiddle": 4}
 
 
@@ -361,6 +374,29 @@ def ntt(ctx: Ctx, data, tw, scale: int | None = None, stream=None):
     _check(lib().mont_ntt(C.byref(ctx), _ptr(data), batch, log_n, _ptr(tw), ctx.r1 if scale is None else scale,
                           _stream_handle(stream)), "mont_ntt")
     return data
+
+
+def barrett_ctx_init(p: int) -> BarrettCtx:
+    c = BarrettCtx()
+    _check(lib().barrett_ctx_init(C.byref(c), p), "barrett_ctx_init")
+    return c
+
+
+def barrett_mul_vec(ctx: BarrettCtx, a, b, out=None, stream=None):
+    """c = a b mod P, plain domain, Barrett's Alg. 1 (comparison kernel, include/barrett.h)."""
+    _dev_u32(a, "a"), _dev_u32(b, "b")
+    out = _out_like(out, a)
+    _check(lib().barrett_mul_vec(C.byref(ctx), _ptr(out), _ptr(a), _ptr(b), a.numel(), _stream_handle(stream)),
+           "barrett_mul_vec")
+    return out
+
+
+def barrett_pow_vec(ctx: BarrettCtx, base, exp, out=None, stream=None):
+    _dev_u32(base, "base"), _dev_u32(exp, "exp")
+    out = _out_like(out, base)
+    _check(lib().barrett_pow_vec(C.byref(ctx), _ptr(out), _ptr(base), _ptr(exp), base.numel(),
+                                 _stream_handle(stream)), "barrett_pow_vec")
+    return out
 
 
 def sm_count() -> int:

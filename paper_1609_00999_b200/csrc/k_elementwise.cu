@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "../../include/barrett.h"
 #include "abi_util.h"
 
 namespace mont {
@@ -31,6 +32,10 @@ struct OpTo {
 struct OpFrom {
     uint32_t p, pinv;
     __device__ __forceinline__ uint32_t operator()(uint32_t x) const { return redc1(x, p, pinv); }
+};
+struct OpBarrett {
+    BarrettDev c;
+    __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return barrett(a, b, c); }
 };
 struct OpXor {  // triad microbenchmark: no modular math
     __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a ^ b; }
@@ -401,3 +406,28 @@ extern "C" mont_status_t mb_copy(uint32_t *out, const uint32_t *in, size_t n, co
 }
 
 extern "C" int mont_sm_count(void) { return sm_count(); }
+
+extern "C" mont_status_t barrett_ctx_init(barrett_ctx_t *ctx, uint32_t p) {
+    if (!ctx) return MONT_EINVAL_ARG;
+    if ((p & 1u) == 0u || p < 3u || p >= 0x80000000u) return MONT_EINVAL_P;
+    uint32_t k = 0;
+    while ((1ull << k) < p) ++k;  // ceil(log2 P)
+    ctx->p = p;
+    ctx->k = k;
+    ctx->pprime = (uint32_t)((1ull << (2 * k)) / p);
+    ctx->pad = 0;
+    return MONT_OK;
+}
+
+static bool barrett_ok(const barrett_ctx_t *c) {
+    return c && (c->p & 1u) && c->p >= 3u && c->p < 0x80000000u && c->k <= 31 && (1ull << c->k) >= c->p &&
+           c->pprime == (uint32_t)((1ull << (2 * c->k)) / c->p);
+}
+
+extern "C" mont_status_t barrett_mul_vec(const barrett_ctx_t *ctx, uint32_t *c, const uint32_t *a, const uint32_t *b,
+                                         size_t n, cudaStream_t stream) {
+    if (!barrett_ok(ctx)) return ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
+    if (n == 0) return MONT_OK;
+    if (!a || !b || !c || ((uintptr_t)a | (uintptr_t)b | (uintptr_t)c) & 3u) return MONT_EINVAL_ARG;
+    return launch_map2<false>(OpBarrett{BarrettDev{ctx->p, ctx->k, ctx->pprime}}, c, a, b, n, kMulVecDefault, stream);
+}

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "../../include/barrett.h"
 #include "abi_util.h"
 
 namespace mont {
@@ -234,6 +235,55 @@ __global__ void __launch_bounds__(256) k_pow_scalar(PowParams q, uint32_t *out, 
     }
 }
 
+// ---- Barrett ladder (include/barrett.h): the same 2-bit window on plain values
+template <int L>
+__device__ __forceinline__ void pow_barrett(const BarrettDev &c, const uint32_t (&base)[L], const uint32_t (&e)[L],
+                                            uint32_t (&out)[L]) {
+    uint32_t t1[L], t2[L], t3[L], acc[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+        t1[l] = base[l] % c.p;
+        t2[l] = barrett(t1[l], t1[l], c);
+        t3[l] = barrett(t2[l], t1[l], c);
+        const uint32_t d = e[l] >> 30;
+        acc[l] = d == 0 ? 1u : d == 1 ? t1[l] : d == 2 ? t2[l] : t3[l];
+    }
+#pragma unroll
+    for (int sh = 28; sh >= 0; sh -= 2) {
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+            uint32_t a = barrett(acc[l], acc[l], c);
+            a = barrett(a, a, c);
+            const uint32_t d = (e[l] >> sh) & 3u;
+            const uint32_t lo = (d & 1u) ? t1[l] : 1u;
+            const uint32_t hi = (d & 1u) ? t3[l] : t2[l];
+            acc[l] = barrett(a, (d & 2u) ? hi : lo, c);
+        }
+    }
+#pragma unroll
+    for (int l = 0; l < L; ++l) out[l] = acc[l];  // barrett() outputs are canonical, and 1 < P
+}
+
+__global__ void __launch_bounds__(256) k_pow_barrett(BarrettDev c, uint32_t *out, const uint32_t *base,
+                                                      const uint32_t *exp, size_t n) {
+    const size_t n4 = n / 4;
+    const uint4 *b4 = reinterpret_cast<const uint4 *>(base);
+    const uint4 *e4 = reinterpret_cast<const uint4 *>(exp);
+    uint4 *o4 = reinterpret_cast<uint4 *>(out);
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n4) {
+        const uint4 bv = ld_stream(b4 + i), ev = ld_stream(e4 + i);
+        uint32_t b[4] = {bv.x, bv.y, bv.z, bv.w}, e[4] = {ev.x, ev.y, ev.z, ev.w}, o[4];
+        pow_barrett<4>(c, b, e, o);
+        st_stream(o4 + i, make_uint4(o[0], o[1], o[2], o[3]));
+    } else if (i < n4 + (n & 3)) {
+        const size_t j = 4 * n4 + (i - n4);
+        uint32_t b[1] = {base[j]}, e[1] = {exp[j]}, o[1];
+        pow_barrett<1>(c, b, e, o);
+        out[j] = o[0];
+    }
+}
+
 // tw[j] = to_mont(w^j): binary ladder on the bits of j, canonical output
 __global__ void __launch_bounds__(256) k_twiddle_table(Ctx c, uint32_t *tw, uint32_t w, size_t len) {
     for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += (size_t)gridDim.x * blockDim.x) {
@@ -320,5 +370,20 @@ extern "C" mont_status_t mont_twiddle_table(const mont_ctx_t *ctx, uint32_t *tw,
     size_t grid = (len + 255) / 256;
     if (grid > (size_t)sms * 8) grid = (size_t)sms * 8;
     k_twiddle_table<<<(unsigned)grid, 256, 0, stream>>>(to_dev(ctx), tw, w, len);
+    return launch_status();
+}
+
+extern "C" mont_status_t barrett_pow_vec(const barrett_ctx_t *ctx, uint32_t *out, const uint32_t *base,
+                                         const uint32_t *exp, size_t n, cudaStream_t stream) {
+    if (!ctx || (ctx->p & 1u) == 0u || ctx->p < 3u || ctx->p >= 0x80000000u || ctx->k > 31 ||
+        ctx->pprime != (uint32_t)((1ull << (2 * ctx->k)) / ctx->p))
+        return ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
+    if (n == 0) return MONT_OK;
+    if (!out || !base || !exp || ((uintptr_t)out | (uintptr_t)base | (uintptr_t)exp) & 15u)
+        return MONT_EINVAL_ARG;  // 16-byte aligned operands only (comparison kernel)
+    const size_t threads = n / 4 + (n & 3);
+    const size_t grid = (threads + 255) / 256;
+    if (grid > 0x7fffffff) return MONT_EUNSUPPORTED;
+    k_pow_barrett<<<(unsigned)grid, 256, 0, stream>>>(BarrettDev{ctx->p, ctx->k, ctx->pprime}, out, base, exp, n);
     return launch_status();
 }

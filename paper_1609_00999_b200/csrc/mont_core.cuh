@@ -160,3 +160,26 @@ __device__ __forceinline__ double fmulmod(double a, double b, double P, double P
 }
 
 }  // namespace mont
+
+namespace mont {
+
+// ---- Barrett (Alg. 1, :71-85) for the comparison kernels of
+// include/barrett.h.  ab < P^2 < 2^(2k); m < 2^k; m P' < 2^63; t = ab - qP < 4P
+// (PAPER.md:85), which can exceed 2^32 for P > 2^30, so t is 64-bit until the
+// first correction.
+struct BarrettDev {
+    uint32_t p, k, pp;
+};
+
+__device__ __forceinline__ uint32_t barrett(uint32_t a, uint32_t b, const BarrettDev &c) {
+    const uint64_t T = mul_wide_u32(a, b);
+    const uint32_t m = (uint32_t)(T >> c.k);                           // floor(ab / 2^k)
+    const uint32_t q = (uint32_t)(mul_wide_u32(m, c.pp) >> c.k);       // floor(m P' / 2^k)
+    uint64_t t = T - mul_wide_u32(q, c.p);                             // < 4P
+    const uint64_t t2 = t - 2ull * c.p;
+    t = (int64_t)t2 >= 0 ? t2 : t;                                     // < 2P
+    const uint32_t r = (uint32_t)t;
+    return umin(r, r - c.p);                                           // < P
+}
+
+}  // namespace mont

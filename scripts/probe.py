@@ -198,3 +198,31 @@ if args.what in ("ntt",):
         redc = batch * (N // 2) * log_n
         out(what="ntt", log_n=log_n, batch=batch, us=med * 1e6, gbs=8 * batch * N / med / 1e9,
             tredc=redc / med / 1e12, frac_imad_floor=redc / med / (148 * 64 / 5 * 1.965e9))
+
+if args.what in ("barrett",):
+    import numpy as np
+    P = 469762049
+    n = 1 << 24
+    base = torch.empty(n, dtype=torch.uint32, device=dev)
+    e = torch.empty(n, dtype=torch.uint32, device=dev)
+    o = torch.empty(n, dtype=torch.uint32, device=dev)
+    m.synth_fill(base, 42, 3, 0, P, mode=1)
+    m.synth_fill(e, 42, 4, 0, P, mode=2)
+    useful = int(31 * n + np.unpackbits(e.cpu().numpy().view(np.uint8)).sum())
+    bctx = m.barrett_ctx_init(P)
+    ctx = m.ctx_init(P)
+    med, _ = timeit(lambda: m.barrett_pow_vec(bctx, base, e, out=o), reps=10)
+    out(what="pow_barrett", us=med * 1e6, tmulmod=useful / med / 1e12)
+    med, _ = timeit(lambda: m.pow_vec(ctx, base, e, out=o), reps=10)
+    out(what="pow_montgomery", us=med * 1e6, tmulmod=useful / med / 1e12)
+    nn = 1 << 26
+    a = torch.empty(nn, dtype=torch.uint32, device=dev)
+    b = torch.empty(nn, dtype=torch.uint32, device=dev)
+    c = torch.empty(nn, dtype=torch.uint32, device=dev)
+    m.synth_fill(a, 42, 1, 0, P)
+    m.synth_fill(b, 42, 2, 0, P)
+    med, _ = timeit(lambda: m.barrett_mul_vec(bctx, a, b, out=c))
+    out(what="mul_vec_barrett", us=med * 1e6, gbs=12 * nn / med / 1e9)
+    med, _ = timeit(lambda: m.mul_vec(ctx, a, b, out=c))
+    out(what="mul_vec_montgomery", us=med * 1e6, gbs=12 * nn / med / 1e9)
+    sink = torch.empty(sms * 8 * 256, dtype=torch.uint32, device=dev)

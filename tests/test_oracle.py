@@ -348,3 +348,20 @@ def test_cyclic_conv_small_integers():
     folded = full[:N].copy()
     folded[:N - 1] += full[N:]
     assert np.array_equal(oracle.cyclic_conv(P, a, b), folded.astype(np.uint32))
+
+
+def test_mulmod_vec_pins():
+    """Plain products: brute force all pairs for small P against Python ints; the Barrett step-by-step
+    oracle and the definition agree (Alg. 1 reaches a*b mod P)."""
+    for P in (3, 17, 97, 257):
+        g = np.arange(P, dtype=np.uint32)
+        a, b = np.repeat(g, P), np.tile(g, P)
+        c = oracle.mulmod_vec(P, a, b)
+        assert all(int(x) == (int(y) * int(z)) % P for x, y, z in zip(c[::7], a[::7], b[::7]))
+    P = 2013265921
+    rng = np.random.default_rng(30)
+    a = rng.integers(0, P, 3000, dtype=np.uint64).astype(np.uint32)
+    b = rng.integers(0, P, 3000, dtype=np.uint64).astype(np.uint32)
+    c = oracle.mulmod_vec(P, a, b)
+    for i in range(0, 3000, 17):
+        assert int(c[i]) == oracle.barrett(P, int(a[i]), int(b[i]))[0] == (int(a[i]) * int(b[i])) % P
