@@ -223,7 +223,7 @@ class Workload:
             m.synth_fill(x, SEED, 5, rank * TW_BATCH * TW_LEN, P0, 0, False)
             x = x.view(TW_BATCH, TW_LEN)
             w = pow(G11_GENERATOR, (P0 - 1) // TW_LEN, P0)
-            tw = m.twiddle_table(self.ctx[P0], w, TW_LEN // 2, device=dev)
+            tw = m.ntt_twiddles(self.ctx[P0], w, 14, device=dev)
             self.ntt_x, self.ntt_x0, self.ntt_w, self.ntt_tw = x, x.clone(), w, tw
             self.inputs += [x]
             self.outputs.append(x)

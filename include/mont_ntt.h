@@ -17,9 +17,12 @@ extern "C" {
 /* In-place batched NTT of `batch` rows of N = 2^log_n canonical residues
  * (row r at data + r*N, natural order in and out):
  *     X[k] = s * sum_{j<N} x[j] w^(j k)  mod P
- * tw    : N/2 twiddles in Montgomery form, tw[j] = to_mont(w^j) (e.g. from
- *         mont_twiddle_table(ctx, tw, w, N/2)), w a primitive N-th root of
- *         unity mod P.  Passing the table of w^-1 gives the inverse transform.
+ * tw    : the stage-major twiddle table of N - 1 Montgomery-form entries built
+ *         by mont_ntt_twiddles(ctx, tw, w, log_n): for stage s = 1..log_n
+ *         (pair distance h = 2^(s-1)) the h twiddles w^(pos N / 2h), pos < h,
+ *         are contiguous at tw[h - 1 + pos], so the threads of a warp read
+ *         consecutive words.  w a primitive N-th root of unity mod P; the
+ *         table of w^-1 gives the inverse transform.
  * scale : the output factor s in Montgomery form (to_mont(s)); ctx->r1 means
  *         s = 1 (no extra multiply); to_mont(N^-1) with the w^-1 table makes
  *         the normalised inverse.
@@ -32,6 +35,11 @@ extern "C" {
  * device pointers; rows may not overlap. */
 mont_status_t mont_ntt(const mont_ctx_t *ctx, uint32_t *data, size_t batch, int log_n, const uint32_t *tw,
                        uint32_t scale, cudaStream_t stream);
+
+/* tw[2^(s-1) - 1 + pos] = to_mont(w^(pos * 2^(log_n - s))) for s = 1..log_n,
+ * pos < 2^(s-1): N - 1 entries (device pointer), each an independent
+ * square-and-multiply on the GPU.  1 <= log_n <= 30. */
+mont_status_t mont_ntt_twiddles(const mont_ctx_t *ctx, uint32_t *tw, uint32_t w, int log_n, cudaStream_t stream);
 
 #ifdef __cplusplus
 }

@@ -86,6 +86,7 @@ SIGNATURES = {
 }
 
 SIGNATURES["mont_ntt"] = (C.c_int, [_CTX, _P, _S, C.c_int, _P, C.c_uint32, _P])
+SIGNATURES["mont_ntt_twiddles"] = (C.c_int, [_CTX, _P, C.c_uint32, C.c_int, _P])
 
 
 class BarrettCtx(C.Structure):
@@ -361,16 +362,24 @@ def mul_twiddle_host(ctx: Ctx, x, tw, out, ws, stream=None):
                                        ws.numel(), _stream_handle(stream)), "mont_mul_twiddle_host")
 
 
+def ntt_twiddles(ctx: Ctx, w: int, log_n: int, device="cuda", stream=None):
+    """Stage-major NTT twiddle table (N - 1 Montgomery-form words) for mont_ntt."""
+    torch = _torch()
+    tw = torch.empty((1 << log_n) - 1, dtype=torch.uint32, device=device)
+    _check(lib().mont_ntt_twiddles(C.byref(ctx), _ptr(tw), w, log_n, _stream_handle(stream)), "mont_ntt_twiddles")
+    return tw
+
+
 def ntt(ctx: Ctx, data, tw, scale: int | None = None, stream=None):
     """In-place batched NTT of the rows of `data` (batch, N), N = 2^k <= 32768 (include/mont_ntt.h).
-    tw: device table of N/2 Montgomery twiddles; scale: Montgomery form of the output factor."""
+    tw: stage-major table from ntt_twiddles(); scale: Montgomery form of the output factor."""
     _dev_u32(data, "data"), _dev_u32(tw, "tw")
     if data.dim() != 2:
         raise ValueError("data must be (batch, N)")
     batch, n = data.shape
     log_n = n.bit_length() - 1
-    if n != 1 << log_n or tw.numel() < n // 2:
-        raise ValueError("N must be a power of two and tw must hold N/2 entries")
+    if n != 1 << log_n or tw.numel() < n - 1:
+        raise ValueError("N must be a power of two and tw must hold the N-1 stage-major twiddles")
     _check(lib().mont_ntt(C.byref(ctx), _ptr(data), batch, log_n, _ptr(tw), ctx.r1 if scale is None else scale,
                           _stream_handle(stream)), "mont_ntt")
     return data

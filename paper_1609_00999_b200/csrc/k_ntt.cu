@@ -36,12 +36,11 @@ __global__ void __launch_bounds__(1024) k_ntt_smem(Ctx c, uint32_t *data, int lo
     __syncthreads();
     for (int st = 1; st <= log_n; ++st) {
         const uint32_t hmask = (1u << (st - 1)) - 1u;
-        const int tshift = log_n - st;
         for (uint32_t t = threadIdx.x; t < half_n; t += blockDim.x) {
             const uint32_t pos = t & hmask;
             const uint32_t i = ((t >> (st - 1)) << st) | pos;
             const uint32_t j = i + hmask + 1u;
-            const uint32_t v = redc(s[j], __ldg(tw + (pos << tshift)), c.p, c.pinv);
+            const uint32_t v = redc(s[j], __ldg(tw + hmask + pos), c.p, c.pinv);
             const uint32_t u = s[i];
             s[i] = mod_add(u, v, c.p);
             s[j] = mod_sub(u, v, c.p);
@@ -106,14 +105,14 @@ __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
         for (int lb = 0; lb < 5; ++lb) {
             const int st = ws + lb + 1;  // stage: pair distance 2^(st-1)
             if (st <= s0) continue;      // done by the previous trip (last, overlapping window)
-            const int tsh = LOG_N - st;
-            // twiddle index (i mod 2^(st-1)) << (LOG_N - st) = (tl << tsh) + (j << (ws + tsh))
-            const uint32_t *twb = tw + (tl << tsh);
+            // stage-major table: this stage's twiddle for pos = tl | j << ws is at
+            // tw[2^(st-1) - 1 + pos]; consecutive lanes (consecutive tl) read consecutive words
+            const uint32_t *twb = tw + ((1u << (st - 1)) - 1u) + tl;
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
                 const int k0 = ((q >> lb) << (lb + 1)) | (q & ((1 << lb) - 1));
                 const int k1 = k0 | (1 << lb);
-                const uint32_t w = __ldg(twb + ((uint32_t)(k0 & ((1 << lb) - 1)) << (ws + tsh)));
+                const uint32_t w = __ldg(twb + ((uint32_t)(k0 & ((1 << lb) - 1)) << ws));
                 const uint32_t x1 = redc(v[k1], w, c.p, c.pinv);
                 const uint32_t u = v[k0];
                 v[k0] = mod_add(u, x1, c.p);
@@ -150,9 +149,40 @@ static mont_status_t launch_ntt_r32(const Ctx &c, uint32_t *data, size_t batch, 
     return launch_status();
 }
 
+__global__ void __launch_bounds__(256) k_ntt_twiddles(Ctx c, uint32_t *tw, uint32_t w, int log_n) {
+    const size_t total = ((size_t)1 << log_n) - 1;
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        // e = 2^(s-1) - 1 + pos  ->  s - 1 = floor(log2(e + 1)), pos = e + 1 - 2^(s-1)
+        const int sm1 = 63 - __clzll((unsigned long long)(e + 1));
+        const size_t pos = e + 1 - ((size_t)1 << sm1);
+        const unsigned long long ex = (unsigned long long)pos << (log_n - 1 - sm1);  // pos * N / 2^s
+        const uint32_t x = redc(w, c.r2, c.p, c.pinv);
+        uint32_t acc = c.r1;
+        for (int sh = 63 - __clzll(ex | 1ull); sh >= 0; --sh) {
+            acc = redc(acc, acc, c.p, c.pinv);
+            if ((ex >> sh) & 1ull) acc = redc(acc, x, c.p, c.pinv);
+        }
+        tw[e] = acc;
+    }
+}
+
 }  // namespace mont
 
 using namespace mont;
+
+extern "C" mont_status_t mont_ntt_twiddles(const mont_ctx_t *ctx, uint32_t *tw, uint32_t w, int log_n,
+                                           cudaStream_t stream) {
+    if (!ctx_ok(ctx)) return ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
+    if (log_n < 1 || log_n > 30) return MONT_EUNSUPPORTED;
+    if (!tw || ((uintptr_t)tw & 3u)) return MONT_EINVAL_ARG;
+    const int sms = sm_count();
+    if (sms <= 0) return MONT_ECUDA;
+    size_t grid = ((((size_t)1 << log_n) - 1) + 255) / 256;
+    if (grid > (size_t)sms * 8) grid = (size_t)sms * 8;
+    if (grid == 0) grid = 1;
+    k_ntt_twiddles<<<(unsigned)grid, 256, 0, stream>>>(to_dev(ctx), tw, w, log_n);
+    return launch_status();
+}
 
 extern "C" mont_status_t mont_ntt(const mont_ctx_t *ctx, uint32_t *data, size_t batch, int log_n, const uint32_t *tw,
                                   uint32_t scale, cudaStream_t stream) {

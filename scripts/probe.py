@@ -190,7 +190,7 @@ if args.what in ("ntt",):
         N = 1 << log_n
         batch = (1 << 26) // N
         w = pow(31, (P - 1) // N, P)
-        tw = m.twiddle_table(ctx, w, N // 2)
+        tw = m.ntt_twiddles(ctx, w, log_n)
         d = torch.empty(batch * N, dtype=torch.uint32, device=dev)
         m.synth_fill(d, 42, 5, 0, P)
         d = d.view(batch, N)

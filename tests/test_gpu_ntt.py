@@ -20,9 +20,9 @@ def tables(m, P, N):
     ctx = m.ctx_init(P)
     w = oracle.root_of_unity(P, GEN[P], N)
     winv = oracle.inverse(w, P)
-    half = max(1, N // 2)
-    tw = m.twiddle_table(ctx, w, half)
-    twi = m.twiddle_table(ctx, winv, half)
+    log_n = N.bit_length() - 1
+    tw = m.ntt_twiddles(ctx, w, log_n)
+    twi = m.ntt_twiddles(ctx, winv, log_n)
     ninv_m = int(oracle.to_mont(P, np.array([oracle.inverse(N, P)], np.uint32))[0])
     return ctx, w, winv, tw, twi, ninv_m
 
@@ -96,3 +96,20 @@ def test_ntt_many_rows_and_validation(m):
     assert L.mont_ntt(C.byref(ctx), d.data_ptr(), 1, 0, tw.data_ptr(), ctx.r1, None) == 4
     assert L.mont_ntt(C.byref(ctx), d.data_ptr(), 0, 10, tw.data_ptr(), ctx.r1, None) == 0
     assert L.mont_ntt(C.byref(ctx), d.data_ptr(), 1, 10, tw.data_ptr(), P, None) == 2
+
+
+@pytest.mark.parametrize("log_n", [1, 2, 5, 11, 16])
+def test_ntt_twiddle_table_layout(m, log_n):
+    """tw[2^(s-1) - 1 + pos] = to_mont(w^(pos N / 2^s)), checked against Python's pow."""
+    P = 2013265921
+    N = 1 << log_n
+    ctx = m.ctx_init(P)
+    w = oracle.root_of_unity(P, 31, N)
+    tw = m.ntt_twiddles(ctx, w, log_n).cpu().numpy()
+    assert tw.size == N - 1
+    rng = np.random.default_rng(log_n)
+    for e in set([0, N - 2] + list(rng.integers(0, N - 1, 200))):
+        s1 = int(e + 1).bit_length() - 1
+        pos = e + 1 - (1 << s1)
+        expo = pos * (N >> (s1 + 1))
+        assert int(tw[e]) == (pow(w, expo, P) << 32) % P

@@ -385,7 +385,7 @@ def test_guards_ntt(m, log_n, batch):
     N = 1 << log_n
     ctx = m.ctx_init(P)
     w = oracle.root_of_unity(P, 3, N)
-    tw = m.twiddle_table(ctx, w, max(1, N // 2))
+    tw = m.ntt_twiddles(ctx, w, log_n)
     x = synth.uniform(42, 26, P, 0, batch * N).reshape(batch, N)
     buf, o = guarded(batch * N, 0)
     o.copy_(dev(x.reshape(-1)))
