@@ -108,7 +108,7 @@ def test_ntt_twiddle_table_layout(m, log_n):
     tw = m.ntt_twiddles(ctx, w, log_n).cpu().numpy()
     assert tw.size == N - 1
     rng = np.random.default_rng(log_n)
-    for e in set([0, N - 2] + list(rng.integers(0, N - 1, 200))):
+    for e in set([0, N - 2] + [int(v) for v in rng.integers(0, N - 1, 200)]):
         s1 = int(e + 1).bit_length() - 1
         pos = e + 1 - (1 << s1)
         expo = pos * (N >> (s1 + 1))
