@@ -579,9 +579,16 @@ def main():
     import torch.distributed as dist
 
     from paper_1609_00999_b200 import shard
-    torch.cuda.set_device(local_rank)
+    # MONT_DIST_BACKEND=gloo + MONT_SHARE_GPU=1: orchestration dry run with all ranks on one GPU
+    # (the kernels of different ranks never wait on each other; only CPU-side gloo collectives)
+    backend = os.environ.get("MONT_DIST_BACKEND", "nccl")
+    dev_index = 0 if os.environ.get("MONT_SHARE_GPU") == "1" else local_rank
+    torch.cuda.set_device(dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
     wl = Workload(args.workload, rank, world)
     checks = verify(wl)
     ok = all(checks.values())
@@ -590,7 +597,7 @@ def main():
         if rank == 0:
             print(json.dumps({"error": "parity check failed", "checks": checks}), flush=True)
         sys.exit(1)
-    sampler = ClockSampler(nvsmi_id(torch, local_rank))
+    sampler = ClockSampler(nvsmi_id(torch, dev_index))
     sampler.start()
     for _ in range(max(3, args.warmup)):
         wl.step()
