@@ -84,6 +84,7 @@ def lib():
         L.oracle_fourier_redc.restype = C.c_uint32
         L.oracle_dft.argtypes = [C.c_uint32, C.c_uint32, _U32P, _U32P, C.c_size_t]
         L.oracle_cyclic_conv.argtypes = [C.c_uint32, _U32P, _U32P, _U32P, C.c_size_t]
+        L.oracle_dot.argtypes = [C.POINTER(Ctx), _U32P, _U32P, _U32P, C.c_size_t, C.c_size_t]
         L.oracle_inverse.argtypes = [C.c_uint32, C.c_uint32]
         L.oracle_inverse.restype = C.c_uint32
         L.oracle_mod_add.argtypes = [C.c_uint32] * 3
@@ -258,3 +259,13 @@ def cyclic_conv(P: int, a, b) -> np.ndarray:
 
 def inverse(x: int, P: int) -> int:
     return int(lib().oracle_inverse(x, P))
+
+
+def dot(P: int, A, x) -> np.ndarray:
+    """out[r] = sum_j A[r][j] x[j] R^-1 mod P (NEXT #4), by definition."""
+    A, x = _u32(A), _u32(x)
+    batch, length = A.shape
+    out = np.empty(batch, dtype=np.uint32)
+    c = ctx(P)
+    lib().oracle_dot(C.byref(c), out, A.reshape(-1), x, batch, length)
+    return out

@@ -385,3 +385,17 @@ uint32_t oracle_inverse(uint32_t x, uint32_t P)
     int64_t r = ext_euclid_inverse((int64_t)(x % P), (int64_t)P);
     return r < 0 ? 0u : (uint32_t)r;
 }
+
+/* Batched modular dot product by definition:
+ * out[r] = sum_j A[r][j] x[j] R^-1 mod P  =  (sum_j (A x mod P)) R^-1 mod P. */
+void oracle_dot(const oracle_ctx_t *c, uint32_t *out, const uint32_t *A, const uint32_t *x, size_t batch, size_t len)
+{
+    for (size_t r = 0; r < batch; ++r) {
+        uint64_t s = 0;
+        for (size_t j = 0; j < len; ++j) {
+            s += mulmod_naive(A[r * len + j] % c->P, x[j] % c->P, c->P);
+            s %= c->P;
+        }
+        out[r] = mulmod_naive((uint32_t)s, c->Rinv, c->P);
+    }
+}

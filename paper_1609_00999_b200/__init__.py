@@ -87,6 +87,7 @@ SIGNATURES = {
 
 SIGNATURES["mont_ntt"] = (C.c_int, [_CTX, _P, _S, C.c_int, _P, C.c_uint32, _P])
 SIGNATURES["mont_ntt_twiddles"] = (C.c_int, [_CTX, _P, C.c_uint32, C.c_int, _P])
+SIGNATURES["mont_dot"] = (C.c_int, [_CTX, _P, _P, _P, _S, _S, _P])
 
 
 class BarrettCtx(C.Structure):
@@ -383,6 +384,19 @@ def ntt(ctx: Ctx, data, tw, scale: int | None = None, stream=None):
     _check(lib().mont_ntt(C.byref(ctx), _ptr(data), batch, log_n, _ptr(tw), ctx.r1 if scale is None else scale,
                           _stream_handle(stream)), "mont_ntt")
     return data
+
+
+def dot(ctx: Ctx, A, x, out=None, stream=None):
+    """out[r] = sum_j A[r][j] x[j] R^-1 mod P for A (batch, len) (include/mont_dot.h)."""
+    torch = _torch()
+    _dev_u32(A, "A"), _dev_u32(x, "x")
+    if A.dim() != 2 or x.dim() != 1 or A.shape[1] != x.shape[0]:
+        raise ValueError("A must be (batch, len) and x (len,)")
+    if out is None:
+        out = torch.empty(A.shape[0], dtype=torch.uint32, device=A.device)
+    _check(lib().mont_dot(C.byref(ctx), _ptr(out), _ptr(A), _ptr(x), A.shape[0], A.shape[1],
+                          _stream_handle(stream)), "mont_dot")
+    return out
 
 
 def barrett_ctx_init(p: int) -> BarrettCtx:

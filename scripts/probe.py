@@ -226,3 +226,16 @@ if args.what in ("barrett",):
     med, _ = timeit(lambda: m.mul_vec(ctx, a, b, out=c))
     out(what="mul_vec_montgomery", us=med * 1e6, gbs=12 * nn / med / 1e9)
     sink = torch.empty(sms * 8 * 256, dtype=torch.uint32, device=dev)
+
+if args.what in ("dot",):
+    P = 2013265921
+    ctx = m.ctx_init(P)
+    batch, L = 4096, 1 << 14
+    A = torch.empty(batch * L, dtype=torch.uint32, device=dev)
+    m.synth_fill(A, 42, 31, 0, P)
+    A = A.view(batch, L)
+    x = torch.empty(L, dtype=torch.uint32, device=dev)
+    m.synth_fill(x, 42, 32, 0, P)
+    o = torch.empty(batch, dtype=torch.uint32, device=dev)
+    med, _ = timeit(lambda: m.dot(ctx, A, x, out=o))
+    out(what="dot", us=med * 1e6, gbs=4 * batch * L / med / 1e9, gmulmod=batch * L / med / 1e9)

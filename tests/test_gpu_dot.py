@@ -1,0 +1,38 @@
+"""Batched lazy-reduction dot products (include/mont_dot.h, NEXT #4) vs the oracle."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def m():
+    import paper_1609_00999_b200 as mod
+    return mod
+
+
+@pytest.mark.parametrize("P", list(synth.CONFIG_PRIMES) + [3, 17, 2147483647])
+@pytest.mark.parametrize("batch,L", [(1, 1), (3, 7), (5, 1024), (17, 4100), (2, 65536 + 4), (64, 16384)])
+def test_dot(m, P, batch, L):
+    A = synth.uniform(42, 31, P, 0, batch * L).reshape(batch, L)
+    x = synth.uniform(42, 32, P, 0, L)
+    A[0, 0] = P - 1
+    x[0] = P - 1
+    out = m.dot(m.ctx_init(P), torch.from_numpy(A).cuda(), torch.from_numpy(x).cuda())
+    assert np.array_equal(out.cpu().numpy(), oracle.dot(P, A, x))
+
+
+def test_dot_misaligned_and_extremes(m):
+    P = 2013265921
+    L = 1001
+    A = np.full((4, L), P - 1, np.uint32)
+    x = np.full(L, P - 1, np.uint32)
+    buf = torch.empty(4 * L + 1, dtype=torch.uint32, device="cuda")
+    tA = buf[1:].view(4, L)
+    tA.copy_(torch.from_numpy(A).cuda())
+    out = m.dot(m.ctx_init(P), tA, torch.from_numpy(x).cuda())
+    assert np.array_equal(out.cpu().numpy(), oracle.dot(P, A, x))

@@ -365,3 +365,17 @@ def test_mulmod_vec_pins():
     c = oracle.mulmod_vec(P, a, b)
     for i in range(0, 3000, 17):
         assert int(c[i]) == oracle.barrett(P, int(a[i]), int(b[i]))[0] == (int(a[i]) * int(b[i])) % P
+
+
+@pytest.mark.parametrize("P", CONFIG_PRIMES + (17,))
+def test_dot_pins(P):
+    """dot(A, to_mont(x)) is the plain dot product mod P (Python ints); the REDC-domain identity."""
+    rng = np.random.default_rng(31)
+    A = rng.integers(0, P, (5, 300), dtype=np.uint64).astype(np.uint32)
+    x = rng.integers(0, P, 300, dtype=np.uint64).astype(np.uint32)
+    got = oracle.dot(P, A, oracle.to_mont(P, x))
+    for r in range(5):
+        assert int(got[r]) == sum(int(a) * int(b) for a, b in zip(A[r], x)) % P
+    raw = oracle.dot(P, A, x)
+    for r in range(5):
+        assert (int(raw[r]) << 32) % P == sum(int(a) * int(b) for a, b in zip(A[r], x)) % P
