@@ -33,7 +33,11 @@ extern "C" {
  *                                   5/6/7/8 = 2-bit window with 3/2/1/0 of
  *                                   each 4 lanes on the IMAD pipe and the
  *                                   rest as FP64 Barrett products on the
- *                                   FP64 pipe.
+ *                                   FP64 pipe; 9 = 2-bit window with
+ *                                   Fourier-prime REDC products (PAPER.md
+ *                                   Alg. 3; P = c 2^n + 1, 2n >= 32,
+ *                                   3P < 2^32, 16-byte aligned operands,
+ *                                   else MONT_EUNSUPPORTED / EINVAL_ARG).
  *                                   ctas_per_sm = 0 selects a flat grid.
  *                 mont_mul_twiddle_ex : 0 = bulk-copy (TMA) staged table,
  *                                   1 = table read through L1/L2 (no smem)

@@ -284,6 +284,54 @@ __global__ void __launch_bounds__(256) k_pow_barrett(BarrettDev c, uint32_t *out
     }
 }
 
+// ---- Fourier-prime REDC ladder (variant 9): the same 2-bit window with every
+// product an Alg. 3 REDC (identical results to the Montgomery ladder)
+template <int L>
+__device__ __forceinline__ void pow_fourier(const PowParams &q, const FourierDev &f, const uint32_t (&base)[L],
+                                            const uint32_t (&e)[L], uint32_t (&out)[L]) {
+    uint32_t t1[L], t2[L], t3[L], acc[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+        t1[l] = redc(base[l], q.r2, (uint32_t)q.p, (uint32_t)q.pinv);  // to_mont, any uint32 base
+        t2[l] = fredc(t1[l], t1[l], f);
+        t3[l] = fredc(t2[l], t1[l], f);
+        const uint32_t d = e[l] >> 30;
+        acc[l] = d == 0 ? q.r1 : d == 1 ? t1[l] : d == 2 ? t2[l] : t3[l];
+    }
+#pragma unroll
+    for (int sh = 28; sh >= 0; sh -= 2) {
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+            uint32_t a = fredc(acc[l], acc[l], f);
+            a = fredc(a, a, f);
+            const uint32_t d = (e[l] >> sh) & 3u;
+            const uint32_t lo = (d & 1u) ? t1[l] : q.r1;
+            const uint32_t hi = (d & 1u) ? t3[l] : t2[l];
+            acc[l] = fredc(a, (d & 2u) ? hi : lo, f);
+        }
+    }
+#pragma unroll
+    for (int l = 0; l < L; ++l) out[l] = redc1(acc[l], (uint32_t)q.p, (uint32_t)q.pinv);
+}
+
+__global__ void __launch_bounds__(256) k_pow_fourier(PowParams q, FourierDev f, uint32_t *out, const uint32_t *base,
+                                                      const uint32_t *exp, size_t n) {
+    const size_t n4 = n / 4;
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n4) {
+        const uint4 bv = ld_stream(reinterpret_cast<const uint4 *>(base) + i);
+        const uint4 ev = ld_stream(reinterpret_cast<const uint4 *>(exp) + i);
+        uint32_t b[4] = {bv.x, bv.y, bv.z, bv.w}, e[4] = {ev.x, ev.y, ev.z, ev.w}, o[4];
+        pow_fourier<4>(q, f, b, e, o);
+        st_stream(reinterpret_cast<uint4 *>(out) + i, make_uint4(o[0], o[1], o[2], o[3]));
+    } else if (i < n4 + (n & 3)) {
+        const size_t j = 4 * n4 + (i - n4);
+        uint32_t b[1] = {base[j]}, e[1] = {exp[j]}, o[1];
+        pow_fourier<1>(q, f, b, e, o);
+        out[j] = o[0];
+    }
+}
+
 // tw[j] = to_mont(w^j): binary ladder on the bits of j, canonical output
 __global__ void __launch_bounds__(256) k_twiddle_table(Ctx c, uint32_t *tw, uint32_t w, size_t len) {
     for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += (size_t)gridDim.x * blockDim.x) {
@@ -338,10 +386,22 @@ extern "C" mont_status_t mont_pow_vec_ex(const mont_ctx_t *ctx, uint32_t *out, c
     if (n == 0) return MONT_OK;
     if (!out || !base || !exp || ((uintptr_t)out | (uintptr_t)base | (uintptr_t)exp) & 3u) return MONT_EINVAL_ARG;
     Launch L = resolve(cfg, kPowDefault);
-    if (L.threads != 256 || L.variant < 0 || L.variant > 8 || L.ctas_per_sm < 0) return MONT_EINVAL_ARG;
+    if (L.threads != 256 || L.variant < 0 || L.variant > 9 || L.ctas_per_sm < 0) return MONT_EINVAL_ARG;
     const int sms = sm_count();
     if (sms <= 0) return MONT_ECUDA;
     const PowParams q{(int32_t)ctx->p, (int32_t)(0u - ctx->pneg), ctx->r1, ctx->r2, (double)ctx->p, 1.0 / (double)ctx->p};
+    if (L.variant == 9) {  // Fourier-prime REDC ladder: P = c 2^n + 1, 2n >= 32, 3P < 2^32
+        uint32_t nn = 0, cc = ctx->p - 1u;
+        while ((cc & 1u) == 0u) { cc >>= 1; ++nn; }
+        if (2 * nn < 32 || (uint64_t)ctx->p * 3u >= (1ull << 32)) return MONT_EUNSUPPORTED;
+        if (((uintptr_t)out | (uintptr_t)base | (uintptr_t)exp) & 15u) return MONT_EINVAL_ARG;
+        const FourierDev f{ctx->p, cc, nn, cc << (2 * nn - 32)};
+        const size_t threads = n / 4 + (n & 3);
+        const size_t grid = (threads + 255) / 256;
+        if (grid > 0x7fffffff) return MONT_EUNSUPPORTED;
+        k_pow_fourier<<<(unsigned)grid, 256, 0, stream>>>(q, f, out, base, exp, n);
+        return launch_status();
+    }
     switch (L.variant) {
         case 0: return launch_pow<0>(q, out, base, exp, n, L.ctas_per_sm, sms, stream);
         case 1: return launch_pow<1>(q, out, base, exp, n, L.ctas_per_sm, sms, stream);

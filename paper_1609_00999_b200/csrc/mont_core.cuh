@@ -183,3 +183,34 @@ __device__ __forceinline__ uint32_t barrett(uint32_t a, uint32_t b, const Barret
 }
 
 }  // namespace mont
+
+namespace mont {
+
+// ---- Fourier-prime REDC (Alg. 3, :105-117)
+// for P = c 2^n + 1 with 2n >= 32 (all three config primes), R = 2^32:
+//   q1 = T >> 32, r1 = T mod R, q2 = c 2^n r1 / R, r2 = c 2^n r1 mod R,
+//   q3 = c 2^n r2 / R (r3 = 0, :117), t = q1 - q2 + q3 in [-(P-1), 2(P-1)].
+// With u = c r1: q2 = u >> (32-n), r2 = (u mod 2^(32-n)) << n, and
+// q3 = c (u mod 2^(32-n)) 2^(2n-32) exactly.  Here t + P is formed directly
+// (the +P folded into the q3 multiply-add) and lies in [1, 3P-1]; two unsigned
+// min-subtracts canonicalise, replacing the paper's three sign-mask steps (:108).
+// Requires 3P < 2^32 (P < 2^30.58); canonical inputs.  Cost on B200: IMAD.WIDE
+// (T) + IMAD.WIDE (u) + IMAD (q3) = 5 FMAHeavy slots, as many as Montgomery,
+// plus 5 ALU ops -- measured in k_pow variant 9.
+struct FourierDev {
+    uint32_t p, c, n, c_sh;  // c_sh = c << (2n - 32)
+};
+
+__device__ __forceinline__ uint32_t fredc(uint32_t a, uint32_t b, const FourierDev &f) {
+    const uint64_t T = mul_wide_u32(a, b);
+    const uint32_t q1 = hi32(T), r1 = (uint32_t)T;
+    const uint64_t u = mul_wide_u32(r1, f.c);
+    const uint32_t q2 = (uint32_t)(u >> (32 - f.n));
+    const uint32_t v = (uint32_t)u & ((1u << (32 - f.n)) - 1u);
+    const uint32_t q3p = v * f.c_sh + f.p;      // q3 + P
+    uint32_t t = q1 - q2 + q3p;                  // t + P in [1, 3P-1]
+    t = umin(t, t - f.p);
+    return umin(t, t - f.p);
+}
+
+}  // namespace mont

@@ -392,3 +392,23 @@ def test_guards_ntt(m, log_n, batch):
     m.ntt(ctx, o.view(batch, N), tw)
     assert np.array_equal(host(o).reshape(batch, N), oracle.dft(P, w, x))
     assert canaries_intact(buf, batch * N, 0)
+
+
+
+# ------------------------------------------ NEXT #2: Fourier-prime REDC ladder (variant 9)
+
+@pytest.mark.parametrize("P", [469762049, 998244353, 65537, 786433])
+@pytest.mark.parametrize("n", [1, 4, 5, 20003])
+def test_pow_fourier_variant(m, P, n):
+    # 469762049 = 7*2^26+1, 998244353 = 119*2^23+1, 65537 = 2^16+1, 786433 = 3*2^18+1
+    base = synth.uniform(42, 3, P, 0, n, low=1)
+    e = synth.exponents(42, 4, 0, n)
+    out = m.pow_vec(m.ctx_init(P), dev(base), dev(e), cfg=m.Launch(variant=9))
+    assert np.array_equal(host(out), oracle.power(P, base, e))
+
+
+def test_pow_fourier_unsupported(m):
+    for P in (2013265921, 1000003, 12289):   # 3P >= 2^32 / not a Fourier prime / 2n < 32
+        with pytest.raises(m.MontError) as ei:
+            m.pow_vec(m.ctx_init(P), dev(np.ones(8, np.uint32)), dev(np.ones(8, np.uint32)), cfg=m.Launch(variant=9))
+        assert ei.value.status == 4
