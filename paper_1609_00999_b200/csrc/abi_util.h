@@ -54,7 +54,8 @@ inline Launch resolve(const mont_launch_t *cfg, Launch def) {
 }
 
 inline bool launch_ok(const Launch &l) {
-    return l.threads >= 32 && l.threads <= 1024 && (l.threads % 32) == 0 && l.ctas_per_sm >= 1 &&
+    return l.threads >= 32 && l.threads <= 1024 && (l.threads % 32) == 0 && l.ctas_per_sm >= 1 && l.chunk >= 0 &&
+           (l.chunk % 4) == 0 &&
            l.ctas_per_sm <= 32 && (l.unroll == 1 || l.unroll == 2 || l.unroll == 4 || l.unroll == 8);
 }
 

@@ -18,6 +18,7 @@
 
 #include "../../include/barrett.h"
 #include "abi_util.h"
+#include "tma.cuh"
 
 namespace mont {
 
@@ -124,6 +125,47 @@ __global__ void __launch_bounds__(512) k_map2(Op op, uint32_t *c, const uint32_t
     if (SUM) block_sum_to(acc, s);
 }
 
+// Bulk-copy (TMA) variant: each CTA stages one tile of a and one of b into
+// shared memory with two cp.async.bulk copies completing on one mbarrier, then
+// computes from shared memory and stores c with 128-bit evict-first stores.
+// Flat grid, one tile per CTA; several CTAs per SM keep copies in flight.
+template <class Op, bool SUM>
+__global__ void __launch_bounds__(256) k_map2_tma(Op op, uint32_t *c, const uint32_t *a, const uint32_t *b,
+                                                   uint32_t head, size_t n4, uint32_t tail, unsigned long long *acc,
+                                                   uint32_t tile4) {
+    extern __shared__ __align__(128) uint4 sm[];
+    __shared__ __align__(8) uint64_t bar;
+    unsigned long long s = 0;
+    const uint4 *a4 = reinterpret_cast<const uint4 *>(a + head);
+    const uint4 *b4 = reinterpret_cast<const uint4 *>(b + head);
+    uint4 *c4 = reinterpret_cast<uint4 *>(c + head);
+    const size_t t0 = (size_t)blockIdx.x * tile4;
+    const uint32_t cnt = (uint32_t)(n4 - t0 < tile4 ? n4 - t0 : tile4);
+    if (threadIdx.x == 0 && cnt) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+        mbar_expect_tx(&bar, cnt * 32u);
+        bulk_g2s(sm, a4 + t0, cnt * 16u, &bar);
+        bulk_g2s(sm + tile4, b4 + t0, cnt * 16u, &bar);
+    }
+    if (blockIdx.x == 0 && threadIdx.x < head + tail) {
+        size_t i = threadIdx.x < head ? threadIdx.x : head + 4 * n4 + (threadIdx.x - head);
+        const uint32_t r = op(a[i], b[i]);
+        c[i] = r;
+        s += r;
+    }
+    __syncthreads();
+    if (cnt) {
+        mbar_wait(&bar, 0);
+        for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+            const uint4 r = apply4(op, sm[i], sm[tile4 + i]);
+            st_stream(c4 + t0 + i, r);
+            if (SUM) s += sum4(r);
+        }
+    }
+    if (SUM) block_sum_to(acc, s);
+}
+
 // 32-bit path for operands that do not share an address mod 16
 template <int U, class Op, bool SUM>
 __global__ void __launch_bounds__(512) k_map2_scalar(Op op, uint32_t *c, const uint32_t *a, const uint32_t *b,
@@ -224,6 +266,23 @@ static mont_status_t launch_map2(const Op &op, uint32_t *c, const uint32_t *a, c
     if (sms <= 0) return MONT_ECUDA;
     const uintptr_t pa = (uintptr_t)a, pb = (uintptr_t)b, pc = (uintptr_t)c;
     const bool flat = L.variant == 0;
+    if (L.variant == 2 && same_mod16(pa, pb) && same_mod16(pa, pc)) {  // bulk-copy (TMA) staged tiles
+        const uint32_t head = head_elems(pa, n);
+        const size_t n4 = (n - head) / 4;
+        const uint32_t tail = (uint32_t)((n - head) % 4);
+        const uint32_t tile4 = (uint32_t)((L.chunk > 0 ? L.chunk : 8192) / 4);
+        const size_t smem = (size_t)tile4 * 32;
+        if (tile4 == 0 || smem > 227 * 1024) return MONT_EINVAL_ARG;
+        size_t grid = (n4 + tile4 - 1) / tile4;
+        if (grid == 0) grid = 1;
+        if (grid > 0x7fffffff) return MONT_EUNSUPPORTED;
+        if (smem > 48 * 1024 &&
+            cudaFuncSetAttribute(k_map2_tma<Op, SUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+                cudaSuccess)
+            return MONT_ECUDA;
+        k_map2_tma<Op, SUM><<<(unsigned)grid, 256, smem, s>>>(op, c, a, b, head, n4, tail, acc, tile4);
+        return launch_status();
+    }
     if (same_mod16(pa, pb) && same_mod16(pa, pc)) {
         const uint32_t head = head_elems(pa, n);
         const size_t n4 = (n - head) / 4;

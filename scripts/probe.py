@@ -239,3 +239,24 @@ if args.what in ("dot",):
     o = torch.empty(batch, dtype=torch.uint32, device=dev)
     med, _ = timeit(lambda: m.dot(ctx, A, x, out=o))
     out(what="dot", us=med * 1e6, gbs=4 * batch * L / med / 1e9, gmulmod=batch * L / med / 1e9)
+
+if args.what in ("tma",):
+    import ctypes as C
+    n = 1 << 26
+    a = torch.empty(n, dtype=torch.uint32, device=dev)
+    b = torch.empty(n, dtype=torch.uint32, device=dev)
+    c = torch.empty(n, dtype=torch.uint32, device=dev)
+    m.synth_fill(a, 42, 1, 0, 2013265921)
+    m.synth_fill(b, 42, 2, 0, 2013265921)
+    ctx = m.ctx_init(2013265921)
+    acc = torch.zeros(1, dtype=torch.int64, device=dev)
+    for chunk in (0, 2048, 4096, 8192, 12288, 16384, 24576):
+        for variant in ((2,) if chunk else (0, 2)):
+            cfg = m.Launch(variant=variant, chunk=chunk)
+            med, best = timeit(lambda: m.mul_vec(ctx, a, b, out=c, cfg=cfg))
+            out(what="mul_vec", variant=variant, chunk=chunk, us=med * 1e6, gbs=12 * n / med / 1e9)
+            med, best = timeit(lambda: lib().mb_triad(c.data_ptr(), a.data_ptr(), b.data_ptr(), n, C.byref(cfg),
+                                                      s.cuda_stream))
+            out(what="triad", variant=variant, chunk=chunk, us=med * 1e6, gbs=12 * n / med / 1e9)
+            med, best = timeit(lambda: m.mul_vec_checksum(ctx, a, b, out=c, acc=acc, cfg=cfg))
+            out(what="mul_vec_checksum", variant=variant, chunk=chunk, us=med * 1e6, gbs=12 * n / med / 1e9)

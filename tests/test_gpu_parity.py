@@ -97,13 +97,14 @@ def test_mul_vec_one_operand_noncanonical(m):
 
 @pytest.mark.parametrize("oa,ob,oc", [(1, 1, 1), (2, 2, 2), (3, 3, 3), (0, 1, 2), (1, 0, 0), (3, 0, 1), (0, 0, 3)])
 @pytest.mark.parametrize("n", [0, 1, 2, 3, 5, 6, 9, 1023, 40_000 + 3])
-def test_mul_vec_alignment(m, oa, ob, oc, n):
+@pytest.mark.parametrize("variant", [0, 2])
+def test_mul_vec_alignment(m, oa, ob, oc, n, variant):
     P = 998244353
     a, b = synth.c2_inputs(P, 7, n)
     ta, tb = offset_view(a, oa), offset_view(b, ob)
     buf = dev(np.full(n + 8, 0xDEADBEEF, dtype=np.uint32))
     tc = buf[oc:oc + n]
-    m.mul_vec(m.ctx_init(P), ta, tb, out=tc)
+    m.mul_vec(m.ctx_init(P), ta, tb, out=tc, cfg=m.Launch(variant=variant))
     full = host(buf)
     assert np.array_equal(full[oc:oc + n], oracle.mont_mul(P, a, b))
     # nothing outside [oc, oc+n) was written
@@ -121,12 +122,14 @@ def test_mul_vec_in_place(m):
     assert np.array_equal(host(tb2), oracle.mont_mul(P, a, b))
 
 
-@pytest.mark.parametrize("threads,ctas,unroll,variant", [(32, 1, 1, 0), (128, 2, 2, 0), (256, 8, 8, 0),
-                                                         (512, 4, 4, 1), (512, 1, 8, 1), (64, 32, 4, 0)])
-def test_mul_vec_launch_configs(m, threads, ctas, unroll, variant):
+@pytest.mark.parametrize("threads,ctas,unroll,variant,chunk", [(32, 1, 1, 0, 0), (128, 2, 2, 0, 0), (256, 8, 8, 0, 0),
+                                                               (512, 4, 4, 1, 0), (512, 1, 8, 1, 0), (64, 32, 4, 0, 0),
+                                                               (256, 4, 1, 2, 0), (256, 4, 1, 2, 1024),
+                                                               (256, 4, 1, 2, 16384), (256, 4, 1, 2, 4)])
+def test_mul_vec_launch_configs(m, threads, ctas, unroll, variant, chunk):
     P = 2013265921
     a, b = synth.c2_inputs(P, 0, 300_007)
-    cfg = m.Launch(threads=threads, ctas_per_sm=ctas, unroll=unroll, variant=variant)
+    cfg = m.Launch(threads=threads, ctas_per_sm=ctas, unroll=unroll, variant=variant, chunk=chunk)
     c = m.mul_vec(m.ctx_init(P), dev(a), dev(b), cfg=cfg)
     assert np.array_equal(host(c), oracle.mont_mul(P, a, b))
 
@@ -311,7 +314,7 @@ def test_mul_vec_checksum_fused(m, n, off):
     assert int(acc.item()) == 2 * oracle.raw_sum(ref)
 
 
-@pytest.mark.parametrize("threads,unroll,variant", [(256, 1, 0), (512, 4, 0), (128, 2, 1), (256, 8, 1)])
+@pytest.mark.parametrize("threads,unroll,variant", [(256, 1, 0), (512, 4, 0), (128, 2, 1), (256, 8, 1), (256, 1, 2)])
 def test_mul_vec_checksum_configs(m, threads, unroll, variant):
     P = 998244353
     a, b = synth.c2_inputs(P, 0, 300_001)
