@@ -70,6 +70,35 @@ def test_c2_fullsize(m, P):
     assert bool((c2.view(torch.int32) == c.view(torch.int32)).all())
 
 
+@pytest.mark.parametrize("P", [P0, P1, P2])
+def test_c2_fullsize_every_element(m, P):
+    """configs[1] at full size, EVERY element against the oracle (host generator -> oracle on all
+    host cores) -- no sampling."""
+    n = 1 << 26
+    ha, hb = synth.c2_inputs(P, 0, n)
+    ref = oracle.mont_mul(P, ha, hb)
+    a = gen(n, 1, P, 0, True, m=m)
+    b = gen(n, 2, P, 0, True, m=m)
+    c, acc = m.mul_vec_checksum(m.ctx_init(P), a, b)
+    assert np.array_equal(a.cpu().numpy(), ha) and np.array_equal(b.cpu().numpy(), hb)
+    assert np.array_equal(c.cpu().numpy(), ref)
+    assert int(acc.item()) % P == oracle.checksum(P, ref)
+
+
+def test_c3_c4_fullsize_every_element(m):
+    """configs[2] and configs[3] at full size, every element against the oracle."""
+    batch, L = 4096, 1 << 14
+    hx = synth.c3_x(P0, batch=batch, length=L)
+    w = oracle.root_of_unity(P0, synth.G11_GENERATOR, L)
+    tw_ref = oracle.twiddle_table(P0, w, L)
+    ctx = m.ctx_init(P0)
+    out = m.mul_twiddle(ctx, torch.from_numpy(hx).cuda(), m.twiddle_table(ctx, w, L))
+    assert np.array_equal(out.cpu().numpy(), oracle.twiddle(P0, hx, tw_ref))
+    hb, he = synth.c4_inputs(P1, 0, 1 << 24)
+    outp = m.pow_vec(m.ctx_init(P1), torch.from_numpy(hb).cuda(), torch.from_numpy(he).cuda())
+    assert np.array_equal(outp.cpu().numpy(), oracle.power(P1, hb, he))
+
+
 def test_c1_full(m):
     """configs[0] exactly: full array vs the oracle, and its checksum."""
     a, b = synth.c1_inputs(P0)
