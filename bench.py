@@ -400,69 +400,53 @@ def time_steps(wl: Workload, K: int):
 
 
 def time_e2e(wl: Workload, steps: int):
-    """The same step through the library's HOST-buffer C ABI (include/mont_host.h): every
-    input starts in pinned host memory and every output lands in pinned host memory, inside
-    the timed region.  Each operation of the step is one host-buffer call on its own stream
-    with its own device workspace, so the chunked H2D / kernel / D2H pipelines of all
-    operations share both copy directions of the PCIe link concurrently."""
+    """The same step through the library's HOST-buffer C ABI (include/mont_host.h,
+    mont_host_run): every input starts in pinned host memory and every output lands in pinned
+    host memory, inside the timed region.  All operations of the step are jobs of one run,
+    whose chunks stream through one ring: one H2D stream, one compute stream, one D2H stream."""
     torch, m = wl.torch, wl.m
     pin = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t)
-    calls = []   # (fn(stream), ...) one per operation
-    ws_bytes = 192 << 20
+    empty = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    jobs, keep = [], []
     if hasattr(wl, "c2"):
         for si, P in enumerate(PRIMES):
             a, b, c = wl.c2[P]
-            ha, hb, hc = pin(a), pin(b), torch.empty(c.shape, dtype=c.dtype, pin_memory=True)
-            ws = m.host_workspace("mul_vec", min_bytes=ws_bytes)
-            calls.append(lambda s, ctx=wl.ctx[P], ha=ha, hb=hb, hc=hc, ws=ws:
-                         m.mul_vec_host(ctx, ha, hb, hc, ws, want_checksum=True, stream=s))
+            ha, hb, hc = pin(a), pin(b), empty(c)
+            acc = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+            jobs.append(m.host_job("mul_vec", wl.ctx[P], hc, ha, hb, acc=acc))
+            keep += [ha, hb, hc, acc]
     if hasattr(wl, "abar"):
         a0 = wl.c2[P0][0]
-        h_in, h_bar, h_back = pin(a0), torch.empty(a0.shape, dtype=a0.dtype, pin_memory=True), \
-            torch.empty(a0.shape, dtype=a0.dtype, pin_memory=True)
-        ws1 = m.host_workspace("to_mont", min_bytes=ws_bytes)
-        ws2 = m.host_workspace("from_mont", min_bytes=ws_bytes)
-
-        def tofrom(s, h_in=h_in, h_bar=h_bar, h_back=h_back, ws1=ws1, ws2=ws2):
-            m.to_mont_host(wl.ctx[P0], h_in, h_bar, ws1, stream=s)
-            # from_mont reads the host result of to_mont: same stream orders them
-            m.from_mont_host(wl.ctx[P0], h_bar, h_back, ws2, stream=s)
-        calls.append(tofrom)
+        h_in, h_bar, h_back = pin(a0), empty(a0), empty(a0)
+        jobs.append(m.host_job("to_mont", wl.ctx[P0], h_bar, h_in))
+        jobs.append(m.host_job("from_mont", wl.ctx[P0], h_back, h_bar, after_previous=True))
+        keep += [h_in, h_bar, h_back]
     if hasattr(wl, "tw_x"):
-        hx, htw = pin(wl.tw_x), pin(wl.tw)
-        ho = torch.empty(wl.tw_x.shape, dtype=torch.uint32, pin_memory=True)
-        ws = m.host_workspace("twiddle", TW_LEN, min_bytes=ws_bytes)
-        calls.append(lambda s, hx=hx, htw=htw, ho=ho, ws=ws: m.mul_twiddle_host(wl.ctx[P0], hx, htw, ho, ws, stream=s))
+        hx, htw, ho = pin(wl.tw_x), pin(wl.tw), empty(wl.tw_x)
+        jobs.append(m.host_job("twiddle", wl.ctx[P0], ho, hx, htw))
+        keep += [hx, htw, ho]
     if hasattr(wl, "pow_bufs"):
         base, e, o = wl.pow_bufs
-        hb, he, ho2 = pin(base), pin(e), torch.empty(o.shape, dtype=o.dtype, pin_memory=True)
-        ws = m.host_workspace("pow_vec", min_bytes=ws_bytes)
-        calls.append(lambda s, hb=hb, he=he, ho2=ho2, ws=ws: m.pow_vec_host(wl.ctx[P1], hb, he, ho2, ws, stream=s))
+        hb, he, ho2 = pin(base), pin(e), empty(o)
+        jobs.append(m.host_job("pow_vec", wl.ctx[P1], ho2, hb, he))
+        keep += [hb, he, ho2]
     if hasattr(wl, "c5"):
         a, b, c = wl.c5
-        ha, hb, hc = pin(a), pin(b), torch.empty(c.shape, dtype=c.dtype, pin_memory=True)
-        ws = m.host_workspace("mul_vec", min_bytes=ws_bytes)
-        calls.append(lambda s, ha=ha, hb=hb, hc=hc, ws=ws: m.mul_vec_host(wl.ctx[P0], ha, hb, hc, ws, True, stream=s))
-    streams = [torch.cuda.Stream() for _ in calls]
+        ha, hb, hc = pin(a), pin(b), empty(c)
+        acc = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+        jobs.append(m.host_job("mul_vec", wl.ctx[P0], hc, ha, hb, acc=acc))
+        keep += [ha, hb, hc, acc]
+    if hasattr(wl, "ntt_x"):
+        return None  # NTT has no host-buffer form
+    ws = m.host_workspace("twiddle", TW_LEN, min_bytes=512 << 20)
     cur = torch.cuda.current_stream()
-    torch.cuda.synchronize()
-
-    def one():
-        ev = torch.cuda.Event()
-        ev.record(cur)
-        for fn, s in zip(calls, streams):
-            s.wait_event(ev)
-            fn(s)
-        for s in streams:
-            cur.wait_stream(s)
-
-    one()
+    m.host_run(jobs, ws)
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(cur)
     for _ in range(steps):
-        one()
+        m.host_run(jobs, ws)
     e1.record(cur)
     e1.synchronize()
     return e0.elapsed_time(e1) / steps
@@ -637,7 +621,8 @@ def main():
         box_checksums = None
     e2e_ms = None
     if not args.no_e2e and world >= 1:
-        e2e_ms = shard.max_over_ranks(time_e2e(wl, max(1, args.e2e_steps)))
+        e2e_ms = time_e2e(wl, max(1, args.e2e_steps))
+        e2e_ms = None if e2e_ms is None else shard.max_over_ranks(e2e_ms)
     if rank != 0:
         if dist.is_initialized():
             dist.destroy_process_group()
@@ -702,9 +687,9 @@ def main():
         line["e2e"] = {"value": round(mulmods_job / (e2e_ms * 1e-3) / 1e9, 3), "unit": "Gmulmod/s",
                        "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": wl.h2d_bytes(),
                        "d2h_bytes_per_step": wl.d2h_bytes(),
-                       "path": "host-buffer C ABI (include/mont_host.h): every input H2D from pinned host and "
-                               "every output D2H to pinned host inside the timed region; one pipelined call per "
-                               "operation, concurrent on separate streams"}
+                       "path": "host-buffer C ABI (include/mont_host.h mont_host_run): every input H2D from "
+                               "pinned host and every output D2H to pinned host inside the timed region; all "
+                               "operations as jobs of one H2D / kernel / D2H ring"}
     if world == 1 and not args.no_cpu_baseline:
         v, cores, sample, secs, frac = cpu_baseline(wl.kind)
         line["cpu_baseline"] = {"value": round(v, 4), "unit": "Gmulmod/s", "cores": cores, "kind": "oracle",

@@ -60,6 +60,35 @@ mont_status_t mont_mul_twiddle_host(const mont_ctx_t *ctx, uint32_t *out_host, c
                                     const uint32_t *tw_host, size_t batch, size_t len, void *ws,
                                     size_t ws_bytes, cudaStream_t stream);
 
+/* ---- one pipelined run over many jobs (the e2e executor) ----
+ *
+ * The calls above pipeline one operation each; several of them share the PCIe
+ * link only as well as concurrent streams interleave.  mont_host_run streams
+ * the chunks of ALL jobs, in job order, through ONE ring of workspace slots:
+ * one H2D stream, one compute stream and one D2H stream, so the host->device
+ * direction stays busy from the first chunk to the last while results flow
+ * back concurrently -- the step costs ~max(total bytes in, total bytes out) /
+ * PCIe bandwidth.  Jobs are independent unless `after_previous` is set: then
+ * the job's first input copy waits until the previous job's outputs are in
+ * host memory (e.g. from_mont of the host result of to_mont).
+ * Workspace: 16-byte aligned; it holds the twiddle tables and checksum
+ * accumulators of the jobs plus 4 slots of 3 chunk buffers; the chunk size is
+ * derived from what is left (MONT_EINVAL_ARG if that is < one row / 256 words). */
+typedef struct mont_host_job {
+    int op;                        /* mont_host_op_t                                       */
+    const mont_ctx_t *ctx;
+    uint32_t *out;                 /* host                                                 */
+    const uint32_t *in0;           /* host: a / x / base                                   */
+    const uint32_t *in1;           /* host: b / exp / the len-word twiddle table (TWIDDLE) */
+    size_t n;                      /* elements (TWIDDLE: rows)                             */
+    size_t len;                    /* TWIDDLE: row length, else ignored                    */
+    unsigned long long *acc_host;  /* MUL_VEC: optional sum of out (overwritten)           */
+    int after_previous;            /* wait for the previous job's outputs                  */
+} mont_host_job_t;
+
+mont_status_t mont_host_run(const mont_host_job_t *jobs, int njobs, void *ws, size_t ws_bytes,
+                            cudaStream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

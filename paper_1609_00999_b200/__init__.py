@@ -105,6 +105,15 @@ SIGNATURES.update({
 HOST_OPS = {"mul_vec": 0, "to_mont": 1, "from_mont": 2, "pow_vec": 3, "twiddle": 4}
 
 
+class HostJob(C.Structure):
+    """mont_host_job_t (include/mont_host.h)."""
+    _fields_ = [("op", C.c_int), ("ctx", _CTX), ("out", C.c_void_p), ("in0", C.c_void_p), ("in1", C.c_void_p),
+                ("n", C.c_size_t), ("len", C.c_size_t), ("acc_host", C.c_void_p), ("after_previous", C.c_int)]
+
+
+SIGNATURES["mont_host_run"] = (C.c_int, [C.POINTER(HostJob), C.c_int, _P, _S, _P])
+
+
 def lib():
     """Load libmont.so (built in-tree by __graft_entry__.build() / make)."""
     global _lib
@@ -420,6 +429,29 @@ def barrett_pow_vec(ctx: BarrettCtx, base, exp, out=None, stream=None):
     _check(lib().barrett_pow_vec(C.byref(ctx), _ptr(out), _ptr(base), _ptr(exp), base.numel(),
                                  _stream_handle(stream)), "barrett_pow_vec")
     return out
+
+
+def host_job(op: str, ctx: Ctx, out, in0, in1=None, acc=None, after_previous: bool = False) -> HostJob:
+    """Describe one operation on HOST tensors for host_run(); twiddle: in0 = x (batch, len), in1 = tw."""
+    j = HostJob()
+    j.op = HOST_OPS[op]
+    j.ctx = C.pointer(ctx)
+    j.out, j.in0 = _ptr(_host_u32(out, "out")), _ptr(_host_u32(in0, "in0"))
+    j.in1 = _ptr(_host_u32(in1, "in1")) if in1 is not None else None
+    if op == "twiddle":
+        j.n, j.len = in0.shape[0], in0.shape[1]
+    else:
+        j.n, j.len = in0.numel(), 0
+    j.acc_host = _ptr(acc) if acc is not None else None
+    j.after_previous = int(after_previous)
+    j._keep = (ctx, out, in0, in1, acc)  # keep the referenced objects alive
+    return j
+
+
+def host_run(jobs, ws, stream=None):
+    """Stream all jobs' chunks through one H2D / kernel / D2H ring (mont_host_run)."""
+    arr = (HostJob * len(jobs))(*jobs)
+    _check(lib().mont_host_run(arr, len(jobs), _ptr(ws), ws.numel(), _stream_handle(stream)), "mont_host_run")
 
 
 def sm_count() -> int:

@@ -225,3 +225,160 @@ extern "C" mont_status_t mont_mul_twiddle_host(const mont_ctx_t *ctx, uint32_t *
     };
     return pipeline(1, in, out_host, batch, len, ws, ws_bytes, len * 4, stream, pre, launch, no_hook);
 }
+
+// ------------------------------------------------------------ mont_host_run
+namespace mont {
+namespace {
+
+constexpr int kRing = 4;
+
+struct JobPlan {
+    int nin;            // streamed inputs (1 or 2)
+    size_t units;       // chunkable units
+    size_t unit_words;  // words per unit
+    size_t chunk;       // units per chunk
+    uint32_t *dtab;     // device twiddle table (TWIDDLE)
+    unsigned long long *dacc;  // device accumulator (MUL_VEC with acc_host)
+};
+
+struct Ring {
+    cudaStream_t h2d = nullptr, krn = nullptr, d2h = nullptr;
+    cudaEvent_t start = nullptr, done_k = nullptr, done_d = nullptr, job_out = nullptr;
+    cudaEvent_t h2d_done[kRing] = {}, k_done[kRing] = {}, d2h_done[kRing] = {};
+    bool ok = true;
+    Ring() {
+        ok &= cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking) == cudaSuccess;
+        ok &= cudaStreamCreateWithFlags(&krn, cudaStreamNonBlocking) == cudaSuccess;
+        ok &= cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking) == cudaSuccess;
+        cudaEvent_t *evs[] = {&start, &done_k, &done_d, &job_out};
+        for (cudaEvent_t *e : evs) ok &= cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
+        for (int s = 0; s < kRing; ++s) {
+            ok &= cudaEventCreateWithFlags(&h2d_done[s], cudaEventDisableTiming) == cudaSuccess;
+            ok &= cudaEventCreateWithFlags(&k_done[s], cudaEventDisableTiming) == cudaSuccess;
+            ok &= cudaEventCreateWithFlags(&d2h_done[s], cudaEventDisableTiming) == cudaSuccess;
+        }
+    }
+    ~Ring() {
+        for (int s = 0; s < kRing; ++s) {
+            if (h2d_done[s]) cudaEventDestroy(h2d_done[s]);
+            if (k_done[s]) cudaEventDestroy(k_done[s]);
+            if (d2h_done[s]) cudaEventDestroy(d2h_done[s]);
+        }
+        cudaEvent_t evs[] = {start, done_k, done_d, job_out};
+        for (cudaEvent_t e : evs)
+            if (e) cudaEventDestroy(e);
+        if (h2d) cudaStreamDestroy(h2d);
+        if (krn) cudaStreamDestroy(krn);
+        if (d2h) cudaStreamDestroy(d2h);
+    }
+};
+
+}  // namespace
+}  // namespace mont
+
+extern "C" mont_status_t mont_host_run(const mont_host_job_t *jobs, int njobs, void *ws, size_t ws_bytes,
+                                       cudaStream_t stream) {
+    if (njobs < 0 || (njobs > 0 && !jobs) || (njobs > 0 && (!ws || ((uintptr_t)ws & 15u)))) return MONT_EINVAL_ARG;
+    if (njobs == 0) return MONT_OK;
+    // plan: reserved area (tables, accumulators), then the ring
+    JobPlan plan[64];
+    if (njobs > 64) return MONT_EUNSUPPORTED;
+    size_t reserved = 0;
+    for (int j = 0; j < njobs; ++j) {
+        const mont_host_job_t &J = jobs[j];
+        if (!ctx_ok(J.ctx)) return J.ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
+        JobPlan &P = plan[j];
+        P.dtab = nullptr;
+        P.dacc = nullptr;
+        switch (J.op) {
+            case MONT_HOST_MUL_VEC: P.nin = 2; P.unit_words = 1; P.units = J.n; break;
+            case MONT_HOST_POW_VEC: P.nin = 2; P.unit_words = 1; P.units = J.n; break;
+            case MONT_HOST_TO_MONT:
+            case MONT_HOST_FROM_MONT: P.nin = 1; P.unit_words = 1; P.units = J.n; break;
+            case MONT_HOST_TWIDDLE:
+                if (J.len == 0 && J.n) return MONT_EINVAL_ARG;
+                P.nin = 1; P.unit_words = J.len; P.units = J.n;
+                P.dtab = (uint32_t *)((char *)ws + reserved);
+                reserved += align_up(J.len * 4);
+                break;
+            default: return MONT_EINVAL_ARG;
+        }
+        if (J.n && (!J.out || !J.in0 || (P.nin == 2 && !J.in1) || (J.op == MONT_HOST_TWIDDLE && !J.in1)))
+            return MONT_EINVAL_ARG;
+        if (J.op == MONT_HOST_MUL_VEC && J.acc_host) {
+            P.dacc = (unsigned long long *)((char *)ws + reserved);
+            reserved += kAlign;
+        }
+    }
+    if (ws_bytes < reserved + kRing * 3 * kAlign) return MONT_EINVAL_ARG;
+    const size_t buf_bytes = ((ws_bytes - reserved) / (kRing * 3)) / kAlign * kAlign;
+    char *ring = (char *)ws + reserved;
+    auto slot_buf = [&](int slot, int k) { return (uint32_t *)(ring + ((size_t)slot * 3 + k) * buf_bytes); };
+    for (int j = 0; j < njobs; ++j) {
+        plan[j].chunk = buf_bytes / (plan[j].unit_words * 4);
+        if (plan[j].chunk == 0 && jobs[j].n) return MONT_EINVAL_ARG;
+    }
+
+    Ring R;
+    if (!R.ok) return MONT_ECUDA;
+    if (cudaEventRecord(R.start, stream) != cudaSuccess) return MONT_ECUDA;
+    cudaStreamWaitEvent(R.h2d, R.start, 0);
+    cudaStreamWaitEvent(R.krn, R.start, 0);
+    cudaStreamWaitEvent(R.d2h, R.start, 0);
+    // prologue: tables in, accumulators zeroed
+    for (int j = 0; j < njobs; ++j) {
+        if (plan[j].dtab &&
+            cudaMemcpyAsync(plan[j].dtab, jobs[j].in1, jobs[j].len * 4, cudaMemcpyHostToDevice, R.h2d) != cudaSuccess)
+            return MONT_ECUDA;
+        if (plan[j].dacc && cudaMemsetAsync(plan[j].dacc, 0, 8, R.krn) != cudaSuccess) return MONT_ECUDA;
+    }
+    size_t g = 0;  // global chunk counter -> ring slot
+    for (int j = 0; j < njobs; ++j) {
+        const mont_host_job_t &J = jobs[j];
+        const JobPlan &P = plan[j];
+        if (J.after_previous && j > 0) cudaStreamWaitEvent(R.h2d, R.job_out, 0);
+        for (size_t u0 = 0; u0 < P.units; u0 += P.chunk, ++g) {
+            const int slot = (int)(g % kRing);
+            const size_t nu = P.units - u0 < P.chunk ? P.units - u0 : P.chunk;
+            const size_t off = u0 * P.unit_words, bytes = nu * P.unit_words * 4;
+            if (g >= (size_t)kRing) cudaStreamWaitEvent(R.h2d, R.k_done[slot], 0);
+            uint32_t *d0 = slot_buf(slot, 0), *d1 = slot_buf(slot, 1), *dout = slot_buf(slot, 2);
+            if (cudaMemcpyAsync(d0, J.in0 + off, bytes, cudaMemcpyHostToDevice, R.h2d) != cudaSuccess)
+                return MONT_ECUDA;
+            if (P.nin == 2 &&
+                cudaMemcpyAsync(d1, J.in1 + off, bytes, cudaMemcpyHostToDevice, R.h2d) != cudaSuccess)
+                return MONT_ECUDA;
+            cudaEventRecord(R.h2d_done[slot], R.h2d);
+            cudaStreamWaitEvent(R.krn, R.h2d_done[slot], 0);
+            if (g >= (size_t)kRing) cudaStreamWaitEvent(R.krn, R.d2h_done[slot], 0);
+            mont_status_t st;
+            switch (J.op) {
+                case MONT_HOST_MUL_VEC:
+                    st = P.dacc ? mont_mul_vec_checksum(J.ctx, dout, d0, d1, nu, P.dacc, R.krn)
+                                : mont_mul_vec(J.ctx, dout, d0, d1, nu, R.krn);
+                    break;
+                case MONT_HOST_POW_VEC: st = mont_pow_vec(J.ctx, dout, d0, d1, nu, R.krn); break;
+                case MONT_HOST_TO_MONT: st = to_mont(J.ctx, dout, d0, nu, R.krn); break;
+                case MONT_HOST_FROM_MONT: st = from_mont(J.ctx, dout, d0, nu, R.krn); break;
+                default: st = mont_mul_twiddle(J.ctx, dout, d0, P.dtab, nu, J.len, R.krn); break;
+            }
+            if (st != MONT_OK) return st;
+            cudaEventRecord(R.k_done[slot], R.krn);
+            cudaStreamWaitEvent(R.d2h, R.k_done[slot], 0);
+            if (cudaMemcpyAsync(J.out + off, dout, bytes, cudaMemcpyDeviceToHost, R.d2h) != cudaSuccess)
+                return MONT_ECUDA;
+            cudaEventRecord(R.d2h_done[slot], R.d2h);
+        }
+        if (P.dacc) {
+            cudaStreamWaitEvent(R.d2h, R.k_done[(g + kRing - 1) % kRing], 0);
+            if (cudaMemcpyAsync(J.acc_host, P.dacc, 8, cudaMemcpyDeviceToHost, R.d2h) != cudaSuccess)
+                return MONT_ECUDA;
+        }
+        cudaEventRecord(R.job_out, R.d2h);  // this job's outputs are (will be) in host memory
+    }
+    cudaEventRecord(R.done_k, R.krn);
+    cudaEventRecord(R.done_d, R.d2h);
+    cudaStreamWaitEvent(stream, R.done_k, 0);
+    cudaStreamWaitEvent(stream, R.done_d, 0);
+    return launch_status();
+}

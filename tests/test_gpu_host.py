@@ -98,3 +98,39 @@ def test_host_validation(m):
     assert L.mont_mul_vec_host(C.byref(ctx), a.data_ptr(), a.data_ptr(), a.data_ptr(), 10, None, ws.data_ptr(),
                                16, None) == 2   # workspace too small
     assert m.lib().mont_host_min_workspace(4, 16384) > 6 * 65536
+
+
+def test_host_run_many_jobs(m):
+    """One ring over mul_vec (x2, one with checksum), to_mont -> from_mont (chained), pow, twiddle."""
+    P, P1_ = 2013265921, 469762049
+    ctx, ctx1 = m.ctx_init(P), m.ctx_init(P1_)
+    n = (1 << 20) + 3
+    a, b = synth.c2_inputs(P, 0, n)
+    a2, b2 = synth.c2_inputs(P1_, 5, 777)
+    base, e = synth.c4_inputs(P1_, 0, 4099)
+    L = 4096
+    x = synth.c3_x(P, batch=33, length=L)
+    tw = synth.uniform(42, 11, P, 0, L)
+    ha, hb, ha2, hb2, hbase, he, hx, htw = (host(v) for v in (a, b, a2, b2, base, e, x, tw))
+    o1, o2, o3, o4, o5 = empty(n), empty(777), empty(n), empty(n), empty(4099)
+    o6 = torch.empty((33, L), dtype=torch.uint32, pin_memory=True)
+    acc = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+    jobs = [m.host_job("mul_vec", ctx, o1, ha, hb, acc=acc),
+            m.host_job("mul_vec", ctx1, o2, ha2, hb2),
+            m.host_job("to_mont", ctx, o3, ha),
+            m.host_job("from_mont", ctx, o4, o3, after_previous=True),
+            m.host_job("pow_vec", ctx1, o5, hbase, he),
+            m.host_job("twiddle", ctx, o6, hx, htw)]
+    for ws_mb in (1, 3, 64):
+        for o in (o1, o2, o3, o4, o5, o6):
+            o.zero_()
+        acc.zero_()
+        m.host_run(jobs, m.host_workspace("twiddle", L, min_bytes=ws_mb << 20))
+        torch.cuda.synchronize()
+        ref1 = oracle.mont_mul(P, a, b)
+        assert np.array_equal(o1.numpy(), ref1) and int(acc.item()) == oracle.raw_sum(ref1)
+        assert np.array_equal(o2.numpy(), oracle.mont_mul(P1_, a2, b2))
+        assert np.array_equal(o3.numpy(), oracle.to_mont(P, a))
+        assert np.array_equal(o4.numpy(), a)
+        assert np.array_equal(o5.numpy(), oracle.power(P1_, base, e))
+        assert np.array_equal(o6.numpy(), oracle.twiddle(P, x, tw))
