@@ -260,3 +260,45 @@ if args.what in ("tma",):
             out(what="triad", variant=variant, chunk=chunk, us=med * 1e6, gbs=12 * n / med / 1e9)
             med, best = timeit(lambda: m.mul_vec_checksum(ctx, a, b, out=c, acc=acc, cfg=cfg))
             out(what="mul_vec_checksum", variant=variant, chunk=chunk, us=med * 1e6, gbs=12 * n / med / 1e9)
+
+if args.what in ("hostrun",):
+    import numpy as np
+    P = 2013265921
+    ctx = m.ctx_init(P)
+    n = 1 << 26
+    ha = torch.empty(n, dtype=torch.uint32, pin_memory=True)
+    hb = torch.empty(n, dtype=torch.uint32, pin_memory=True)
+    hcs = [torch.empty(n, dtype=torch.uint32, pin_memory=True) for _ in range(3)]
+    d = torch.empty(n, dtype=torch.uint32, device=dev)
+    m.synth_fill(d, 42, 1, 0, P)
+    ha.copy_(d)
+    m.synth_fill(d, 42, 2, 0, P)
+    hb.copy_(d)
+    for ws_mb in (96, 192, 512, 1024):
+        ws = m.host_workspace("mul_vec", min_bytes=ws_mb << 20)
+        jobs = [m.host_job("mul_vec", ctx, hc, ha, hb) for hc in hcs]
+        med, _ = timeit(lambda: m.host_run(jobs, ws), reps=3, warm=1)
+        out(what="host_run 3x mul_vec", ws_mb=ws_mb, ms=med * 1e3, h2d_gbs=3 * 8 * n / med / 1e9,
+            d2h_gbs=3 * 4 * n / med / 1e9)
+    # raw: the same bytes as two big concurrent copies
+    dbig = torch.empty(6 * n, dtype=torch.uint32, device=dev)
+    hbig = torch.empty(6 * n, dtype=torch.uint32, pin_memory=True)
+    dout = torch.empty(3 * n, dtype=torch.uint32, device=dev)
+    hout = torch.empty(3 * n, dtype=torch.uint32, pin_memory=True)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def raw():
+        ev = torch.cuda.Event()
+        ev.record()
+        s1.wait_event(ev)
+        s2.wait_event(ev)
+        with torch.cuda.stream(s1):
+            dbig.copy_(hbig, non_blocking=True)
+        with torch.cuda.stream(s2):
+            hout.copy_(dout, non_blocking=True)
+        torch.cuda.current_stream().wait_stream(s1)
+        torch.cuda.current_stream().wait_stream(s2)
+    med, _ = timeit(raw, reps=3, warm=1)
+    out(what="raw 1.5GB h2d || 0.75GB d2h", ms=med * 1e3, h2d_gbs=24 * n / med / 1e9)
+    med, _ = timeit(lambda: dbig.copy_(hbig, non_blocking=True), reps=3, warm=1)
+    out(what="raw 1.5GB h2d alone", ms=med * 1e3, gbs=24 * n / med / 1e9)
