@@ -68,9 +68,10 @@ mont_status_t mont_mul_twiddle_host(const mont_ctx_t *ctx, uint32_t *out_host, c
  * one H2D stream, one compute stream and one D2H stream, so the host->device
  * direction stays busy from the first chunk to the last while results flow
  * back concurrently -- the step costs ~max(total bytes in, total bytes out) /
- * PCIe bandwidth.  Jobs are independent unless `after_previous` is set: then
- * the job's first input copy waits until the previous job's outputs are in
- * host memory (e.g. from_mont of the host result of to_mont).
+ * PCIe bandwidth.  Jobs are independent unless `depends_on` >= 0: then the
+ * job's first input copy waits until job `depends_on` (an earlier index) has
+ * all its outputs in host memory (e.g. from_mont of the host result of
+ * to_mont) -- put independent jobs in between to hide the wait.
  * Workspace: 16-byte aligned; it holds the twiddle tables and checksum
  * accumulators of the jobs plus 4 slots of 3 chunk buffers; the chunk size is
  * derived from what is left (MONT_EINVAL_ARG if that is < one row / 256 words). */
@@ -83,7 +84,7 @@ typedef struct mont_host_job {
     size_t n;                      /* elements (TWIDDLE: rows)                             */
     size_t len;                    /* TWIDDLE: row length, else ignored                    */
     unsigned long long *acc_host;  /* MUL_VEC: optional sum of out (overwritten)           */
-    int after_previous;            /* wait for the previous job's outputs                  */
+    int depends_on;                /* index of an earlier job whose outputs this reads, or -1 */
 } mont_host_job_t;
 
 mont_status_t mont_host_run(const mont_host_job_t *jobs, int njobs, void *ws, size_t ws_bytes,

@@ -108,7 +108,7 @@ HOST_OPS = {"mul_vec": 0, "to_mont": 1, "from_mont": 2, "pow_vec": 3, "twiddle":
 class HostJob(C.Structure):
     """mont_host_job_t (include/mont_host.h)."""
     _fields_ = [("op", C.c_int), ("ctx", _CTX), ("out", C.c_void_p), ("in0", C.c_void_p), ("in1", C.c_void_p),
-                ("n", C.c_size_t), ("len", C.c_size_t), ("acc_host", C.c_void_p), ("after_previous", C.c_int)]
+                ("n", C.c_size_t), ("len", C.c_size_t), ("acc_host", C.c_void_p), ("depends_on", C.c_int)]
 
 
 SIGNATURES["mont_host_run"] = (C.c_int, [C.POINTER(HostJob), C.c_int, _P, _S, _P])
@@ -431,7 +431,7 @@ def barrett_pow_vec(ctx: BarrettCtx, base, exp, out=None, stream=None):
     return out
 
 
-def host_job(op: str, ctx: Ctx, out, in0, in1=None, acc=None, after_previous: bool = False) -> HostJob:
+def host_job(op: str, ctx: Ctx, out, in0, in1=None, acc=None, depends_on: int = -1) -> HostJob:
     """Describe one operation on HOST tensors for host_run(); twiddle: in0 = x (batch, len), in1 = tw."""
     j = HostJob()
     j.op = HOST_OPS[op]
@@ -443,7 +443,7 @@ def host_job(op: str, ctx: Ctx, out, in0, in1=None, acc=None, after_previous: bo
     else:
         j.n, j.len = in0.numel(), 0
     j.acc_host = _ptr(acc) if acc is not None else None
-    j.after_previous = int(after_previous)
+    j.depends_on = int(depends_on)
     j._keep = (ctx, out, in0, in1, acc)  # keep the referenced objects alive
     return j
 

@@ -243,14 +243,15 @@ struct JobPlan {
 
 struct Ring {
     cudaStream_t h2d = nullptr, krn = nullptr, d2h = nullptr;
-    cudaEvent_t start = nullptr, done_k = nullptr, done_d = nullptr, job_out = nullptr;
+    cudaEvent_t start = nullptr, done_k = nullptr, done_d = nullptr;
+    cudaEvent_t job_out[64] = {};
     cudaEvent_t h2d_done[kRing] = {}, k_done[kRing] = {}, d2h_done[kRing] = {};
     bool ok = true;
     Ring() {
         ok &= cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking) == cudaSuccess;
         ok &= cudaStreamCreateWithFlags(&krn, cudaStreamNonBlocking) == cudaSuccess;
         ok &= cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking) == cudaSuccess;
-        cudaEvent_t *evs[] = {&start, &done_k, &done_d, &job_out};
+        cudaEvent_t *evs[] = {&start, &done_k, &done_d};
         for (cudaEvent_t *e : evs) ok &= cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
         for (int s = 0; s < kRing; ++s) {
             ok &= cudaEventCreateWithFlags(&h2d_done[s], cudaEventDisableTiming) == cudaSuccess;
@@ -264,8 +265,10 @@ struct Ring {
             if (k_done[s]) cudaEventDestroy(k_done[s]);
             if (d2h_done[s]) cudaEventDestroy(d2h_done[s]);
         }
-        cudaEvent_t evs[] = {start, done_k, done_d, job_out};
+        cudaEvent_t evs[] = {start, done_k, done_d};
         for (cudaEvent_t e : evs)
+            if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : job_out)
             if (e) cudaEventDestroy(e);
         if (h2d) cudaStreamDestroy(h2d);
         if (krn) cudaStreamDestroy(krn);
@@ -305,6 +308,7 @@ extern "C" mont_status_t mont_host_run(const mont_host_job_t *jobs, int njobs, v
         }
         if (J.n && (!J.out || !J.in0 || (P.nin == 2 && !J.in1) || (J.op == MONT_HOST_TWIDDLE && !J.in1)))
             return MONT_EINVAL_ARG;
+        if (J.depends_on >= j || J.depends_on < -1) return MONT_EINVAL_ARG;
         if (J.op == MONT_HOST_MUL_VEC && J.acc_host) {
             P.dacc = (unsigned long long *)((char *)ws + reserved);
             reserved += kAlign;
@@ -321,6 +325,11 @@ extern "C" mont_status_t mont_host_run(const mont_host_job_t *jobs, int njobs, v
 
     Ring R;
     if (!R.ok) return MONT_ECUDA;
+    for (int j = 0; j < njobs; ++j) {  // completion events only for jobs someone depends on
+        const int d = jobs[j].depends_on;
+        if (d >= 0 && !R.job_out[d] && cudaEventCreateWithFlags(&R.job_out[d], cudaEventDisableTiming) != cudaSuccess)
+            return MONT_ECUDA;
+    }
     if (cudaEventRecord(R.start, stream) != cudaSuccess) return MONT_ECUDA;
     cudaStreamWaitEvent(R.h2d, R.start, 0);
     cudaStreamWaitEvent(R.krn, R.start, 0);
@@ -336,7 +345,7 @@ extern "C" mont_status_t mont_host_run(const mont_host_job_t *jobs, int njobs, v
     for (int j = 0; j < njobs; ++j) {
         const mont_host_job_t &J = jobs[j];
         const JobPlan &P = plan[j];
-        if (J.after_previous && j > 0) cudaStreamWaitEvent(R.h2d, R.job_out, 0);
+        if (J.depends_on >= 0) cudaStreamWaitEvent(R.h2d, R.job_out[J.depends_on], 0);
         for (size_t u0 = 0; u0 < P.units; u0 += P.chunk, ++g) {
             const int slot = (int)(g % kRing);
             const size_t nu = P.units - u0 < P.chunk ? P.units - u0 : P.chunk;
@@ -374,7 +383,7 @@ extern "C" mont_status_t mont_host_run(const mont_host_job_t *jobs, int njobs, v
             if (cudaMemcpyAsync(J.acc_host, P.dacc, 8, cudaMemcpyDeviceToHost, R.d2h) != cudaSuccess)
                 return MONT_ECUDA;
         }
-        cudaEventRecord(R.job_out, R.d2h);  // this job's outputs are (will be) in host memory
+        if (R.job_out[j]) cudaEventRecord(R.job_out[j], R.d2h);  // this job's outputs are in host memory
     }
     cudaEventRecord(R.done_k, R.krn);
     cudaEventRecord(R.done_d, R.d2h);

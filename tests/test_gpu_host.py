@@ -114,15 +114,17 @@ def test_host_run_many_jobs(m):
     ha, hb, ha2, hb2, hbase, he, hx, htw = (host(v) for v in (a, b, a2, b2, base, e, x, tw))
     o1, o2, o3, o4, o5 = empty(n), empty(777), empty(n), empty(n), empty(4099)
     o6 = torch.empty((33, L), dtype=torch.uint32, pin_memory=True)
+    o7 = empty(n)
     acc = torch.zeros(1, dtype=torch.int64, pin_memory=True)
     jobs = [m.host_job("mul_vec", ctx, o1, ha, hb, acc=acc),
             m.host_job("mul_vec", ctx1, o2, ha2, hb2),
             m.host_job("to_mont", ctx, o3, ha),
-            m.host_job("from_mont", ctx, o4, o3, after_previous=True),
+            m.host_job("from_mont", ctx, o4, o3, depends_on=2),
             m.host_job("pow_vec", ctx1, o5, hbase, he),
-            m.host_job("twiddle", ctx, o6, hx, htw)]
+            m.host_job("twiddle", ctx, o6, hx, htw),
+            m.host_job("from_mont", ctx, o7, o3, depends_on=2)]
     for ws_mb in (1, 3, 64):
-        for o in (o1, o2, o3, o4, o5, o6):
+        for o in (o1, o2, o3, o4, o5, o6, o7):
             o.zero_()
         acc.zero_()
         m.host_run(jobs, m.host_workspace("twiddle", L, min_bytes=ws_mb << 20))
@@ -134,3 +136,4 @@ def test_host_run_many_jobs(m):
         assert np.array_equal(o4.numpy(), a)
         assert np.array_equal(o5.numpy(), oracle.power(P1_, base, e))
         assert np.array_equal(o6.numpy(), oracle.twiddle(P, x, tw))
+        assert np.array_equal(o7.numpy(), a)
