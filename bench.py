@@ -70,6 +70,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--soak", type=float, default=1.0, help="seconds of untimed steps before timing (clocks)")
     ap.add_argument("--serial", action="store_true", help="report the serial (one-stream) step instead")
+    ap.add_argument("--graph", action="store_true", help="replay the two-lane step as one CUDA graph")
     ap.add_argument("--pow-ctas", type=int, default=5, help="CTAs per SM of the persistent pow grid (0 = flat)")
     return ap.parse_args()
 
@@ -374,6 +375,36 @@ def time_steps_concurrent(wl: Workload, K: int):
     return start.elapsed_time(end)
 
 
+def capture_step_graph(wl: Workload):
+    """Capture one two-lane step (both lanes, forked from and joined into the capture stream)
+    into a CUDA graph; replaying it issues the step's launches with one graph launch."""
+    torch = wl.torch
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        wl.step_concurrent()            # warm the lanes on this stream
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=s):
+        wl.step_concurrent()
+    torch.cuda.synchronize()
+    return g
+
+
+def time_steps_graph(wl: Workload, g, K: int):
+    torch = wl.torch
+    s = torch.cuda.current_stream()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(s)
+    for _ in range(K):
+        g.replay()
+    end.record(s)
+    end.synchronize()
+    return start.elapsed_time(end)
+
+
 def time_steps(wl: Workload, K: int):
     """K serial steps between CUDA events on the launching stream; per-launch events too."""
     torch = wl.torch
@@ -609,7 +640,17 @@ def main():
     shard.barrier()
     torch.cuda.synchronize()
     # the reported number: K steps with the runtime's two-lane schedule
-    total_ms = time_steps_concurrent(wl, args.steps) if not args.serial else serial_ms
+    graph = None
+    if args.graph and not args.serial:
+        graph = capture_step_graph(wl)
+        for _ in range(3):
+            graph.replay()
+        torch.cuda.synchronize()
+        shard.barrier()
+        torch.cuda.synchronize()
+        total_ms = time_steps_graph(wl, graph, args.steps)
+    else:
+        total_ms = time_steps_concurrent(wl, args.steps) if not args.serial else serial_ms
     torch.cuda.synchronize()
     shard.barrier()
     clocks = sampler.stop()
@@ -685,7 +726,8 @@ def main():
                    "mulmods_per_step_per_rank": wl.mulmods, **wl.config},
         "gpu_launches": len(wl.launches) * args.steps,
         "schedule": ("serial, one stream" if args.serial else
-                     "two lanes: HBM-bound launches on one stream, the IMAD-bound pow on another"),
+                     "two lanes: HBM-bound launches on one stream, the IMAD-bound pow on another" +
+                     (", replayed as one CUDA graph" if args.graph else "")),
         "ms_per_step_serial": round(serial_ms / args.steps, 5),
         "roofline": roof,
         "kernels": rooflines,
