@@ -70,7 +70,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--soak", type=float, default=1.0, help="seconds of untimed steps before timing (clocks)")
     ap.add_argument("--serial", action="store_true", help="report the serial (one-stream) step instead")
-    ap.add_argument("--graph", action="store_true", help="replay the two-lane step as one CUDA graph")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="issue the two-lane step launch by launch instead of replaying it as one CUDA graph")
     ap.add_argument("--pow-ctas", type=int, default=5, help="CTAs per SM of the persistent pow grid (0 = flat)")
     return ap.parse_args()
 
