@@ -1,10 +1,11 @@
 #!/bin/bash
 # On-GPU measurement pass (run under gpurun):
-#   1. plain bench (the number), 2. same command under ncu: per-launch durations,
-#   3. ncu --set full captures of the top kernels (each after its own plain run).
+#   1. the default bench line (the number), 2. the bench command under ncu: per-launch
+#   durations, 3. ncu --set full captures of the top kernels (each after its own plain run).
 set -u
 OUT=${OUT:-gpurun_out}
 mkdir -p $OUT
+timeout 900 python bench.py > $OUT/bench_final.log 2>&1; echo "bench rc=$?"
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --soak 0"
 $CMD > $OUT/plain_small.log 2>&1 || { echo "plain small bench failed"; tail -20 $OUT/plain_small.log; exit 1; }
 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
@@ -13,3 +14,6 @@ for K in k_map2 k_pow k_twiddle k_map1; do
   ncu --set full --clock-control none --import-source on -k regex:"^${K}" -s 3 -c 1 -o $OUT/prof_${K} $CMD > $OUT/ncu_${K}.log 2>&1
   echo "ncu full ${K} rc=$?"
 done
+CMD2="python bench.py --workload ntt --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --soak 0"
+$CMD2 > $OUT/plain_ntt.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"^k_ntt_r32" -s 3 -c 1 -o $OUT/prof_k_ntt_r32 $CMD2 > $OUT/ncu_k_ntt.log 2>&1
+echo "ncu full k_ntt rc=$?"
