@@ -215,9 +215,10 @@ class Workload:
             self.outputs.append(o)
             # in the two-lane schedule pow runs as a persistent grid of POW_CTAS CTAs per SM so it
             # co-resides with the HBM-bound kernels instead of filling every SM first
-            pcfg = m.Launch(ctas_per_sm=POW_CTAS) if POW_CTAS > 0 else None
-            L.append(("mont_pow_vec", lambda base=base, e=e, o=o, pcfg=pcfg:
-                      m.pow_vec(self.ctx[P1], base, e, out=o, cfg=pcfg), 12 * N_C4, ladder, "imad"))
+            self.pow_cfg_lane = m.Launch(ctas_per_sm=POW_CTAS) if POW_CTAS > 0 else None
+            self.pow_cfg = None   # flat grid (best standalone) unless a lane schedule is running
+            L.append(("mont_pow_vec", lambda base=base, e=e, o=o:
+                      m.pow_vec(self.ctx[P1], base, e, out=o, cfg=self.pow_cfg), 12 * N_C4, ladder, "imad"))
             self.config.update({"c4_n": N_C4, "c4_ladder_mulmods": ladder})
         if kind == "ntt":
             # forward NTT of the configs[2] batch (4096 rows of 2^14) over P0
@@ -266,6 +267,7 @@ class Workload:
         launches are independent (disjoint outputs), so results are identical."""
         torch = self.torch
         cur = torch.cuda.current_stream()
+        self.pow_cfg = getattr(self, "pow_cfg_lane", None)
         if not hasattr(self, "_lanes"):
             self._lanes = {"hbm": torch.cuda.Stream(), "imad": torch.cuda.Stream()}
         ev = torch.cuda.Event()
@@ -280,6 +282,7 @@ class Workload:
                         fn()
         for st in self._lanes.values():
             cur.wait_stream(st)
+        self.pow_cfg = None
 
     def h2d_bytes(self):
         return sum(t.numel() * 4 for t in self.inputs)
