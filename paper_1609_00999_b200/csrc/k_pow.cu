@@ -224,6 +224,38 @@ __global__ void __launch_bounds__(256) k_pow(PowParams q, uint32_t *out, const u
     }
 }
 
+// 8 lanes per thread (two uint4): twice the independent chains per thread, so a
+// smaller grid saturates the IMAD pipe and leaves thread slots to co-running
+// HBM-bound kernels (variant 10)
+__global__ void __launch_bounds__(256) k_pow8(PowParams q, uint32_t *out, const uint32_t *base, const uint32_t *exp,
+                                               uint32_t head, size_t n4, uint32_t tail) {
+    if (blockIdx.x == 0 && threadIdx.x < head + tail) {
+        size_t i = threadIdx.x < head ? threadIdx.x : head + 4 * n4 + (threadIdx.x - head);
+        uint32_t b[1] = {base[i]}, e[1] = {exp[i]}, o[1];
+        pow_window<2, 1, false>(q, b, e, o, nullptr);
+        out[i] = o[0];
+    }
+    const uint4 *b4 = reinterpret_cast<const uint4 *>(base + head);
+    const uint4 *e4 = reinterpret_cast<const uint4 *>(exp + head);
+    uint4 *o4 = reinterpret_cast<uint4 *>(out + head);
+    const size_t n8 = n4 / 2;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (size_t)gridDim.x * blockDim.x) {
+        const uint4 b0 = ld_stream(b4 + 2 * i), b1 = ld_stream(b4 + 2 * i + 1);
+        const uint4 e0 = ld_stream(e4 + 2 * i), e1 = ld_stream(e4 + 2 * i + 1);
+        uint32_t b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+        uint32_t e[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w}, o[8];
+        pow_window<2, 8, false>(q, b, e, o, nullptr);
+        st_stream(o4 + 2 * i, make_uint4(o[0], o[1], o[2], o[3]));
+        st_stream(o4 + 2 * i + 1, make_uint4(o[4], o[5], o[6], o[7]));
+    }
+    if ((n4 & 1) && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {  // odd last uint4
+        const uint4 bv = ld_stream(b4 + n4 - 1), ev = ld_stream(e4 + n4 - 1);
+        uint32_t b[4] = {bv.x, bv.y, bv.z, bv.w}, e[4] = {ev.x, ev.y, ev.z, ev.w}, o[4];
+        pow_window<2, 4, false>(q, b, e, o, nullptr);
+        st_stream(o4 + n4 - 1, make_uint4(o[0], o[1], o[2], o[3]));
+    }
+}
+
 template <int V>
 __global__ void __launch_bounds__(256) k_pow_scalar(PowParams q, uint32_t *out, const uint32_t *base,
                                                      const uint32_t *exp, size_t n) {
@@ -386,10 +418,23 @@ extern "C" mont_status_t mont_pow_vec_ex(const mont_ctx_t *ctx, uint32_t *out, c
     if (n == 0) return MONT_OK;
     if (!out || !base || !exp || ((uintptr_t)out | (uintptr_t)base | (uintptr_t)exp) & 3u) return MONT_EINVAL_ARG;
     Launch L = resolve(cfg, kPowDefault);
-    if (L.threads != 256 || L.variant < 0 || L.variant > 9 || L.ctas_per_sm < 0) return MONT_EINVAL_ARG;
+    if (L.threads != 256 || L.variant < 0 || L.variant > 10 || L.ctas_per_sm < 0) return MONT_EINVAL_ARG;
     const int sms = sm_count();
     if (sms <= 0) return MONT_ECUDA;
     const PowParams q{(int32_t)ctx->p, (int32_t)(0u - ctx->pneg), ctx->r1, ctx->r2, (double)ctx->p, 1.0 / (double)ctx->p};
+    if (L.variant == 10 && same_mod16((uintptr_t)base, (uintptr_t)exp) && same_mod16((uintptr_t)base, (uintptr_t)out)) {
+        const uint32_t head = head_elems((uintptr_t)base, n);
+        const size_t n4 = (n - head) / 4;
+        const uint32_t tail = (uint32_t)((n - head) % 4);
+        const size_t need = (n4 / 2 + 255) / 256;
+        size_t grid = L.ctas_per_sm > 0 ? (size_t)sms * L.ctas_per_sm : need;
+        if (grid > need) grid = need;
+        if (grid == 0) grid = 1;
+        if (grid > 0x7fffffff) grid = 0x7fffffff;
+        k_pow8<<<(unsigned)grid, 256, 0, stream>>>(q, out, base, exp, head, n4, tail);
+        return launch_status();
+    }
+    if (L.variant == 10) L.variant = 0;  // misaligned operands: the 4-lane kernel handles them
     if (L.variant == 9) {  // Fourier-prime REDC ladder: P = c 2^n + 1, 2n >= 32, 3P < 2^32
         uint32_t nn = 0, cc = ctx->p - 1u;
         while ((cc & 1u) == 0u) { cc >>= 1; ++nn; }
