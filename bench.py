@@ -55,6 +55,7 @@ SEED = 42
 METRIC = json.loads((ROOT / "BASELINE.json").read_text())["metric"]
 G11_GENERATOR = 31
 POW_CTAS = 0   # set from --pow-ctas
+POW_VARIANT = 0  # set from --pow-variant
 LANE_ORDER = tuple(os.environ.get("MONT_LANE_ORDER", "imad,hbm").split(","))
 
 
@@ -73,6 +74,7 @@ def parse():
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="issue the two-lane step launch by launch instead of replaying it as one CUDA graph")
     ap.add_argument("--pow-ctas", type=int, default=5, help="CTAs per SM of the persistent pow grid (0 = flat)")
+    ap.add_argument("--pow-variant", type=int, default=0, help="mont_pow_vec_ex variant used in the lane schedule")
     return ap.parse_args()
 
 
@@ -215,7 +217,7 @@ class Workload:
             self.outputs.append(o)
             # in the two-lane schedule pow runs as a persistent grid of POW_CTAS CTAs per SM so it
             # co-resides with the HBM-bound kernels instead of filling every SM first
-            self.pow_cfg_lane = m.Launch(ctas_per_sm=POW_CTAS) if POW_CTAS > 0 else None
+            self.pow_cfg_lane = m.Launch(ctas_per_sm=POW_CTAS, variant=POW_VARIANT) if POW_CTAS > 0 else None
             self.pow_cfg = None   # flat grid (best standalone) unless a lane schedule is running
             L.append(("mont_pow_vec", lambda base=base, e=e, o=o:
                       m.pow_vec(self.ctx[P1], base, e, out=o, cfg=self.pow_cfg), 12 * N_C4, ladder, "imad"))
@@ -595,8 +597,9 @@ def ncu_traffic(name: str):
 
 def main():
     args = parse()
-    global POW_CTAS
+    global POW_CTAS, POW_VARIANT
     POW_CTAS = 0 if args.serial else args.pow_ctas
+    POW_VARIANT = args.pow_variant
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

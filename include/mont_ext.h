@@ -37,7 +37,9 @@ extern "C" {
  *                                   Fourier-prime REDC products (PAPER.md
  *                                   Alg. 3; P = c 2^n + 1, 2n >= 32,
  *                                   3P < 2^32, 16-byte aligned operands,
- *                                   else MONT_EUNSUPPORTED / EINVAL_ARG).
+ *                                   else MONT_EUNSUPPORTED / EINVAL_ARG);
+ *                                   10 = variant 0 with 8 lanes (two uint4)
+ *                                   per thread.
  *                                   ctas_per_sm = 0 selects a flat grid.
  *                 mont_mul_twiddle_ex : 0 = bulk-copy (TMA) staged table,
  *                                   1 = table read through L1/L2 (no smem)

@@ -179,7 +179,7 @@ def test_to_mont_alignment_in_place(m, off_in, off_out):
 # --------------------------------------------------------------------- pow
 
 @pytest.mark.parametrize("P", PRIMES + (17, 257, 2147483647, 3))
-@pytest.mark.parametrize("variant", list(range(9)))
+@pytest.mark.parametrize("variant", list(range(9)) + [10])
 def test_pow_parity(m, P, variant):
     n = 20_003
     base = synth.uniform(42, synth.STREAM_BASE, P, 0, n, low=1) if P > 3 else \
@@ -206,8 +206,8 @@ def test_pow_full_32bit_exponents_and_big_bases(m):
         assert np.array_equal(host(out), ref), variant
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6, 7, 1000, 1 << 16 | 3])
-@pytest.mark.parametrize("variant", [0, 5, 6])
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6, 7, 8, 9, 12, 1000, 1 << 16 | 3, (1 << 16) + 4])
+@pytest.mark.parametrize("variant", [0, 5, 6, 10])
 def test_pow_ragged_and_misaligned(m, n, variant):
     P = 469762049
     base, exp = synth.c4_inputs(P, 5, n)
@@ -415,3 +415,12 @@ def test_pow_fourier_unsupported(m):
         with pytest.raises(m.MontError) as ei:
             m.pow_vec(m.ctx_init(P), dev(np.ones(8, np.uint32)), dev(np.ones(8, np.uint32)), cfg=m.Launch(variant=9))
         assert ei.value.status == 4
+
+
+@pytest.mark.parametrize("ctas", [0, 1, 3, 5])
+@pytest.mark.parametrize("n", [4, 8, 12, 4100, 1 << 20])
+def test_pow_variant10_grids(m, ctas, n):
+    P = 469762049
+    base, e = synth.c4_inputs(P, 0, n)
+    out = m.pow_vec(m.ctx_init(P), dev(base), dev(e), cfg=m.Launch(variant=10, ctas_per_sm=ctas))
+    assert np.array_equal(host(out), oracle.power(P, base, e))
