@@ -73,8 +73,8 @@ def parse():
     ap.add_argument("--serial", action="store_true", help="report the serial (one-stream) step instead")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="issue the two-lane step launch by launch instead of replaying it as one CUDA graph")
-    ap.add_argument("--pow-ctas", type=int, default=5, help="CTAs per SM of the persistent pow grid (0 = flat)")
-    ap.add_argument("--pow-variant", type=int, default=0, help="mont_pow_vec_ex variant used in the lane schedule")
+    ap.add_argument("--pow-ctas", type=int, default=2, help="CTAs per SM of the persistent pow grid (0 = flat)")
+    ap.add_argument("--pow-variant", type=int, default=10, help="mont_pow_vec_ex variant used in the lane schedule")
     return ap.parse_args()
 
 
