@@ -33,7 +33,11 @@ __device__ __forceinline__ void op(uint32_t &x, uint64_t &w, uint32_t c, int32_t
     } else if (KIND == 9) {
         asm volatile("add.u32 %0, %0, %1;" : "+r"(x) : "r"(c));           // IADD (ALU)
     } else if (KIND == 10) {
-        asm volatile("xor.b32 %0, %0, %1;" : "+r"(x) : "r"(c));           // LOP3 (ALU)
+        asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x) : "r"(c), "r"((uint32_t)p));  // LOP3 (ALU)
+    } else if (KIND == 13) {
+        asm volatile("min.u32 %0, %0, %1;" : "+r"(x) : "r"(c));             // VIMNMX (ALU)
+    } else if (KIND == 14) {
+        asm volatile("shf.l.wrap.b32 %0, %0, %0, %1;" : "+r"(x) : "r"(c));  // SHF (ALU)
     }
 }
 
@@ -77,7 +81,7 @@ using namespace mont;
 
 extern "C" mont_status_t mb_imad(uint32_t *sink, int kind, int iters, const mont_launch_t *cfg, cudaStream_t stream,
                                  unsigned long long *threads_launched) {
-    if (!sink || kind < 0 || kind > 12 || iters < 1) return MONT_EINVAL_ARG;
+    if (!sink || kind < 0 || kind > 14 || iters < 1) return MONT_EINVAL_ARG;
     const int sms = sm_count();
     if (sms <= 0) return MONT_ECUDA;
     const int ctas = (cfg && cfg->ctas_per_sm > 0) ? cfg->ctas_per_sm : 8;
@@ -99,7 +103,9 @@ extern "C" mont_status_t mb_imad(uint32_t *sink, int kind, int iters, const mont
         case 9: k_imad<9><<<grid, 256, 0, stream>>>(sink, iters, c, (int32_t)p, (int32_t)pinv); break;
         case 10: k_imad<10><<<grid, 256, 0, stream>>>(sink, iters, c, (int32_t)p, (int32_t)pinv); break;
         case 11: k_imad<11><<<grid, 256, 0, stream>>>(sink, iters, c, (int32_t)p, (int32_t)pinv); break;
-        default: k_imad<12><<<grid, 256, 0, stream>>>(sink, iters, c, (int32_t)p, (int32_t)pinv); break;
+        case 12: k_imad<12><<<grid, 256, 0, stream>>>(sink, iters, c, (int32_t)p, (int32_t)pinv); break;
+        case 13: k_imad<13><<<grid, 256, 0, stream>>>(sink, iters, c, (int32_t)p, (int32_t)pinv); break;
+        default: k_imad<14><<<grid, 256, 0, stream>>>(sink, iters, c, (int32_t)p, (int32_t)pinv); break;
     }
     if (threads_launched) *threads_launched = (unsigned long long)grid * 256ull;
     return launch_status();
