@@ -49,8 +49,9 @@ if args.what in ("all", "imad"):
     import ctypes as C
     sink = torch.empty(sms * 32 * 256, dtype=torch.uint32, device=dev)
     names = {0: "IMAD", 1: "IMAD.HI", 2: "IMAD.WIDE(hoisted)", 3: "sredc", 4: "redc", 5: "sredc_mulhi",
-             6: "sredc_hiadd", 7: "DFMA", 8: "fmulmod", 9: "IADD", 10: "LOP3", 11: "mix3:1", 12: "mix1:1"}
-    for kind in range(13):
+             6: "sredc_hiadd", 7: "DFMA", 8: "fmulmod", 9: "IADD", 10: "LOP3", 11: "mix3:1", 12: "mix1:1",
+             13: "VIMNMX(fused 3-in)", 14: "SHF"}
+    for kind in range(15):
         for ctas in (4, 8):
             iters = 2000
             nthr = C.c_ulonglong(0)
