@@ -41,6 +41,24 @@ mont_status_t mont_ntt(const mont_ctx_t *ctx, uint32_t *data, size_t batch, int 
  * square-and-multiply on the GPU.  1 <= log_n <= 30. */
 mont_status_t mont_ntt_twiddles(const mont_ctx_t *ctx, uint32_t *tw, uint32_t w, int log_n, cudaStream_t stream);
 
+/* ---- large transforms, 2^16 <= N <= 2^30 (six-step) ----
+ * N = N1 N2 with N1 = 2^floor(log_n/2), N2 = 2^ceil(log_n/2) (both <= 2^15):
+ * transpose, N2 transforms of length N1 with the twiddle w^(n2 k1) applied in
+ * their epilogue (the configs[2] "twiddle multiply of one NTT stage", here 2-D
+ * and generated from two half tables), transpose, N1 transforms of length N2,
+ * transpose to natural order.  HBM traffic 5 x 8 bytes per element.
+ *
+ * plan: device buffer of mont_ntt_plan_words(log_n) words, filled by
+ *       mont_ntt_plan_init for a primitive N-th root w (w^-1: inverse).
+ * in  : the N inputs (canonical); DESTROYED (used as scratch).
+ * out : the N outputs, natural order; must not overlap `in`.
+ * scale as in mont_ntt. */
+size_t mont_ntt_plan_words(int log_n);   /* 0 if log_n is outside [16, 30] */
+mont_status_t mont_ntt_plan_init(const mont_ctx_t *ctx, uint32_t *plan, uint32_t w, int log_n,
+                                 cudaStream_t stream);
+mont_status_t mont_ntt_large(const mont_ctx_t *ctx, uint32_t *out, uint32_t *in, int log_n,
+                             const uint32_t *plan, uint32_t scale, cudaStream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

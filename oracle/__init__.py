@@ -85,6 +85,8 @@ def lib():
         L.oracle_dft.argtypes = [C.c_uint32, C.c_uint32, _U32P, _U32P, C.c_size_t]
         L.oracle_cyclic_conv.argtypes = [C.c_uint32, _U32P, _U32P, _U32P, C.c_size_t]
         L.oracle_dot.argtypes = [C.POINTER(Ctx), _U32P, _U32P, _U32P, C.c_size_t, C.c_size_t]
+        L.oracle_dft_at.argtypes = [C.c_uint32, C.c_uint32, _U32P, C.c_size_t, C.c_size_t]
+        L.oracle_dft_at.restype = C.c_uint32
         L.oracle_inverse.argtypes = [C.c_uint32, C.c_uint32]
         L.oracle_inverse.restype = C.c_uint32
         L.oracle_mod_add.argtypes = [C.c_uint32] * 3
@@ -269,3 +271,9 @@ def dot(P: int, A, x) -> np.ndarray:
     c = ctx(P)
     lib().oracle_dot(C.byref(c), out, A.reshape(-1), x, batch, length)
     return out
+
+
+def dft_at(P: int, w: int, x, k: int) -> int:
+    """X[k] = sum_j x[j] w^(jk) mod P, one output by definition (O(N))."""
+    x = _u32(x).reshape(-1)
+    return int(lib().oracle_dft_at(P, w, x, x.size, k))

@@ -399,3 +399,23 @@ void oracle_dot(const oracle_ctx_t *c, uint32_t *out, const uint32_t *A, const u
         out[r] = mulmod_naive((uint32_t)s, c->Rinv, c->P);
     }
 }
+
+/* One output of the DFT by definition, X[k] = sum_j x[j] w^(j k) mod P, O(N):
+ * for sampled checks of transforms too large for oracle_dft. */
+uint32_t oracle_dft_at(uint32_t P, uint32_t w, const uint32_t *x, size_t N, size_t k)
+{
+    /* wk = w^k by repeated squaring on plain values */
+    uint32_t wk = 1u % P, b = w % P;
+    for (size_t e = k % N; e; e >>= 1) {
+        if (e & 1u) wk = mulmod_naive(wk, b, P);
+        b = mulmod_naive(b, b, P);
+    }
+    uint64_t s = 0;
+    uint32_t pw = 1u % P;
+    for (size_t j = 0; j < N; ++j) {
+        s += mulmod_naive(x[j] % P, pw, P);
+        s %= P;
+        pw = mulmod_naive(pw, wk, P);
+    }
+    return (uint32_t)s;
+}

@@ -88,6 +88,9 @@ SIGNATURES = {
 SIGNATURES["mont_ntt"] = (C.c_int, [_CTX, _P, _S, C.c_int, _P, C.c_uint32, _P])
 SIGNATURES["mont_ntt_twiddles"] = (C.c_int, [_CTX, _P, C.c_uint32, C.c_int, _P])
 SIGNATURES["mont_dot"] = (C.c_int, [_CTX, _P, _P, _P, _S, _S, _P])
+SIGNATURES["mont_ntt_plan_words"] = (C.c_size_t, [C.c_int])
+SIGNATURES["mont_ntt_plan_init"] = (C.c_int, [_CTX, _P, C.c_uint32, C.c_int, _P])
+SIGNATURES["mont_ntt_large"] = (C.c_int, [_CTX, _P, _P, C.c_int, _P, C.c_uint32, _P])
 
 
 class BarrettCtx(C.Structure):
@@ -393,6 +396,30 @@ def ntt(ctx: Ctx, data, tw, scale: int | None = None, stream=None):
     _check(lib().mont_ntt(C.byref(ctx), _ptr(data), batch, log_n, _ptr(tw), ctx.r1 if scale is None else scale,
                           _stream_handle(stream)), "mont_ntt")
     return data
+
+
+def ntt_plan(ctx: Ctx, w: int, log_n: int, device="cuda", stream=None):
+    """Device plan (tables) for mont_ntt_large of size 2^log_n, 16 <= log_n <= 30."""
+    torch = _torch()
+    words = int(lib().mont_ntt_plan_words(log_n))
+    if words == 0:
+        raise ValueError("log_n must be in [16, 30]")
+    plan = torch.empty(words, dtype=torch.uint32, device=device)
+    _check(lib().mont_ntt_plan_init(C.byref(ctx), _ptr(plan), w, log_n, _stream_handle(stream)), "mont_ntt_plan_init")
+    return plan
+
+
+def ntt_large(ctx: Ctx, x, plan, out=None, scale: int | None = None, stream=None):
+    """Natural-order NTT of one vector of 2^k (16 <= k <= 30) words; x is destroyed (scratch)."""
+    _dev_u32(x, "x"), _dev_u32(plan, "plan")
+    n = x.numel()
+    log_n = n.bit_length() - 1
+    if n != 1 << log_n:
+        raise ValueError("length must be a power of two")
+    out = _out_like(out, x)
+    _check(lib().mont_ntt_large(C.byref(ctx), _ptr(out), _ptr(x), log_n, _ptr(plan),
+                                ctx.r1 if scale is None else scale, _stream_handle(stream)), "mont_ntt_large")
+    return out
 
 
 def dot(ctx: Ctx, A, x, out=None, stream=None):

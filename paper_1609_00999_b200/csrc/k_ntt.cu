@@ -68,6 +68,16 @@ __global__ void __launch_bounds__(1024) k_ntt_smem(Ctx c, uint32_t *data, int lo
 // (checked exhaustively for log_n = 10..15 offline; scripts/ntt_swizzle.py).
 __device__ __forceinline__ uint32_t swz(uint32_t a) { return a ^ (((a >> 5) ^ (a >> 10)) & 31u); }
 
+// optional 2-D twiddle epilogue of the six-step large transform: element
+// (row, idx) is multiplied by w^(row * idx mod N) = lo[e mod 2^shift] * hi[e >> shift]
+struct Tw2D {
+    const uint32_t *lo, *hi;
+    uint64_t mask;      // N - 1 of the large transform
+    uint32_t lomask;    // 2^shift - 1
+    int shift;
+    size_t row0;        // global index of row 0 of this launch
+};
+
 // LOG_N is a template parameter so every shift, window position and twiddle
 // stride is a compile-time constant.  Because the swizzle is linear over
 // GF(2) and the per-thread bits and the per-k bits of an index are disjoint,
@@ -75,7 +85,7 @@ __device__ __forceinline__ uint32_t swz(uint32_t a) { return a ^ (((a >> 5) ^ (a
 // access, and twiddle addresses become (per-thread base) + (constant offset).
 template <int LOG_N>
 __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
-    k_ntt_r32(Ctx c, uint32_t *data, size_t batch, const uint32_t *__restrict__ tw, uint32_t scale) {
+    k_ntt_r32(Ctx c, uint32_t *data, size_t batch, const uint32_t *__restrict__ tw, uint32_t scale, Tw2D t2) {
     constexpr uint32_t N = 1u << LOG_N, T = N >> 5;
     extern __shared__ uint32_t sm[];
     const uint32_t rl = threadIdx.x / T, t = threadIdx.x % T;
@@ -125,18 +135,25 @@ __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
     }
     if (live) {
         const uint32_t st0 = swz(t);
+        const uint64_t rowg = (uint64_t)(row + t2.row0);
 #pragma unroll
         for (int k = 0; k < 32; ++k) {
+            const uint32_t idx = t + (uint32_t)k * T;
             uint32_t x = s[st0 ^ swz((uint32_t)k * T)];
+            if (t2.lo) {  // six-step twiddle w^(row * idx), from two half tables
+                const uint64_t e = (rowg * idx) & t2.mask;
+                const uint32_t we = redc(__ldg(t2.hi + (e >> t2.shift)), __ldg(t2.lo + (e & t2.lomask)), c.p, c.pinv);
+                x = redc(x, we, c.p, c.pinv);
+            }
             if (scale != c.r1) x = redc(x, scale, c.p, c.pinv);
-            st_stream1(g + t + (uint32_t)k * T, x);
+            st_stream1(g + idx, x);
         }
     }
 }
 
 template <int LOG_N>
 static mont_status_t launch_ntt_r32(const Ctx &c, uint32_t *data, size_t batch, const uint32_t *tw, uint32_t scale,
-                                    cudaStream_t stream) {
+                                    cudaStream_t stream, Tw2D t2 = Tw2D{nullptr, nullptr, 0, 0, 0, 0}) {
     constexpr uint32_t N = 1u << LOG_N, T = N >> 5;
     constexpr uint32_t rpc = T >= 256 ? 1u : 256u / T;  // rows per CTA
     const size_t smem = (size_t)rpc * N * 4;
@@ -145,7 +162,7 @@ static mont_status_t launch_ntt_r32(const Ctx &c, uint32_t *data, size_t batch, 
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(k_ntt_r32<LOG_N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return MONT_ECUDA;
-    k_ntt_r32<LOG_N><<<(unsigned)grid, rpc * T, smem, stream>>>(c, data, batch, tw, scale);
+    k_ntt_r32<LOG_N><<<(unsigned)grid, rpc * T, smem, stream>>>(c, data, batch, tw, scale, t2);
     return launch_status();
 }
 
@@ -166,9 +183,121 @@ __global__ void __launch_bounds__(256) k_ntt_twiddles(Ctx c, uint32_t *tw, uint3
     }
 }
 
+// tiled transpose of an R x C row-major uint32 matrix (32 x 32 tiles through
+// padded shared memory; coalesced 128-byte rows on both sides)
+__global__ void __launch_bounds__(256) k_transpose(uint32_t *dst, const uint32_t *src, size_t R, size_t C) {
+    __shared__ uint32_t tile[32][33];
+    const size_t c0 = (size_t)blockIdx.x * 32, r0 = (size_t)blockIdx.y * 32;
+    const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+#pragma unroll
+    for (int k = 0; k < 32; k += 8) {
+        const size_t r = r0 + ty + k, cc = c0 + tx;
+        if (r < R && cc < C) tile[ty + k][tx] = ld_stream1(src + r * C + cc);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 32; k += 8) {
+        const size_t cc = c0 + ty + k, r = r0 + tx;  // dst is C x R
+        if (r < R && cc < C) st_stream1(dst + cc * R + r, tile[tx][ty + k]);
+    }
+}
+
+static mont_status_t transpose(uint32_t *dst, const uint32_t *src, size_t R, size_t C, cudaStream_t s) {
+    const size_t gx = (C + 31) / 32, gy = (R + 31) / 32;
+    if (gx > 0x7fffffffu || gy > 65535) return MONT_EUNSUPPORTED;
+    k_transpose<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, s>>>(dst, src, R, C);
+    return launch_status();
+}
+
+static mont_status_t ntt_rows(const Ctx &c, uint32_t *data, size_t batch, int log_n, const uint32_t *tw,
+                              uint32_t scale, cudaStream_t s, Tw2D t2) {
+    switch (log_n) {
+        case 5: return launch_ntt_r32<5>(c, data, batch, tw, scale, s, t2);
+        case 6: return launch_ntt_r32<6>(c, data, batch, tw, scale, s, t2);
+        case 7: return launch_ntt_r32<7>(c, data, batch, tw, scale, s, t2);
+        case 8: return launch_ntt_r32<8>(c, data, batch, tw, scale, s, t2);
+        case 9: return launch_ntt_r32<9>(c, data, batch, tw, scale, s, t2);
+        case 10: return launch_ntt_r32<10>(c, data, batch, tw, scale, s, t2);
+        case 11: return launch_ntt_r32<11>(c, data, batch, tw, scale, s, t2);
+        case 12: return launch_ntt_r32<12>(c, data, batch, tw, scale, s, t2);
+        case 13: return launch_ntt_r32<13>(c, data, batch, tw, scale, s, t2);
+        case 14: return launch_ntt_r32<14>(c, data, batch, tw, scale, s, t2);
+        case 15: return launch_ntt_r32<15>(c, data, batch, tw, scale, s, t2);
+        default: return MONT_EUNSUPPORTED;
+    }
+}
+
+// split of a large transform: N = N1 * N2, log N1 = a <= log N2 = b <= 15
+static void ntt_split(int log_n, int &a, int &b, int &sh) {
+    a = log_n / 2;
+    b = log_n - a;
+    sh = (log_n + 1) / 2;  // two-level table split of the exponent
+}
+
+static uint32_t host_powmod(uint32_t x, uint64_t e, uint32_t p) {
+    uint64_t r = 1 % p, b = x % p;
+    while (e) {
+        if (e & 1) r = r * b % p;
+        b = b * b % p;
+        e >>= 1;
+    }
+    return (uint32_t)r;
+}
+
 }  // namespace mont
 
 using namespace mont;
+
+extern "C" size_t mont_ntt_plan_words(int log_n) {
+    if (log_n < 16 || log_n > 30) return 0;
+    int a, b, sh;
+    ntt_split(log_n, a, b, sh);
+    return ((size_t)1 << a) - 1 + ((size_t)1 << b) - 1 + ((size_t)1 << sh) + ((size_t)1 << (log_n - sh));
+}
+
+extern "C" mont_status_t mont_ntt_plan_init(const mont_ctx_t *ctx, uint32_t *plan, uint32_t w, int log_n,
+                                            cudaStream_t stream) {
+    if (!ctx_ok(ctx)) return ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
+    if (log_n < 16 || log_n > 30) return MONT_EUNSUPPORTED;
+    if (!plan || ((uintptr_t)plan & 3u)) return MONT_EINVAL_ARG;
+    int a, b, sh;
+    ntt_split(log_n, a, b, sh);
+    const uint32_t p = ctx->p;
+    uint32_t *tw1 = plan, *tw2 = tw1 + ((1u << a) - 1), *tlo = tw2 + ((1u << b) - 1), *thi = tlo + (1u << sh);
+    mont_status_t st;
+    // column transforms have length N1 = 2^a: root w^(N2); row transforms N2 = 2^b: root w^(N1)
+    if ((st = mont_ntt_twiddles(ctx, tw1, host_powmod(w, 1ull << b, p), a, stream)) != MONT_OK) return st;
+    if ((st = mont_ntt_twiddles(ctx, tw2, host_powmod(w, 1ull << a, p), b, stream)) != MONT_OK) return st;
+    if ((st = mont_twiddle_table(ctx, tlo, w, (size_t)1 << sh, stream)) != MONT_OK) return st;
+    return mont_twiddle_table(ctx, thi, host_powmod(w, 1ull << sh, p), (size_t)1 << (log_n - sh), stream);
+}
+
+extern "C" mont_status_t mont_ntt_large(const mont_ctx_t *ctx, uint32_t *out, uint32_t *in, int log_n,
+                                        const uint32_t *plan, uint32_t scale, cudaStream_t stream) {
+    if (!ctx_ok(ctx)) return ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
+    if (log_n < 16 || log_n > 30) return MONT_EUNSUPPORTED;
+    if (!out || !in || !plan || out == in || (((uintptr_t)out | (uintptr_t)in | (uintptr_t)plan) & 3u) ||
+        scale >= ctx->p)
+        return MONT_EINVAL_ARG;
+    int a, b, sh;
+    ntt_split(log_n, a, b, sh);
+    const size_t N1 = (size_t)1 << a, N2 = (size_t)1 << b;
+    const uint32_t *tw1 = plan, *tw2 = tw1 + (N1 - 1), *tlo = tw2 + (N2 - 1), *thi = tlo + ((size_t)1 << sh);
+    const Ctx c = to_dev(ctx);
+    const Tw2D none{nullptr, nullptr, 0, 0, 0, 0};
+    const Tw2D t2{tlo, thi, ((uint64_t)1 << log_n) - 1, (1u << sh) - 1u, sh, 0};
+    mont_status_t st;
+    // x as N1 x N2 [n1][n2] -> out as N2 x N1 [n2][n1]
+    if ((st = transpose(out, in, N1, N2, stream)) != MONT_OK) return st;
+    // N2 column transforms of length N1, then the twiddle w^(n2 k1)
+    if ((st = ntt_rows(c, out, N2, a, tw1, c.r1, stream, t2)) != MONT_OK) return st;
+    // back to N1 x N2 [k1][n2]
+    if ((st = transpose(in, out, N2, N1, stream)) != MONT_OK) return st;
+    // N1 row transforms of length N2 -> [k1][k2], with the output scale
+    if ((st = ntt_rows(c, in, N1, b, tw2, scale, stream, none)) != MONT_OK) return st;
+    // X[k1 + N1 k2] = [k1][k2]: transpose to N2 x N1 -> natural order in out
+    return transpose(out, in, N1, N2, stream);
+}
 
 extern "C" mont_status_t mont_ntt_twiddles(const mont_ctx_t *ctx, uint32_t *tw, uint32_t w, int log_n,
                                            cudaStream_t stream) {

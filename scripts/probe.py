@@ -303,3 +303,17 @@ if args.what in ("hostrun",):
     out(what="raw 1.5GB h2d || 0.75GB d2h", ms=med * 1e3, h2d_gbs=24 * n / med / 1e9)
     med, _ = timeit(lambda: dbig.copy_(hbig, non_blocking=True), reps=3, warm=1)
     out(what="raw 1.5GB h2d alone", ms=med * 1e3, gbs=24 * n / med / 1e9)
+
+if args.what in ("nttlarge",):
+    P = 2013265921
+    ctx = m.ctx_init(P)
+    for log_n in (20, 22, 24, 26):
+        N = 1 << log_n
+        w = pow(31, (P - 1) // N, P)
+        plan = m.ntt_plan(ctx, w, log_n)
+        x = torch.empty(N, dtype=torch.uint32, device=dev)
+        m.synth_fill(x, 42, 5, 0, P)
+        o = torch.empty_like(x)
+        med, _ = timeit(lambda: m.ntt_large(ctx, x, plan, out=o), reps=10)
+        out(what="ntt_large", log_n=log_n, us=med * 1e6, gbs_5pass=40 * N / med / 1e9,
+            tbutterfly=(N // 2) * log_n / med / 1e12)

@@ -113,3 +113,42 @@ def test_ntt_twiddle_table_layout(m, log_n):
         pos = e + 1 - (1 << s1)
         expo = pos * (N >> (s1 + 1))
         assert int(tw[e]) == (pow(w, expo, P) << 32) % P
+
+
+@pytest.mark.parametrize("P", list(GEN))
+@pytest.mark.parametrize("log_n", [16, 17, 20, 23])
+def test_ntt_large(m, P, log_n):
+    """Six-step transform: sampled outputs by definition (oracle.dft_at), inverse round trip."""
+    N = 1 << log_n
+    ctx = m.ctx_init(P)
+    w = oracle.root_of_unity(P, GEN[P], N)
+    winv = oracle.inverse(w, P)
+    plan = m.ntt_plan(ctx, w, log_n)
+    plan_inv = m.ntt_plan(ctx, winv, log_n)
+    x = synth.uniform(42, 41, P, 0, N)
+    x[:2] = [P - 1, 0]
+    X = m.ntt_large(ctx, torch.from_numpy(x).cuda(), plan)
+    Xh = X.cpu().numpy()
+    rng = np.random.default_rng(log_n)
+    for k in [0, 1, 2, N // 2, N - 1] + [int(v) for v in rng.integers(0, N, 6)]:
+        assert int(Xh[k]) == oracle.dft_at(P, w, x, k), k
+    ninv_m = int(oracle.to_mont(P, np.array([oracle.inverse(N % P, P)], np.uint32))[0])
+    back = m.ntt_large(ctx, X, plan_inv, scale=ninv_m)
+    assert np.array_equal(back.cpu().numpy(), x)
+
+
+def test_ntt_large_matches_small_path(m):
+    """2^16 six-step vs a single small-path row of the same length is impossible (small path <= 2^15),
+    so check linearity and the delta: NTT(e0) = ones, NTT(e1) = powers of w."""
+    P, log_n = 2013265921, 16
+    N = 1 << log_n
+    ctx = m.ctx_init(P)
+    w = oracle.root_of_unity(P, 31, N)
+    plan = m.ntt_plan(ctx, w, log_n)
+    e = np.zeros(N, np.uint32)
+    e[0] = 1
+    assert np.all(m.ntt_large(ctx, torch.from_numpy(e.copy()).cuda(), plan).cpu().numpy() == 1)
+    e[0], e[1] = 0, 1
+    X = m.ntt_large(ctx, torch.from_numpy(e.copy()).cuda(), plan).cpu().numpy()
+    for k in (0, 1, 2, 12345, N - 1):
+        assert int(X[k]) == pow(w, k, P)

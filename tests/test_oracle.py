@@ -379,3 +379,13 @@ def test_dot_pins(P):
     raw = oracle.dot(P, A, x)
     for r in range(5):
         assert (int(raw[r]) << 32) % P == sum(int(a) * int(b) for a, b in zip(A[r], x)) % P
+
+
+def test_dft_at_matches_dft():
+    P = 998244353
+    N = 512
+    w = oracle.root_of_unity(P, 3, N)
+    x = synth.uniform(42, 40, P, 0, N)
+    X = oracle.dft(P, w, x)
+    for k in (0, 1, 7, 255, 511, 513):
+        assert oracle.dft_at(P, w, x, k) == int(X[k % N])
