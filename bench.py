@@ -65,7 +65,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="step", choices=["step", "c2", "c3", "c4", "c5", "ntt"])
+    ap.add_argument("--workload", default="step", choices=["step", "c1", "c2", "c3", "c4", "c5", "ntt"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -222,6 +222,22 @@ class Workload:
             L.append(("mont_pow_vec", lambda base=base, e=e, o=o:
                       m.pow_vec(self.ctx[P1], base, e, out=o, cfg=self.pow_cfg), 12 * N_C4, ladder, "imad"))
             self.config.update({"c4_n": N_C4, "c4_ladder_mulmods": ladder})
+        if kind == "c1":
+            # configs[0]: n = 65536 with the fixed-index edge values (G12); launch-latency bound
+            import numpy as np
+
+            import synth as _synth  # the shared input generator (no method arithmetic)
+            ha, hb = _synth.c1_inputs(P0)
+            a = torch.from_numpy(ha).to(dev)
+            b = torch.from_numpy(hb).to(dev)
+            c = torch.empty_like(a)
+            self.c1 = (a, b, c)
+            self.inputs += [a, b]
+            self.outputs.append(c)
+            L.append(("mont_mul_vec_checksum[c1]",
+                      lambda a=a, b=b, c=c: m.mul_vec_checksum(self.ctx[P0], a, b, out=c, acc=self.acc[0:1]),
+                      12 * a.numel(), a.numel(), "hbm"))
+            self.config.update({"c1_n": a.numel()})
         if kind == "ntt":
             # forward NTT of the configs[2] batch (4096 rows of 2^14) over P0
             x = torch.empty(TW_BATCH * TW_LEN, **u32)
@@ -349,6 +365,9 @@ def verify(wl: Workload) -> dict:
     if hasattr(wl, "c5"):
         a, b, c = wl.c5
         checks["c5_identity"] = identity(P0, a, b, c)
+    if hasattr(wl, "c1"):
+        a, b, c = wl.c1
+        checks["c1_identity"] = identity(P0, a, b, c)
     if hasattr(wl, "ntt_x"):
         x0 = wl.ntt_x0[7].cpu().numpy()
         X = wl.ntt_x[7].cpu().numpy()
@@ -470,6 +489,12 @@ def time_e2e(wl: Workload, steps: int):
         hb, he, ho2 = pin(base), pin(e), empty(o)
         jobs.append(m.host_job("pow_vec", wl.ctx[P1], ho2, hb, he))
         keep += [hb, he, ho2]
+    if hasattr(wl, "c1"):
+        a, b, c = wl.c1
+        ha, hb, hc = pin(a), pin(b), empty(c)
+        acc = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+        jobs.append(m.host_job("mul_vec", wl.ctx[P0], hc, ha, hb, acc=acc))
+        keep += [ha, hb, hc, acc]
     if hasattr(wl, "c5"):
         a, b, c = wl.c5
         ha, hb, hc = pin(a), pin(b), empty(c)
@@ -665,14 +690,14 @@ def main():
     serial_ms = shard.max_over_ranks(serial_ms)
     ms_per_step = total_ms / args.steps
     # checksum partials -> one NCCL all-reduce SUM (A11), outside the timed region
-    if wl.kind in ("step", "c2", "c5"):
+    if wl.kind in ("step", "c1", "c2", "c5"):
         wl.acc.zero_()
         for name, fn, *_ in wl.launches:
             if name.startswith("mont_mul_vec_checksum"):
                 fn()
         torch.cuda.synchronize()
         local = [int(v) for v in wl.acc.tolist()]
-        prim = list(PRIMES) if wl.kind != "c5" else [P0]
+        prim = list(PRIMES) if wl.kind not in ("c5", "c1") else [P0]
         box_checksums = shard.combine_checksums(local[:len(prim)], prim)
     else:
         box_checksums = None
@@ -727,6 +752,7 @@ def main():
                                          "configs[2] twiddle + configs[3] pow (checksum fused into mul_vec)",
                                 "c2": "configs[1] mul_vec x3 primes + checksums", "c3": "configs[2] twiddle",
                                 "c4": "configs[3] pow", "c5": "configs[4] sharded mul_vec n=2^31 + checksum",
+                                "c1": "configs[0] mul_vec n=65536 with fixed edge values (launch-latency bound)",
                                 "ntt": "SURVEY 8(f) NEXT #1: in-place forward NTT of the configs[2] batch, 4096 x 2^14"}[wl.kind],
                    "parallelism": f"dp{world} (contiguous global-index slices, no data-path collective)",
                    "l2": "inputs larger than L2 (step working set ~3.3 GiB vs 126 MB L2)",
