@@ -540,6 +540,14 @@ def cpu_baseline(kind: str, target_s: float = 3.0, nsteps: int = 1):
         n4 = max(4, int(N_C4 * frac))
         rows = max(1, int(TW_BATCH * frac))
         parts = []
+        if kind == "c1":
+            a, b = synth.c1_inputs(P0)
+            t0 = time.perf_counter()
+            for _ in range(max(1, int(frac * 1024))):
+                oracle.mont_mul(P0, a, b, nthreads=cores)
+            t_total += time.perf_counter() - t0
+            mm += a.size * max(1, int(frac * 1024))
+            parts.append(f"c1 {a.size} x {max(1, int(frac * 1024))} repetitions")
         if kind in ("step", "c2", "c5"):
             for P in (PRIMES if kind != "c5" else (P0,)):
                 a, b = (synth.c2_inputs(P, 0, n2) if kind != "c5" else synth.c5_inputs(P, 0, n2))
@@ -823,6 +831,14 @@ def _ref_step(kind, frac):
     n4 = max(4, int(N_C4 * frac))
     rows = max(1, int(TW_BATCH * frac))
     t_total, mm = 0.0, 0
+    if kind == "c1":
+        a, b = synth.c1_inputs(P0)
+        reps = max(1, int(frac * 1024))
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            oracle.mont_mul(P0, a, b, nthreads=cores)
+        t_total += time.perf_counter() - t0
+        mm += a.size * reps
     if kind in ("step", "c2", "c5"):
         for P in (PRIMES if kind != "c5" else (P0,)):
             a, b = synth.c2_inputs(P, 0, n2)
