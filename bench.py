@@ -797,7 +797,7 @@ def main():
                                "operations as jobs of one H2D / kernel / D2H ring"}
     if world == 1 and not args.no_cpu_baseline:
         v, cores, sample, secs, frac = cpu_baseline(wl.kind)
-        line["cpu_baseline"] = {"value": round(v, 4), "unit": "Gmulmod/s", "cores": cores, "kind": "oracle",
+        line["cpu_baseline"] = {"value": float(f"{v:.4g}"), "unit": "Gmulmod/s", "cores": cores, "kind": "oracle",
                                 "sample": sample, "seconds": round(secs, 3)}
     print(json.dumps(line), flush=True)
     if dist.is_initialized():
@@ -820,13 +820,13 @@ def main_reference(args, rank, world):
             times.append((secs, v))
     tot_s = sum(s for s, _ in times)
     value = statistics.median(v for _, v in times)
-    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "Gmulmod/s", "n_gpus": world,
+    line = {"impl": "reference", "metric": METRIC, "value": float(f"{value:.4g}"), "unit": "Gmulmod/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot_s / max(1, len(times)), 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (seeded SplitMix64 counter generator, host-side synth/)",
             "config": {"workload": f"bounded sample of the '{kind}' workload (oracle/ on host cores)",
                        "sample_fraction": frac},
-            "cpu_baseline": {"value": round(value, 4), "unit": "Gmulmod/s", "cores": cores, "kind": "oracle",
+            "cpu_baseline": {"value": float(f"{value:.4g}"), "unit": "Gmulmod/s", "cores": cores, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": round(value, 4), "unit": "Gmulmod/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
