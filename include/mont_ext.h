@@ -42,7 +42,8 @@ extern "C" {
  *                                   per thread.
  *                                   ctas_per_sm = 0 selects a flat grid.
  *                 mont_mul_twiddle_ex : 0 = bulk-copy (TMA) staged table,
- *                                   1 = table read through L1/L2 (no smem)
+ *                                   1 = table read through L1/L2 (no smem),
+ *                                   2 = flat stream (power-of-two len; else 0)
  *   chunk     : mont_mul_twiddle_ex only: table columns staged per CTA
  *               (multiple of 4; 0 = min(len, 4096)).                       */
 typedef struct mont_launch {

@@ -95,6 +95,30 @@ __global__ void __launch_bounds__(512) k_twiddle(Ctx c, uint32_t *out, const uin
     if (!waited) mbar_wait(&bar, 0);  // never leave with a copy in flight
 }
 
+// Flat variant (variant 2) for power-of-two len: the batch is one flat stream
+// of uint4 chunks (like k_map1), chunk i uses table quad i mod (len/4), read
+// through the read-only path (the whole table stays L1/L2-resident).
+template <int U>
+__global__ void __launch_bounds__(512) k_twiddle_flat(Ctx c, uint32_t *out, const uint32_t *x, const uint32_t *tw,
+                                                       size_t n4, size_t qmask) {
+    const uint4 *x4 = reinterpret_cast<const uint4 *>(x);
+    const uint4 *t4 = reinterpret_cast<const uint4 *>(tw);
+    uint4 *o4 = reinterpret_cast<uint4 *>(out);
+    const size_t tile = (size_t)U * blockDim.x;
+    const size_t base = (size_t)blockIdx.x * tile + threadIdx.x;
+    uint4 v[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+        const size_t i = base + (size_t)k * blockDim.x;
+        if (i < n4) v[k] = ld_stream(x4 + i);
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+        const size_t i = base + (size_t)k * blockDim.x;
+        if (i < n4) st_stream(o4 + i, redc4(v[k], __ldg(t4 + (i & qmask)), c.p, c.pinv));
+    }
+}
+
 // Scalar fallback (len % 4 != 0 or misaligned operands)
 __global__ void __launch_bounds__(256) k_twiddle_scalar(Ctx c, uint32_t *out, const uint32_t *x, const uint32_t *tw,
                                                          size_t batch, size_t len) {
@@ -149,10 +173,10 @@ extern "C" mont_status_t mont_mul_twiddle_ex(const mont_ctx_t *ctx, uint32_t *ou
     if (len == 0) return MONT_EINVAL_ARG;
     if (!out || !x || !tw || ((uintptr_t)out | (uintptr_t)x | (uintptr_t)tw) & 3u) return MONT_EINVAL_ARG;
     if (batch > ((size_t)-1) / len) return MONT_EINVAL_ARG;
-    const Launch L = resolve(cfg, kTwDefault);
+    Launch L = resolve(cfg, kTwDefault);
     if (L.threads < 32 || L.threads > 512 || (L.threads & 31) || L.ctas_per_sm < 1 || L.chunk < 4 ||
         (L.chunk & 3) || !(L.unroll == 1 || L.unroll == 2 || L.unroll == 4 || L.unroll == 8) || L.variant < 0 ||
-        L.variant > 1)
+        L.variant > 2)
         return MONT_EINVAL_ARG;
     const int sms = sm_count();
     if (sms <= 0) return MONT_ECUDA;
@@ -167,6 +191,20 @@ extern "C" mont_status_t mont_mul_twiddle_ex(const mont_ctx_t *ctx, uint32_t *ou
         k_twiddle_scalar<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, stream>>>(c, out, x, tw, batch, len);
         return launch_status();
     }
+    if (L.variant == 2 && (len & (len - 1)) == 0) {  // flat stream, power-of-two rows
+        const size_t n4 = batch * len / 4;
+        const size_t tile = (size_t)L.unroll * L.threads;
+        const size_t grid = (n4 + tile - 1) / tile;
+        if (grid > 0x7fffffff) return MONT_EUNSUPPORTED;
+        switch (L.unroll) {
+            case 1: k_twiddle_flat<1><<<(unsigned)grid, L.threads, 0, stream>>>(c, out, x, tw, n4, len / 4 - 1); break;
+            case 2: k_twiddle_flat<2><<<(unsigned)grid, L.threads, 0, stream>>>(c, out, x, tw, n4, len / 4 - 1); break;
+            case 4: k_twiddle_flat<4><<<(unsigned)grid, L.threads, 0, stream>>>(c, out, x, tw, n4, len / 4 - 1); break;
+            default: k_twiddle_flat<8><<<(unsigned)grid, L.threads, 0, stream>>>(c, out, x, tw, n4, len / 4 - 1); break;
+        }
+        return launch_status();
+    }
+    if (L.variant == 2) L.variant = 0;
     if (L.variant == 0) {
         switch (L.unroll) {
             case 1: return launch_tw<1, true>(c, out, x, tw, batch, len, L, sms, stream);

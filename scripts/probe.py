@@ -317,3 +317,23 @@ if args.what in ("nttlarge",):
         med, _ = timeit(lambda: m.ntt_large(ctx, x, plan, out=o), reps=10)
         out(what="ntt_large", log_n=log_n, us=med * 1e6, gbs_5pass=40 * N / med / 1e9,
             tbutterfly=(N // 2) * log_n / med / 1e12)
+
+if args.what in ("tw2",):
+    P = 2013265921
+    ctx = m.ctx_init(P)
+    batch, L = 4096, 1 << 14
+    x = torch.empty(batch * L, dtype=torch.uint32, device=dev)
+    m.synth_fill(x, 42, 5, 0, P)
+    x = x.view(batch, L)
+    o = torch.empty_like(x)
+    tw = m.twiddle_table(ctx, 1657000625, L)
+    med, _ = timeit(lambda: m.mul_twiddle(ctx, x, tw, out=o))
+    out(what="twiddle default", us=med * 1e6, gbs=8 * batch * L / med / 1e9)
+    for threads in (256, 512):
+        for unroll in (1, 2, 4):
+            cfg = m.Launch(threads=threads, unroll=unroll, variant=2)
+            med, _ = timeit(lambda: m.mul_twiddle(ctx, x, tw, out=o, cfg=cfg))
+            out(what="twiddle flat", threads=threads, unroll=unroll, us=med * 1e6, gbs=8 * batch * L / med / 1e9)
+    cfg = m.Launch(threads=512, unroll=2)
+    med, _ = timeit(lambda: m.to_mont(ctx, x.view(-1), out=o.view(-1), cfg=cfg))
+    out(what="to_mont 512x2", us=med * 1e6, gbs=8 * batch * L / med / 1e9)
