@@ -106,16 +106,19 @@ __global__ void __launch_bounds__(512) k_twiddle_flat(Ctx c, uint32_t *out, cons
     uint4 *o4 = reinterpret_cast<uint4 *>(out);
     const size_t tile = (size_t)U * blockDim.x;
     const size_t base = (size_t)blockIdx.x * tile + threadIdx.x;
-    uint4 v[U];
+    uint4 v[U], t[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) {
         const size_t i = base + (size_t)k * blockDim.x;
-        if (i < n4) v[k] = ld_stream(x4 + i);
+        if (i < n4) {
+            v[k] = ld_stream(x4 + i);
+            t[k] = __ldg(t4 + (i & qmask));
+        }
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
         const size_t i = base + (size_t)k * blockDim.x;
-        if (i < n4) st_stream(o4 + i, redc4(v[k], __ldg(t4 + (i & qmask)), c.p, c.pinv));
+        if (i < n4) st_stream(o4 + i, redc4(v[k], t[k], c.p, c.pinv));
     }
 }
 
