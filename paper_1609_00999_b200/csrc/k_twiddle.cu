@@ -133,10 +133,12 @@ __global__ void __launch_bounds__(256) k_twiddle_scalar(Ctx c, uint32_t *out, co
     }
 }
 
-// B200 sweep: many small CTAs (target 64 per SM, a few rows each)
-// balance like a flat grid; a 4096-column (16 KiB) staged chunk keeps the
-// table re-read from L2 at 1/4 of the x stream per row block.
-static const Launch kTwDefault{256, 64, 4, 0, 4096};
+// B200 sweeps: for power-of-two rows the flat stream with the
+// table through L1 (variant 2, 512 threads x 4 uint4) runs at the to_mont rate
+// (82 us for configs[2], 1.0x the measured copy peak); the bulk-copy staged
+// table (variant 0) peaks at 84-86 us with many small CTAs (64 per SM, a few
+// rows and a 4096-column chunk each) and is the path for other row lengths.
+static const Launch kTwDefault{512, 64, 4, 2, 4096};
 
 template <int U, bool TMA>
 static mont_status_t launch_tw(const Ctx &c, uint32_t *out, const uint32_t *x, const uint32_t *tw, size_t batch,
@@ -207,7 +209,10 @@ extern "C" mont_status_t mont_mul_twiddle_ex(const mont_ctx_t *ctx, uint32_t *ou
         }
         return launch_status();
     }
-    if (L.variant == 2) L.variant = 0;
+    if (L.variant == 2) {  // not a power of two: the staged-table kernel with its own best shape
+        L.variant = 0;
+        if (!cfg || cfg->threads == 0) L.threads = 256;
+    }
     if (L.variant == 0) {
         switch (L.unroll) {
             case 1: return launch_tw<1, true>(c, out, x, tw, batch, len, L, sms, stream);
