@@ -193,10 +193,6 @@ def _ptr(t) -> int:
     return t.data_ptr()
 
 
-def _cfg(cfg):
-    return C.byref(cfg) if cfg is not None else None
-
-
 def mul_vec(ctx: Ctx, a, b, out=None, stream=None, cfg: Launch | None = None):
     """c[i] = a[i] b[i] R^-1 mod P (mont_mul_vec)."""
     _dev_u32(a, "a"), _dev_u32(b, "b")
