@@ -46,7 +46,7 @@ def combine_checksums(local_sums, P, group=None):
     Ps = [P] * len(sums) if not isinstance(P, (list, tuple)) else list(P)
     vals = torch.tensor([int(s) % int(p) for s, p in zip(sums, Ps)], dtype=torch.int64,
                         device=_device_for(group))
-    if dist.is_initialized() and dist.get_world_size(group) > 1:
+    if dist.is_initialized():
         dist.all_reduce(vals, op=dist.ReduceOp.SUM, group=group)
     out = [int(v) % int(p) for v, p in zip(vals.tolist(), Ps)]
     return out[0] if single else out
@@ -54,7 +54,7 @@ def combine_checksums(local_sums, P, group=None):
 
 def max_over_ranks(x: float, group=None) -> float:
     """Box timing: the MAX of a per-rank float over all ranks."""
-    if not (dist.is_initialized() and dist.get_world_size(group) > 1):
+    if not dist.is_initialized():
         return float(x)
     t = torch.tensor([float(x)], dtype=torch.float64, device=_device_for(group))
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
@@ -62,7 +62,7 @@ def max_over_ranks(x: float, group=None) -> float:
 
 
 def barrier(group=None) -> None:
-    if dist.is_initialized() and dist.get_world_size(group) > 1:
+    if dist.is_initialized():
         if dist.get_backend(group) == "nccl":
             dist.barrier(group=group, device_ids=[torch.cuda.current_device()])
         else:
