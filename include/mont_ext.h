@@ -43,7 +43,11 @@ extern "C" {
  *                                   ctas_per_sm = 0 selects a flat grid.
  *                 mont_mul_twiddle_ex : 0 = bulk-copy (TMA) staged table,
  *                                   1 = table read through L1/L2 (no smem),
- *                                   2 = flat stream (power-of-two len; else 0)
+ *                                   2 = flat stream (power-of-two len; else 0),
+ *                                   3 = whole table staged once per CTA
+ *                                   by TMA + cluster-launch-control work
+ *                                   stealing over 2-row items (4 len <=
+ *                                   200 KiB; else 0)
  *   chunk     : mont_mul_twiddle_ex only: table columns staged per CTA
  *               (multiple of 4; 0 = min(len, 4096)).                       */
 typedef struct mont_launch {

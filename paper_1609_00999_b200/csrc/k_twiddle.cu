@@ -122,6 +122,68 @@ __global__ void __launch_bounds__(512) k_twiddle_flat(Ctx c, uint32_t *out, cons
     }
 }
 
+// Variant 3: the whole table staged ONCE per CTA lifetime by the bulk-copy
+// engine, rows processed in blocks of `rows_per_item`, and the CTA keeps
+// taking row blocks from not-yet-launched CTAs by cluster launch control
+// (hardware work stealing) -- TMA staging without paying the table per block,
+// with the dynamic balance of a flat grid.  len % 4 == 0, 4 len <= 227 KB.
+__global__ void __launch_bounds__(512) k_twiddle_clc(Ctx c, uint32_t *out, const uint32_t *x, const uint32_t *tw,
+                                                      size_t batch, size_t len, uint32_t rows_per_item) {
+    extern __shared__ __align__(128) uint4 s_tw[];
+    __shared__ __align__(8) uint64_t bar_tw;
+    __shared__ __align__(8) uint64_t bar_clc;
+    __shared__ __align__(16) uint4 clc_resp;
+    const uint32_t len4 = (uint32_t)(len >> 2);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar_tw, 1);
+        mbar_init(&bar_clc, 1);
+        fence_mbar_init();
+        const uint32_t bytes = len4 * 16u;
+        mbar_expect_tx(&bar_tw, bytes);
+        for (uint32_t off = 0; off < bytes; off += 16384u)
+            bulk_g2s(reinterpret_cast<char *>(s_tw) + off, reinterpret_cast<const char *>(tw) + off,
+                     bytes - off < 16384u ? bytes - off : 16384u, &bar_tw);
+    }
+    __syncthreads();
+    mbar_wait(&bar_tw, 0);
+    const uint4 *x4 = reinterpret_cast<const uint4 *>(x);
+    uint4 *o4 = reinterpret_cast<uint4 *>(out);
+    uint32_t item = blockIdx.x, phase = 0;
+    while (true) {
+        if (threadIdx.x == 0) {  // ask for the next item while this one streams
+            fence_mbar_init();
+            mbar_expect_tx(&bar_clc, 16u);
+            clc_try_cancel(&clc_resp, &bar_clc);
+        }
+        const size_t r0 = (size_t)item * rows_per_item;
+        const size_t nrows = batch - r0 < rows_per_item ? batch - r0 : rows_per_item;
+        for (size_t r = 0; r < nrows; ++r) {
+            const uint4 *xr = x4 + (r0 + r) * len4;
+            uint4 *orow = o4 + (r0 + r) * len4;
+            for (uint32_t c0 = threadIdx.x; c0 < len4; c0 += 4 * blockDim.x) {
+                uint4 v[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t cc = c0 + k * blockDim.x;
+                    if (cc < len4) v[k] = ld_stream(xr + cc);
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t cc = c0 + k * blockDim.x;
+                    if (cc < len4) st_stream(orow + cc, redc4(v[k], s_tw[cc], c.p, c.pinv));
+                }
+            }
+        }
+        mbar_wait(&bar_clc, phase);
+        phase ^= 1u;
+        uint32_t next;
+        const bool more = clc_query(clc_resp, next);
+        __syncthreads();  // everyone has read clc_resp before it is overwritten
+        if (!more) break;
+        item = next;
+    }
+}
+
 // Scalar fallback (len % 4 != 0 or misaligned operands)
 __global__ void __launch_bounds__(256) k_twiddle_scalar(Ctx c, uint32_t *out, const uint32_t *x, const uint32_t *tw,
                                                          size_t batch, size_t len) {
@@ -181,7 +243,7 @@ extern "C" mont_status_t mont_mul_twiddle_ex(const mont_ctx_t *ctx, uint32_t *ou
     Launch L = resolve(cfg, kTwDefault);
     if (L.threads < 32 || L.threads > 512 || (L.threads & 31) || L.ctas_per_sm < 1 || L.chunk < 4 ||
         (L.chunk & 3) || !(L.unroll == 1 || L.unroll == 2 || L.unroll == 4 || L.unroll == 8) || L.variant < 0 ||
-        L.variant > 2)
+        L.variant > 3)
         return MONT_EINVAL_ARG;
     const int sms = sm_count();
     if (sms <= 0) return MONT_ECUDA;
@@ -196,6 +258,18 @@ extern "C" mont_status_t mont_mul_twiddle_ex(const mont_ctx_t *ctx, uint32_t *ou
         k_twiddle_scalar<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, stream>>>(c, out, x, tw, batch, len);
         return launch_status();
     }
+    if (L.variant == 3 && len * 4 <= 200 * 1024) {  // staged once per CTA + CLC work stealing
+        const uint32_t rows_per_item = 2u;
+        const size_t items = (batch + rows_per_item - 1) / rows_per_item;
+        const size_t smem = len * 4;
+        if (items > 0x7fffffff) return MONT_EUNSUPPORTED;
+        if (smem > 48 * 1024 &&
+            cudaFuncSetAttribute(k_twiddle_clc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return MONT_ECUDA;
+        k_twiddle_clc<<<(unsigned)items, 512, smem, stream>>>(c, out, x, tw, batch, len, rows_per_item);
+        return launch_status();
+    }
+    if (L.variant == 3) L.variant = 0;
     if (L.variant == 2 && (len & (len - 1)) == 0) {  // flat stream, power-of-two rows
         const size_t n4 = batch * len / 4;
         const size_t tile = (size_t)L.unroll * L.threads;

@@ -40,4 +40,32 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
     } while (!done);
 }
 
+// ---- cluster launch control (sm_100): hardware work stealing.  A running CTA
+// asks the scheduler to cancel a not-yet-launched CTA of the same grid and, on
+// success, processes that CTA's work itself -- a persistent kernel with dynamic
+// load balancing and no global work counter.  The 16-byte response lands in
+// shared memory and completes on an mbarrier like a bulk copy.
+__device__ __forceinline__ void clc_try_cancel(uint4 *resp, uint64_t *bar) {
+    asm volatile(
+        "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];" ::"r"(
+            smem_u32(resp)),
+        "r"(smem_u32(bar))
+        : "memory");
+}
+// returns true and the first ctaid.x of the cancelled CTA, or false (no more work)
+__device__ __forceinline__ bool clc_query(const uint4 &r, uint32_t &ctaid_x) {
+    uint32_t ok, x;
+    asm volatile(
+        "{\n\t.reg .b128 resp;\n\t.reg .pred p;\n\t"
+        "mov.b128 resp, {%2, %3};\n\t"
+        "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, resp;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t"
+        "@p clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %1, resp;\n\t}"
+        : "=r"(ok), "=r"(x)
+        : "l"(((unsigned long long)r.y << 32) | r.x), "l"(((unsigned long long)r.w << 32) | r.z)
+        : "memory");
+    ctaid_x = x;
+    return ok != 0;
+}
+
 }  // namespace mont

@@ -329,6 +329,12 @@ if args.what in ("tw2",):
     tw = m.twiddle_table(ctx, 1657000625, L)
     med, _ = timeit(lambda: m.mul_twiddle(ctx, x, tw, out=o))
     out(what="twiddle default", us=med * 1e6, gbs=8 * batch * L / med / 1e9)
+    cfg = m.Launch(variant=3)
+    med, _ = timeit(lambda: m.mul_twiddle(ctx, x, tw, out=o, cfg=cfg))
+    out(what="twiddle TMA-staged once + CLC work stealing (variant 3)", us=med * 1e6, gbs=8 * batch * L / med / 1e9)
+    cfg = m.Launch(variant=0, threads=256)
+    med, _ = timeit(lambda: m.mul_twiddle(ctx, x, tw, out=o, cfg=cfg))
+    out(what="twiddle TMA-staged per CTA (variant 0)", us=med * 1e6, gbs=8 * batch * L / med / 1e9)
     for threads in (256, 512):
         for unroll in (1, 2, 4):
             cfg = m.Launch(threads=threads, unroll=unroll, variant=2)

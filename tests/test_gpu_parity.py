@@ -235,8 +235,8 @@ def test_twiddle_table_parity(m, L):
 
 
 @pytest.mark.parametrize("batch,L", [(1, 4), (3, 8), (5, 1000), (17, 1024), (7, 16384), (3, 16388), (2, 40000),
-                                     (1000, 64), (33, 4100), (513, 4)])
-@pytest.mark.parametrize("variant", [0, 1, 2])
+                                     (1000, 64), (33, 4100), (513, 4), (4096, 2048)])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
 def test_twiddle_parity(m, batch, L, variant):
     P = 2013265921
     x = synth.c3_x(P, batch=batch, length=L)
