@@ -26,15 +26,22 @@ extern "C" {
  * scale : the output factor s in Montgomery form (to_mont(s)); ctx->r1 means
  *         s = 1 (no extra multiply); to_mont(N^-1) with the w^-1 table makes
  *         the normalised inverse.
- * Radix-2 Cooley-Tukey (decimation in time, bit-reversed load) with each
- * butterfly u' = u + REDC(v, tw), v' = u - REDC(v, tw) on plain residues, mod
- * add/sub by one conditional correction ("straightforward").  One
- * CTA per row; the row lives in shared memory for all log_n stages, so HBM
- * traffic is 8 bytes per element.  1 <= log_n <= 15 (N <= 32768 words = 128 KiB
+ * Radix-2 Gentleman-Sande (decimation in frequency) with each butterfly
+ * (u, v) -> (u + v, REDC(u - v, tw)) on plain residues, mod add/sub by one
+ * conditional correction ("straightforward"); 32 elements per
+ * thread, five stages per trip through shared memory.  A row is read from and
+ * written to HBM once: 8 bytes per element.  1 <= log_n <= 15 (N <= 32768 words = 128 KiB
  * of shared memory), else MONT_EUNSUPPORTED.  data 4-byte aligned; tw, data
  * device pointers; rows may not overlap. */
 mont_status_t mont_ntt(const mont_ctx_t *ctx, uint32_t *data, size_t batch, int log_n, const uint32_t *tw,
                        uint32_t scale, cudaStream_t stream);
+
+/* mont_ntt with an explicit kernel: variant 0 = decimation in frequency (the
+ * default: natural-order input read straight into registers, bit reversal in
+ * the final shared-memory gather), 1 = decimation in time (bit-reversed load),
+ * 2 = one butterfly per thread per stage in shared memory (reference). */
+mont_status_t mont_ntt_ex(const mont_ctx_t *ctx, uint32_t *data, size_t batch, int log_n, const uint32_t *tw,
+                          uint32_t scale, int variant, cudaStream_t stream);
 
 /* tw[2^(s-1) - 1 + pos] = to_mont(w^(pos * 2^(log_n - s))) for s = 1..log_n,
  * pos < 2^(s-1): N - 1 entries (device pointer), each an independent

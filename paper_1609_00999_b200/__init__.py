@@ -87,6 +87,7 @@ SIGNATURES = {
 
 SIGNATURES["mont_ntt"] = (C.c_int, [_CTX, _P, _S, C.c_int, _P, C.c_uint32, _P])
 SIGNATURES["mont_ntt_twiddles"] = (C.c_int, [_CTX, _P, C.c_uint32, C.c_int, _P])
+SIGNATURES["mont_ntt_ex"] = (C.c_int, [_CTX, _P, _S, C.c_int, _P, C.c_uint32, C.c_int, _P])
 SIGNATURES["mont_dot"] = (C.c_int, [_CTX, _P, _P, _P, _S, _S, _P])
 SIGNATURES["mont_ntt_plan_words"] = (C.c_size_t, [C.c_int])
 SIGNATURES["mont_ntt_plan_init"] = (C.c_int, [_CTX, _P, C.c_uint32, C.c_int, _P])
@@ -379,7 +380,7 @@ def ntt_twiddles(ctx: Ctx, w: int, log_n: int, device="cuda", stream=None):
     return tw
 
 
-def ntt(ctx: Ctx, data, tw, scale: int | None = None, stream=None):
+def ntt(ctx: Ctx, data, tw, scale: int | None = None, stream=None, variant: int | None = None):
     """In-place batched NTT of the rows of `data` (batch, N), N = 2^k <= 32768 (include/mont_ntt.h).
     tw: stage-major table from ntt_twiddles(); scale: Montgomery form of the output factor."""
     _dev_u32(data, "data"), _dev_u32(tw, "tw")
@@ -389,8 +390,13 @@ def ntt(ctx: Ctx, data, tw, scale: int | None = None, stream=None):
     log_n = n.bit_length() - 1
     if n != 1 << log_n or tw.numel() < n - 1:
         raise ValueError("N must be a power of two and tw must hold the N-1 stage-major twiddles")
-    _check(lib().mont_ntt(C.byref(ctx), _ptr(data), batch, log_n, _ptr(tw), ctx.r1 if scale is None else scale,
-                          _stream_handle(stream)), "mont_ntt")
+    sc = ctx.r1 if scale is None else scale
+    if variant is None:
+        _check(lib().mont_ntt(C.byref(ctx), _ptr(data), batch, log_n, _ptr(tw), sc, _stream_handle(stream)),
+               "mont_ntt")
+    else:
+        _check(lib().mont_ntt_ex(C.byref(ctx), _ptr(data), batch, log_n, _ptr(tw), sc, variant,
+                                 _stream_handle(stream)), "mont_ntt_ex")
     return data
 
 

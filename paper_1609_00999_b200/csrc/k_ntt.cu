@@ -151,6 +151,94 @@ __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
     }
 }
 
+// ---- decimation-in-frequency form (Gentleman-Sande), natural-order input:
+// trip 0 reads its 32 elements per thread straight from global memory
+// (window = the TOP five index bits, so lanes read consecutive words) and the
+// bit-reversed result is unscrambled by the final shared-memory gather -- one
+// shared-memory pass fewer than the DIT kernel above.  Butterfly:
+// (u, v) -> (u + v, (u - v) w^pos), stages from pair distance N/2 down to 1.
+template <int LOG_N>
+__global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
+    k_ntt_dif(Ctx c, uint32_t *data, size_t batch, const uint32_t *__restrict__ tw, uint32_t scale, Tw2D t2) {
+    constexpr uint32_t N = 1u << LOG_N, T = N >> 5;
+    extern __shared__ uint32_t sm[];
+    const uint32_t rl = threadIdx.x / T, t = threadIdx.x % T;
+    const size_t row = (size_t)blockIdx.x * (blockDim.x / T) + rl;
+    const bool live = row < batch;
+    uint32_t *s = sm + (size_t)rl * N;
+    uint32_t *g = data + row * N;
+    uint32_t v[32];
+    constexpr int NTRIP = (LOG_N + 4) / 5;
+#pragma unroll
+    for (int trip = 0; trip < NTRIP; ++trip) {
+        // window of this trip: bits [wlo, wlo + 5); stages done: bits >= hi_done
+        const int top = LOG_N - 5 * trip;               // bits >= top already processed
+        const int wlo = top - 5 > 0 ? top - 5 : 0;
+        const uint32_t tl = t & ((1u << wlo) - 1u);
+        const uint32_t base = tl | ((t >> wlo) << (wlo + 5));
+        const uint32_t sb = swz(base);
+        if (trip == 0) {
+            if (live) {
+#pragma unroll
+                for (int k = 0; k < 32; ++k) v[k] = ld_stream1(g + base + ((uint32_t)k << wlo));
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) v[k] = s[sb ^ swz((uint32_t)k << wlo)];
+        }
+#pragma unroll
+        for (int lb = 4; lb >= 0; --lb) {
+            const int b = wlo + lb;                     // pair distance 2^b
+            if (b >= top) continue;                     // done by an earlier trip
+            const uint32_t *twb = tw + ((1u << b) - 1u) + tl;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int k0 = ((q >> lb) << (lb + 1)) | (q & ((1 << lb) - 1));
+                const int k1 = k0 | (1 << lb);
+                const uint32_t w = __ldg(twb + ((uint32_t)(k0 & ((1 << lb) - 1)) << wlo));
+                const uint32_t a = v[k0], d = v[k1];
+                v[k0] = mod_add(a, d, c.p);
+                v[k1] = redc(mod_sub(a, d, c.p), w, c.p, c.pinv);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 32; ++k) s[sb ^ swz((uint32_t)k << wlo)] = v[k];
+        __syncthreads();
+    }
+    if (live) {
+        // X[idx] sits at the bit-reversed position
+        const uint32_t bt = swz(__brev(t) >> (32 - LOG_N));
+        const uint64_t rowg = (uint64_t)(row + t2.row0);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            const uint32_t idx = t + (uint32_t)k * T;
+            uint32_t x = s[bt ^ swz(__brev((uint32_t)k * T) >> (32 - LOG_N))];
+            if (t2.lo) {
+                const uint64_t e = (rowg * idx) & t2.mask;
+                const uint32_t we = redc(__ldg(t2.hi + (e >> t2.shift)), __ldg(t2.lo + (e & t2.lomask)), c.p, c.pinv);
+                x = redc(x, we, c.p, c.pinv);
+            }
+            if (scale != c.r1) x = redc(x, scale, c.p, c.pinv);
+            st_stream1(g + idx, x);
+        }
+    }
+}
+
+template <int LOG_N>
+static mont_status_t launch_ntt_dif(const Ctx &c, uint32_t *data, size_t batch, const uint32_t *tw, uint32_t scale,
+                                    cudaStream_t stream, Tw2D t2) {
+    constexpr uint32_t N = 1u << LOG_N, T = N >> 5;
+    constexpr uint32_t rpc = T >= 256 ? 1u : 256u / T;
+    const size_t smem = (size_t)rpc * N * 4;
+    const size_t grid = (batch + rpc - 1) / rpc;
+    if (grid > 0x7fffffffu) return MONT_EUNSUPPORTED;
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(k_ntt_dif<LOG_N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return MONT_ECUDA;
+    k_ntt_dif<LOG_N><<<(unsigned)grid, rpc * T, smem, stream>>>(c, data, batch, tw, scale, t2);
+    return launch_status();
+}
+
 template <int LOG_N>
 static mont_status_t launch_ntt_r32(const Ctx &c, uint32_t *data, size_t batch, const uint32_t *tw, uint32_t scale,
                                     cudaStream_t stream, Tw2D t2 = Tw2D{nullptr, nullptr, 0, 0, 0, 0}) {
@@ -209,23 +297,29 @@ static mont_status_t transpose(uint32_t *dst, const uint32_t *src, size_t R, siz
     return launch_status();
 }
 
+#define MONT_NTT_CASE(L)                                                                           \
+    case L:                                                                                        \
+        return dif ? launch_ntt_dif<L>(c, data, batch, tw, scale, s, t2)                          \
+                   : launch_ntt_r32<L>(c, data, batch, tw, scale, s, t2);
+
 static mont_status_t ntt_rows(const Ctx &c, uint32_t *data, size_t batch, int log_n, const uint32_t *tw,
-                              uint32_t scale, cudaStream_t s, Tw2D t2) {
+                              uint32_t scale, cudaStream_t s, Tw2D t2, bool dif = true) {
     switch (log_n) {
-        case 5: return launch_ntt_r32<5>(c, data, batch, tw, scale, s, t2);
-        case 6: return launch_ntt_r32<6>(c, data, batch, tw, scale, s, t2);
-        case 7: return launch_ntt_r32<7>(c, data, batch, tw, scale, s, t2);
-        case 8: return launch_ntt_r32<8>(c, data, batch, tw, scale, s, t2);
-        case 9: return launch_ntt_r32<9>(c, data, batch, tw, scale, s, t2);
-        case 10: return launch_ntt_r32<10>(c, data, batch, tw, scale, s, t2);
-        case 11: return launch_ntt_r32<11>(c, data, batch, tw, scale, s, t2);
-        case 12: return launch_ntt_r32<12>(c, data, batch, tw, scale, s, t2);
-        case 13: return launch_ntt_r32<13>(c, data, batch, tw, scale, s, t2);
-        case 14: return launch_ntt_r32<14>(c, data, batch, tw, scale, s, t2);
-        case 15: return launch_ntt_r32<15>(c, data, batch, tw, scale, s, t2);
+        MONT_NTT_CASE(5)
+        MONT_NTT_CASE(6)
+        MONT_NTT_CASE(7)
+        MONT_NTT_CASE(8)
+        MONT_NTT_CASE(9)
+        MONT_NTT_CASE(10)
+        MONT_NTT_CASE(11)
+        MONT_NTT_CASE(12)
+        MONT_NTT_CASE(13)
+        MONT_NTT_CASE(14)
+        MONT_NTT_CASE(15)
         default: return MONT_EUNSUPPORTED;
     }
 }
+#undef MONT_NTT_CASE
 
 // split of a large transform: N = N1 * N2, log N1 = a <= log N2 = b <= 15
 static void ntt_split(int log_n, int &a, int &b, int &sh) {
@@ -313,28 +407,18 @@ extern "C" mont_status_t mont_ntt_twiddles(const mont_ctx_t *ctx, uint32_t *tw, 
     return launch_status();
 }
 
-extern "C" mont_status_t mont_ntt(const mont_ctx_t *ctx, uint32_t *data, size_t batch, int log_n, const uint32_t *tw,
-                                  uint32_t scale, cudaStream_t stream) {
+extern "C" mont_status_t mont_ntt_ex(const mont_ctx_t *ctx, uint32_t *data, size_t batch, int log_n,
+                                     const uint32_t *tw, uint32_t scale, int variant, cudaStream_t stream) {
     if (!ctx_ok(ctx)) return ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
     if (log_n < 1 || log_n > 15) return MONT_EUNSUPPORTED;
     if (batch == 0) return MONT_OK;
     if (!data || !tw || ((uintptr_t)data & 3u) || ((uintptr_t)tw & 3u) || scale >= ctx->p) return MONT_EINVAL_ARG;
-    if (batch > 0x7fffffffu) return MONT_EUNSUPPORTED;
+    if (batch > 0x7fffffffu || variant < 0 || variant > 2) return variant < 0 || variant > 2 ? MONT_EINVAL_ARG
+                                                                                             : MONT_EUNSUPPORTED;
     const uint32_t N = 1u << log_n;
-    switch (log_n) {
-        case 5: return launch_ntt_r32<5>(to_dev(ctx), data, batch, tw, scale, stream);
-        case 6: return launch_ntt_r32<6>(to_dev(ctx), data, batch, tw, scale, stream);
-        case 7: return launch_ntt_r32<7>(to_dev(ctx), data, batch, tw, scale, stream);
-        case 8: return launch_ntt_r32<8>(to_dev(ctx), data, batch, tw, scale, stream);
-        case 9: return launch_ntt_r32<9>(to_dev(ctx), data, batch, tw, scale, stream);
-        case 10: return launch_ntt_r32<10>(to_dev(ctx), data, batch, tw, scale, stream);
-        case 11: return launch_ntt_r32<11>(to_dev(ctx), data, batch, tw, scale, stream);
-        case 12: return launch_ntt_r32<12>(to_dev(ctx), data, batch, tw, scale, stream);
-        case 13: return launch_ntt_r32<13>(to_dev(ctx), data, batch, tw, scale, stream);
-        case 14: return launch_ntt_r32<14>(to_dev(ctx), data, batch, tw, scale, stream);
-        case 15: return launch_ntt_r32<15>(to_dev(ctx), data, batch, tw, scale, stream);
-        default: break;
-    }
+    if (log_n >= 5 && variant != 2)
+        return ntt_rows(to_dev(ctx), data, batch, log_n, tw, scale, stream, Tw2D{nullptr, nullptr, 0, 0, 0, 0},
+                        variant == 0);
     int threads = (int)(N / 2 < 1024 ? N / 2 : 1024);
     if (threads < 32) threads = 32;
     const size_t smem = (size_t)N * 4;
@@ -343,4 +427,9 @@ extern "C" mont_status_t mont_ntt(const mont_ctx_t *ctx, uint32_t *data, size_t 
         return MONT_ECUDA;
     k_ntt_smem<<<(unsigned)batch, threads, smem, stream>>>(to_dev(ctx), data, log_n, tw, scale);
     return launch_status();
+}
+
+extern "C" mont_status_t mont_ntt(const mont_ctx_t *ctx, uint32_t *data, size_t batch, int log_n, const uint32_t *tw,
+                                  uint32_t scale, cudaStream_t stream) {
+    return mont_ntt_ex(ctx, data, batch, log_n, tw, scale, 0, stream);
 }

@@ -195,10 +195,12 @@ if args.what in ("ntt",):
         d = torch.empty(batch * N, dtype=torch.uint32, device=dev)
         m.synth_fill(d, 42, 5, 0, P)
         d = d.view(batch, N)
-        med, best = timeit(lambda: m.ntt(ctx, d, tw), reps=10)
-        redc = batch * (N // 2) * log_n
-        out(what="ntt", log_n=log_n, batch=batch, us=med * 1e6, gbs=8 * batch * N / med / 1e9,
-            tredc=redc / med / 1e12, frac_imad_floor=redc / med / (148 * 64 / 5 * 1.965e9))
+        for variant in (0, 1):
+            med, best = timeit(lambda: m.ntt(ctx, d, tw, variant=variant), reps=10)
+            redc = batch * (N // 2) * log_n
+            out(what="ntt", variant=("dif", "dit")[variant], log_n=log_n, batch=batch, us=med * 1e6,
+                gbs=8 * batch * N / med / 1e9, tredc=redc / med / 1e12,
+                frac_imad_floor=redc / med / (148 * 64 / 5 * 1.965e9))
 
 if args.what in ("barrett",):
     import numpy as np

@@ -29,28 +29,30 @@ def tables(m, P, N):
 
 @pytest.mark.parametrize("P", list(GEN))
 @pytest.mark.parametrize("log_n", [1, 2, 3, 5, 6, 8, 10, 11, 12])
-def test_ntt_vs_dft(m, P, log_n):
+@pytest.mark.parametrize("variant", [None, 1, 2])
+def test_ntt_vs_dft(m, P, log_n, variant):
     N = 1 << log_n
     batch = 3
     ctx, w, winv, tw, twi, ninv_m = tables(m, P, N)
     x = synth.uniform(42, 21, P, 0, batch * N).reshape(batch, N)
     x[0, :2] = [0, P - 1]
     d = torch.from_numpy(x).cuda()
-    m.ntt(ctx, d, tw)
+    m.ntt(ctx, d, tw, variant=variant)
     X = d.cpu().numpy()
     assert np.array_equal(X, oracle.dft(P, w, x))
-    m.ntt(ctx, d, twi, scale=ninv_m)
+    m.ntt(ctx, d, twi, scale=ninv_m, variant=variant)
     assert np.array_equal(d.cpu().numpy(), x)
 
 
 @pytest.mark.parametrize("log_n", [13, 14, 15])
-def test_ntt_large_properties(m, log_n):
+@pytest.mark.parametrize("variant", [None, 1])
+def test_ntt_large_properties(m, log_n, variant):
     P = 998244353
     N = 1 << log_n
     ctx, w, winv, tw, twi, ninv_m = tables(m, P, N)
     x = synth.uniform(42, 22, P, 0, 2 * N).reshape(2, N)
     d = torch.from_numpy(x).cuda()
-    m.ntt(ctx, d, tw)
+    m.ntt(ctx, d, tw, variant=variant)
     X = d.cpu().numpy()
     xs = [int(v) for v in x[1]]
     for k in (0, 1, 2, N // 2, N - 1, 12345 % N):
@@ -60,7 +62,7 @@ def test_ntt_large_properties(m, log_n):
             acc = (acc + v * pw) % P
             pw = pw * wk % P
         assert int(X[1, k]) == acc
-    m.ntt(ctx, d, twi, scale=ninv_m)
+    m.ntt(ctx, d, twi, scale=ninv_m, variant=variant)
     assert np.array_equal(d.cpu().numpy(), x)
 
 
