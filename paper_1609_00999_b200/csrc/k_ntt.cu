@@ -198,7 +198,9 @@ __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
                 const uint32_t w = __ldg(twb + ((uint32_t)(k0 & ((1 << lb) - 1)) << wlo));
                 const uint32_t a = v[k0], d = v[k1];
                 v[k0] = mod_add(a, d, c.p);
-                v[k1] = redc(mod_sub(a, d, c.p), w, c.p, c.pinv);
+                // REDC needs only (a - d) w < 2^32 P, so a - d + P in (0, 2P) goes in unreduced:
+                // the subtraction's correction is folded into the multiply
+                v[k1] = redc(a - d + c.p, w, c.p, c.pinv);
             }
         }
 #pragma unroll
