@@ -46,6 +46,7 @@ KIND = {  # ncu kernel name prefix -> bench.py kernel label prefix
     "k_pow": "mont_pow_vec",
     "k_sum": "mont_checksum",
     "k_ntt_r32": "mont_ntt",
+    "k_ntt_dif": "mont_ntt",
 }
 
 

@@ -15,5 +15,5 @@ for K in k_map2 k_pow k_twiddle k_map1; do
   echo "ncu full ${K} rc=$?"
 done
 CMD2="python bench.py --workload ntt --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --soak 0"
-$CMD2 > $OUT/plain_ntt.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"^k_ntt_r32" -s 3 -c 1 -o $OUT/prof_k_ntt_r32 $CMD2 > $OUT/ncu_k_ntt.log 2>&1
+$CMD2 > $OUT/plain_ntt.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"^k_ntt_dif" -s 3 -c 1 -o $OUT/prof_k_ntt_dif $CMD2 > $OUT/ncu_k_ntt.log 2>&1
 echo "ncu full k_ntt rc=$?"
