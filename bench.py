@@ -742,7 +742,7 @@ def main():
                       "frac": round(gbs / hbm_peak, 4), "bytes_per_launch": nbytes})
         else:
             # integer-multiply (FMAHeavy) pipe: the measured REDC floor is 5 FMAHeavy issue
-            # slots per product (DESIGN.md §5/§6) -> 64/5 products per clk per SM.
+            # slots per product -> 64/5 products per clk per SM.
             sms = torch.cuda.get_device_properties(0).multi_processor_count
             clk = (clocks.get("sm_mhz") or sm_max) * 1e6
             peak = sms * 64 / 5 * clk / 1e12

@@ -5,14 +5,16 @@
 //   K6 mont_checksum *acc += sum x[i]                 4 B/elem  (A11)
 // plus the triad/copy microbenchmarks that share K1's launch shape.
 //
-// B200 design (DESIGN.md §5): the paper vectorises REDC across the 4 lanes of
+// B200 design (DESIGN.md §6): the paper vectorises REDC across the 4 lanes of
 // a 128-bit SSE register (§3.2, :125).  Here each thread owns whole
 // 128-bit chunks (4 residues = one uint4), loaded with LDG.E.128 on the
-// non-coherent path and stored evict-first; a CTA moves a contiguous tile of
-// U * threads chunks per trip and tiles are dealt round-robin to a persistent
-// grid of SMs * k CTAs.  All U loads of a trip are issued before any
-// arithmetic (memory-level parallelism), the REDC math is ~7 integer
-// instructions per residue and hides under the HBM stream.
+// non-coherent path and stored evict-first.  Default shape: a flat grid, one
+// tile of threads * U chunks per CTA (the block scheduler balances fast and
+// slow SMs); variant 1 deals tiles round-robin to a persistent grid of
+// SMs * k CTAs, variant 2 stages each CTA's tiles with cp.async.bulk (TMA).
+// All U loads of a tile are issued before any arithmetic (memory-level
+// parallelism); the REDC is 5 FMAHeavy issue slots + 2 ALU ops per residue and
+// hides under the HBM stream (~25 % FMAHeavy at full bandwidth).
 #include <cuda_runtime.h>
 #include <stdint.h>
 

@@ -5,7 +5,7 @@
 // argues the residue-class conversion cost becomes negligible:
 // one to_mont, ~46 Montgomery products held in registers, one from_mont.
 // The kernel is bound by the integer-multiply (FMAHeavy) pipe, not HBM
-// (12 B per ~48 REDCs).  B200 design choices (DESIGN.md §5):
+// (12 B per ~48 REDCs).  B200 design choices (DESIGN.md §6):
 //   * signed lazy REDC (mont_core.cuh sredc): 3 FMAHeavy ops per product
 //     (IMAD.WIDE, IMAD, IMAD.WIDE), values stay in (-P, P) with no correction
 //     inside the chain;

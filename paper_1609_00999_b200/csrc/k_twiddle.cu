@@ -2,16 +2,18 @@
 // (BASELINE configs[2]: batch 4096 x len 2^14, the
 // twiddle multiply of one NTT stage of the paper's modular FFTs).
 //
-// B200 design: the grid is 2-D, blockIdx.x = a column chunk of
-// the table (<= 16384 entries = 64 KiB by default), blockIdx.y = a contiguous
-// block of rows.  Each CTA stages its chunk of tw ONCE into shared memory with
-// the bulk-copy engine (cp.async.bulk global->shared, completion counted on an
-// mbarrier by transaction bytes -- the TMA path, SASS UBLKCP), then streams
-// its rows of x through registers with 128-bit non-coherent loads and
-// evict-first stores; the table operand comes from shared memory (LDS.128,
-// conflict-free: consecutive lanes read consecutive 16 B).  HBM traffic is the
-// 8 B/elem of x and out; the table costs gridDim.x*gridDim.y*64 KiB of L2
-// reads, ~0.1 % of the stream at configs[2].
+// B200 design, three table paths, all measured:
+//  * variant 2 (default for power-of-two rows): the batch as one flat 128-bit
+//    stream, table quads read through the read-only path where the 64 KiB
+//    table stays L1-resident per SM;
+//  * variant 0 (other row lengths): a 2-D grid, blockIdx.x = a column chunk of
+//    the table, blockIdx.y = a block of rows; each CTA stages its chunk ONCE
+//    into shared memory with the bulk-copy engine (cp.async.bulk, completion
+//    counted on an mbarrier by transaction bytes -- the TMA path, SASS UBLKCP)
+//    and reads it with conflict-free LDS.128;
+//  * variant 3: the whole table staged once per CTA lifetime plus cluster
+//    launch control work stealing.
+// HBM traffic is the 8 B/elem of x and out in every case.
 #include <cuda_runtime.h>
 #include <stdint.h>
 

@@ -2,7 +2,7 @@
 
 This module holds NO Montgomery / modular-multiplication arithmetic: it only
 turns (seed, stream, element index) into uint32 residues, exponents and the
-edge-value injections that DESIGN.md §3 ("input recipe") fixes.  Both the
+edge-value injections that DESIGN.md §5 ("input recipe") fixes.  Both the
 oracle tests and the product bench draw their host inputs from here; the CUDA
 library carries its own implementation of the same counter-based function
 (`synth_*` in csrc/synth.cu), cross-checked against this one in
@@ -21,7 +21,7 @@ and the value maps
 
 The paper fixes no input distribution (§3.1 works over "word-size
 primes", arbitrary residues), so uniform residues with the edge values
-0, 1, P-1 injected stand in for the paper's operands (DESIGN.md §3).
+0, 1, P-1 injected stand in for the paper's operands (DESIGN.md §5).
 """
 from __future__ import annotations
 
