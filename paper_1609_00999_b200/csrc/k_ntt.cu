@@ -195,12 +195,19 @@ __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
             for (int q = 0; q < 16; ++q) {
                 const int k0 = ((q >> lb) << (lb + 1)) | (q & ((1 << lb) - 1));
                 const int k1 = k0 | (1 << lb);
-                const uint32_t w = __ldg(twb + ((uint32_t)(k0 & ((1 << lb) - 1)) << wlo));
+                const uint32_t j = (uint32_t)(k0 & ((1 << lb) - 1));
                 const uint32_t a = v[k0], d = v[k1];
                 v[k0] = mod_add(a, d, c.p);
-                // REDC needs only (a - d) w < 2^32 P, so a - d + P in (0, 2P) goes in unreduced:
-                // the subtraction's correction is folded into the multiply
-                v[k1] = redc(a - d + c.p, w, c.p, c.pinv);
+                if (wlo == 0 && j == 0) {
+                    // pos = 0 (tl is empty when wlo = 0): the twiddle is w^0 = 1, so the product is
+                    // skipped (a compile-time decision; 30 of the last trip's 64 butterflies at 2^14)
+                    v[k1] = mod_sub(a, d, c.p);
+                } else {
+                    const uint32_t w = __ldg(twb + (j << wlo));
+                    // REDC needs only (a - d) w < 2^32 P, so a - d + P in (0, 2P) goes in unreduced:
+                    // the subtraction's correction is folded into the multiply
+                    v[k1] = redc(a - d + c.p, w, c.p, c.pinv);
+                }
             }
         }
 #pragma unroll
