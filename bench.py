@@ -473,15 +473,14 @@ def time_e2e(wl: Workload, steps: int):
             acc = torch.zeros(1, dtype=torch.int64, pin_memory=True)
             jobs.append(m.host_job("mul_vec", wl.ctx[P], hc, ha, hb, acc=acc))
             keep += [ha, hb, hc, acc]
-    tail_jobs = []
-    if hasattr(wl, "abar"):
-        # to_mont first, from_mont (which reads to_mont's host result) last: the other jobs
-        # stream in between, hiding the dependency
-        a0 = wl.c2[P0][0]
-        h_in, h_bar, h_back = pin(a0), empty(a0), empty(a0)
-        jobs.insert(0, m.host_job("to_mont", wl.ctx[P0], h_bar, h_in))
-        tail_jobs.append(m.host_job("from_mont", wl.ctx[P0], h_back, h_bar, depends_on=0))
-        keep += [h_in, h_bar, h_back]
+            if P == P0 and hasattr(wl, "abar"):
+                # to_mont(a0) and from_mont(to_mont's result) right after the P0 product: the three
+                # jobs form one fusion group (a0 is uploaded once, abar comes back to the host but
+                # from_mont reads it on the device)
+                h_bar, h_back = empty(a), empty(a)
+                jobs.append(m.host_job("to_mont", wl.ctx[P0], h_bar, ha))
+                jobs.append(m.host_job("from_mont", wl.ctx[P0], h_back, h_bar))
+                keep += [h_bar, h_back]
     if hasattr(wl, "tw_x"):
         hx, htw, ho = pin(wl.tw_x), pin(wl.tw), empty(wl.tw_x)
         jobs.append(m.host_job("twiddle", wl.ctx[P0], ho, hx, htw))
@@ -505,12 +504,8 @@ def time_e2e(wl: Workload, steps: int):
         keep += [ha, hb, hc, acc]
     if hasattr(wl, "ntt_x"):
         return None  # NTT has no host-buffer form
-    jobs += tail_jobs
-    # bytes actually copied per step (the to_mont -> from_mont chain goes through host memory,
-    # so a0 is uploaded twice and abar crosses the link both ways)
-    wl.e2e_h2d = sum(j.n * (j.len or 1) * 4 * (2 if j.op in (0, 3) else 1) + (j.len * 4 if j.op == 4 else 0)
-                     for j in jobs)
-    wl.e2e_d2h = sum(j.n * (j.len or 1) * 4 + (8 if j.acc_host else 0) for j in jobs)
+    # bytes actually copied per step, as the library plans them (after fusion)
+    wl.e2e_h2d, wl.e2e_d2h = m.host_run_bytes(jobs)
     ws = m.host_workspace("twiddle", TW_LEN, min_bytes=512 << 20)
     cur = torch.cuda.current_stream()
     m.host_run(jobs, ws)

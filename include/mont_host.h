@@ -68,13 +68,25 @@ mont_status_t mont_mul_twiddle_host(const mont_ctx_t *ctx, uint32_t *out_host, c
  * one H2D stream, one compute stream and one D2H stream, so the host->device
  * direction stays busy from the first chunk to the last while results flow
  * back concurrently -- the step costs ~max(total bytes in, total bytes out) /
- * PCIe bandwidth.  Jobs are independent unless `depends_on` >= 0: then the
- * job's first input copy waits until job `depends_on` (an earlier index) has
- * all its outputs in host memory (e.g. from_mont of the host result of
- * to_mont) -- put independent jobs in between to hide the wait.
+ * PCIe bandwidth.
+ *
+ * Fusion: consecutive elementwise jobs (MUL_VEC, TO_MONT, FROM_MONT, POW_VEC)
+ * with the same n form one group when each later job reads a host buffer of the
+ * group (an input of an earlier job, or an earlier job's output) and writes
+ * none of them.  A group streams chunk by chunk: each distinct host input is
+ * uploaded once per chunk, a job reading an earlier group job's output takes
+ * that device chunk (no trip through host memory), and every job's output is
+ * downloaded.  Results are those of running the jobs one after another.
+ *
+ * Dependencies: jobs in different groups are independent unless `depends_on`
+ * >= 0: then the job's group starts its input copies only after job
+ * `depends_on` (an earlier index) has all its outputs in host memory -- needed
+ * when a job reads a host buffer an earlier job of ANOTHER group writes; put
+ * independent jobs in between to hide the wait.  Inside a group it is implied.
  * Workspace: 16-byte aligned; it holds the twiddle tables and checksum
- * accumulators of the jobs plus 4 slots of 3 chunk buffers; the chunk size is
- * derived from what is left (MONT_EINVAL_ARG if that is < one row / 256 words). */
+ * accumulators of the jobs plus 4 slots of max(3, group inputs + outputs)
+ * chunk buffers; the chunk size is derived from what is left (MONT_EINVAL_ARG
+ * if that is < one row / 256 words). */
 typedef struct mont_host_job {
     int op;                        /* mont_host_op_t                                       */
     const mont_ctx_t *ctx;
@@ -89,6 +101,12 @@ typedef struct mont_host_job {
 
 mont_status_t mont_host_run(const mont_host_job_t *jobs, int njobs, void *ws, size_t ws_bytes,
                             cudaStream_t stream);
+
+/* Host<->device bytes one mont_host_run(jobs, njobs, ...) copies (after fusion):
+ * *h2d_bytes = uploaded inputs + twiddle tables, *d2h_bytes = outputs + 8 per
+ * checksum.  Validates like mont_host_run; host only, no CUDA call. */
+mont_status_t mont_host_run_bytes(const mont_host_job_t *jobs, int njobs, unsigned long long *h2d_bytes,
+                                  unsigned long long *d2h_bytes);
 
 #ifdef __cplusplus
 }

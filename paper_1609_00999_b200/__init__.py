@@ -116,6 +116,8 @@ class HostJob(C.Structure):
 
 
 SIGNATURES["mont_host_run"] = (C.c_int, [C.POINTER(HostJob), C.c_int, _P, _S, _P])
+SIGNATURES["mont_host_run_bytes"] = (C.c_int, [C.POINTER(HostJob), C.c_int, C.POINTER(C.c_ulonglong),
+                                               C.POINTER(C.c_ulonglong)])
 
 
 def lib():
@@ -481,6 +483,14 @@ def host_run(jobs, ws, stream=None):
     """Stream all jobs' chunks through one H2D / kernel / D2H ring (mont_host_run)."""
     arr = (HostJob * len(jobs))(*jobs)
     _check(lib().mont_host_run(arr, len(jobs), _ptr(ws), ws.numel(), _stream_handle(stream)), "mont_host_run")
+
+
+def host_run_bytes(jobs):
+    """(h2d_bytes, d2h_bytes) that host_run(jobs, ...) copies, after fusion (mont_host_run_bytes)."""
+    arr = (HostJob * len(jobs))(*jobs)
+    h2d, d2h = C.c_ulonglong(0), C.c_ulonglong(0)
+    _check(lib().mont_host_run_bytes(arr, len(jobs), C.byref(h2d), C.byref(d2h)), "mont_host_run_bytes")
+    return int(h2d.value), int(d2h.value)
 
 
 def sm_count() -> int:

@@ -279,14 +279,40 @@ struct Ring {
 }  // namespace
 }  // namespace mont
 
-extern "C" mont_status_t mont_host_run(const mont_host_job_t *jobs, int njobs, void *ws, size_t ws_bytes,
-                                       cudaStream_t stream) {
-    if (njobs < 0 || (njobs > 0 && !jobs) || (njobs > 0 && (!ws || ((uintptr_t)ws & 15u)))) return MONT_EINVAL_ARG;
-    if (njobs == 0) return MONT_OK;
+namespace mont {
+namespace {
+
+// A fusion group: consecutive elementwise jobs over the same n that share host
+// buffers.  Each distinct host input is uploaded once per chunk; a job whose
+// input is an earlier group job's output reads that job's device chunk (no
+// round trip through host memory); every job's output is downloaded.
+constexpr int kMaxBufs = 16;
+struct Group {
+    int j0 = 0, j1 = 0;                    // jobs [j0, j1)
+    int nbuf_in = 0;                       // distinct uploaded inputs: buffers [0, nbuf_in)
+    const uint32_t *in_host[kMaxBufs];     // their host pointers
+    int src[64][2];                        // per job input k: buffer index
+    int dst[64];                           // per job: output buffer index
+    int nbuf = 0;                          // inputs + outputs
+};
+
+bool elementwise(int op) { return op == MONT_HOST_MUL_VEC || op == MONT_HOST_TO_MONT || op == MONT_HOST_FROM_MONT ||
+                                  op == MONT_HOST_POW_VEC; }
+
+}  // namespace
+}  // namespace mont
+
+namespace mont {
+namespace {
+
+// Validates the jobs and plans the run: per-job units and reserved workspace
+// (twiddle tables, checksum accumulators; ws may be null when only counting),
+// then the fusion groups.
+mont_status_t plan_run(const mont_host_job_t *jobs, int njobs, void *ws, JobPlan *plan, Group *groups, int &ng,
+                       size_t &reserved) {
     // plan: reserved area (tables, accumulators), then the ring
-    JobPlan plan[64];
     if (njobs > 64) return MONT_EUNSUPPORTED;
-    size_t reserved = 0;
+    reserved = 0;
     for (int j = 0; j < njobs; ++j) {
         const mont_host_job_t &J = jobs[j];
         if (!ctx_ok(J.ctx)) return J.ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
@@ -314,10 +340,80 @@ extern "C" mont_status_t mont_host_run(const mont_host_job_t *jobs, int njobs, v
             reserved += kAlign;
         }
     }
-    if (ws_bytes < reserved + kRing * 3 * kAlign) return MONT_EINVAL_ARG;
-    const size_t buf_bytes = ((ws_bytes - reserved) / (kRing * 3)) / kAlign * kAlign;
+    // fusion groups (see Group): job j joins the group of job j-1 when both are elementwise over
+    // the same n, j reads at least one buffer of the group (an input, or an output it then takes
+    // from the device), and j's output aliases no buffer of the group
+    ng = 0;
+    for (int j = 0; j < njobs; ++j) {
+        const mont_host_job_t &J = jobs[j];
+        const uint32_t *ins[2] = {J.in0, plan[j].nin == 2 ? J.in1 : nullptr};
+        bool join = false;
+        if (ng > 0 && elementwise(J.op)) {
+            Group &G = groups[ng - 1];
+            const mont_host_job_t &F = jobs[G.j0];
+            if (elementwise(F.op) && F.n == J.n && G.nbuf + 3 <= kMaxBufs) {
+                bool shares = false, clash = false;
+                for (int q = G.j0; q < j; ++q) {
+                    const mont_host_job_t &Q = jobs[q];
+                    const uint32_t *qb[3] = {Q.in0, plan[q].nin == 2 ? Q.in1 : nullptr, Q.out};
+                    for (int k = 0; k < 2; ++k)
+                        for (int b = 0; b < 3; ++b) shares |= ins[k] && ins[k] == qb[b];
+                    for (int b = 0; b < 3; ++b) clash |= qb[b] && (const uint32_t *)J.out == qb[b];
+                }
+                join = shares && !clash;
+            }
+        }
+        if (!join) {
+            Group &G = groups[ng++];
+            G.j0 = j;
+            G.nbuf_in = 0;
+            G.nbuf = 0;
+        }
+        Group &G = groups[ng - 1];
+        G.j1 = j + 1;
+        for (int k = 0; k < 2; ++k) {
+            G.src[j - G.j0][k] = -1;
+            if (!ins[k]) continue;
+            for (int q = G.j0; q < j && G.src[j - G.j0][k] < 0; ++q)  // an earlier job's output?
+                if ((const uint32_t *)jobs[q].out == ins[k]) G.src[j - G.j0][k] = G.dst[q - G.j0];
+            for (int b = 0; b < G.nbuf_in && G.src[j - G.j0][k] < 0; ++b)  // an input already uploaded?
+                if (G.in_host[b] == ins[k]) G.src[j - G.j0][k] = b;
+            if (G.src[j - G.j0][k] < 0) {  // a new uploaded input: inputs come first, so shift outputs
+                for (int q = G.j0; q < j; ++q) {
+                    ++G.dst[q - G.j0];
+                    for (int kk = 0; kk < 2; ++kk)
+                        if (G.src[q - G.j0][kk] >= G.nbuf_in) ++G.src[q - G.j0][kk];
+                }
+                if (k == 1 && G.src[j - G.j0][0] >= G.nbuf_in) ++G.src[j - G.j0][0];
+                G.in_host[G.nbuf_in] = ins[k];
+                G.src[j - G.j0][k] = G.nbuf_in++;
+                ++G.nbuf;
+            }
+        }
+        G.dst[j - G.j0] = G.nbuf++;
+    }
+    return MONT_OK;
+}
+
+}  // namespace
+}  // namespace mont
+
+extern "C" mont_status_t mont_host_run(const mont_host_job_t *jobs, int njobs, void *ws, size_t ws_bytes,
+                                       cudaStream_t stream) {
+    if (njobs < 0 || (njobs > 0 && !jobs) || (njobs > 0 && (!ws || ((uintptr_t)ws & 15u)))) return MONT_EINVAL_ARG;
+    if (njobs == 0) return MONT_OK;
+    static thread_local JobPlan plan[64];
+    static thread_local Group groups[64];
+    int ng = 0;
+    size_t reserved = 0;
+    const mont_status_t pst = plan_run(jobs, njobs, ws, plan, groups, ng, reserved);
+    if (pst != MONT_OK) return pst;
+    int kb = 3;
+    for (int gi = 0; gi < ng; ++gi) kb = groups[gi].nbuf > kb ? groups[gi].nbuf : kb;
+    if (ws_bytes < reserved + (size_t)kRing * kb * kAlign) return MONT_EINVAL_ARG;
+    const size_t buf_bytes = ((ws_bytes - reserved) / ((size_t)kRing * kb)) / kAlign * kAlign;
     char *ring = (char *)ws + reserved;
-    auto slot_buf = [&](int slot, int k) { return (uint32_t *)(ring + ((size_t)slot * 3 + k) * buf_bytes); };
+    auto slot_buf = [&](int slot, int k) { return (uint32_t *)(ring + ((size_t)slot * kb + k) * buf_bytes); };
     for (int j = 0; j < njobs; ++j) {
         plan[j].chunk = buf_bytes / (plan[j].unit_words * 4);
         if (plan[j].chunk == 0 && jobs[j].n) return MONT_EINVAL_ARG;
@@ -342,52 +438,92 @@ extern "C" mont_status_t mont_host_run(const mont_host_job_t *jobs, int njobs, v
         if (plan[j].dacc && cudaMemsetAsync(plan[j].dacc, 0, 8, R.krn) != cudaSuccess) return MONT_ECUDA;
     }
     size_t g = 0;  // global chunk counter -> ring slot
-    for (int j = 0; j < njobs; ++j) {
-        const mont_host_job_t &J = jobs[j];
-        const JobPlan &P = plan[j];
-        if (J.depends_on >= 0) cudaStreamWaitEvent(R.h2d, R.job_out[J.depends_on], 0);
+    int slot_out0[kRing];  // per slot: first output buffer of the chunk that used it last
+    for (int gi = 0; gi < ng; ++gi) {
+        const Group &G = groups[gi];
+        const JobPlan &P = plan[G.j0];  // all jobs of a group share n, unit size and chunk
+        for (int j = G.j0; j < G.j1; ++j) {  // dependencies on earlier groups' host outputs
+            const int d = jobs[j].depends_on;
+            if (d >= 0 && d < G.j0) cudaStreamWaitEvent(R.h2d, R.job_out[d], 0);
+        }
         for (size_t u0 = 0; u0 < P.units; u0 += P.chunk, ++g) {
             const int slot = (int)(g % kRing);
             const size_t nu = P.units - u0 < P.chunk ? P.units - u0 : P.chunk;
             const size_t off = u0 * P.unit_words, bytes = nu * P.unit_words * 4;
-            if (g >= (size_t)kRing) cudaStreamWaitEvent(R.h2d, R.k_done[slot], 0);
-            uint32_t *d0 = slot_buf(slot, 0), *d1 = slot_buf(slot, 1), *dout = slot_buf(slot, 2);
-            if (cudaMemcpyAsync(d0, J.in0 + off, bytes, cudaMemcpyHostToDevice, R.h2d) != cudaSuccess)
-                return MONT_ECUDA;
-            if (P.nin == 2 &&
-                cudaMemcpyAsync(d1, J.in1 + off, bytes, cudaMemcpyHostToDevice, R.h2d) != cudaSuccess)
-                return MONT_ECUDA;
+            // the slot's previous chunk must be done with the buffers this upload overwrites: its
+            // kernels, and also its downloads when some of them were outputs there (a group with
+            // more inputs than the one before it)
+            if (g >= (size_t)kRing)
+                cudaStreamWaitEvent(R.h2d, G.nbuf_in > slot_out0[slot] ? R.d2h_done[slot] : R.k_done[slot], 0);
+            slot_out0[slot] = G.nbuf_in;
+            for (int b = 0; b < G.nbuf_in; ++b)
+                if (cudaMemcpyAsync(slot_buf(slot, b), G.in_host[b] + off, bytes, cudaMemcpyHostToDevice, R.h2d) !=
+                    cudaSuccess)
+                    return MONT_ECUDA;
             cudaEventRecord(R.h2d_done[slot], R.h2d);
             cudaStreamWaitEvent(R.krn, R.h2d_done[slot], 0);
             if (g >= (size_t)kRing) cudaStreamWaitEvent(R.krn, R.d2h_done[slot], 0);
-            mont_status_t st;
-            switch (J.op) {
-                case MONT_HOST_MUL_VEC:
-                    st = P.dacc ? mont_mul_vec_checksum(J.ctx, dout, d0, d1, nu, P.dacc, R.krn)
-                                : mont_mul_vec(J.ctx, dout, d0, d1, nu, R.krn);
-                    break;
-                case MONT_HOST_POW_VEC: st = mont_pow_vec(J.ctx, dout, d0, d1, nu, R.krn); break;
-                case MONT_HOST_TO_MONT: st = to_mont(J.ctx, dout, d0, nu, R.krn); break;
-                case MONT_HOST_FROM_MONT: st = from_mont(J.ctx, dout, d0, nu, R.krn); break;
-                default: st = mont_mul_twiddle(J.ctx, dout, d0, P.dtab, nu, J.len, R.krn); break;
+            for (int j = G.j0; j < G.j1; ++j) {
+                const mont_host_job_t &J = jobs[j];
+                const JobPlan &Pj = plan[j];
+                uint32_t *d0 = slot_buf(slot, G.src[j - G.j0][0]);
+                uint32_t *d1 = Pj.nin == 2 ? slot_buf(slot, G.src[j - G.j0][1]) : nullptr;
+                uint32_t *dout = slot_buf(slot, G.dst[j - G.j0]);
+                mont_status_t st;
+                switch (J.op) {
+                    case MONT_HOST_MUL_VEC:
+                        st = Pj.dacc ? mont_mul_vec_checksum(J.ctx, dout, d0, d1, nu, Pj.dacc, R.krn)
+                                     : mont_mul_vec(J.ctx, dout, d0, d1, nu, R.krn);
+                        break;
+                    case MONT_HOST_POW_VEC: st = mont_pow_vec(J.ctx, dout, d0, d1, nu, R.krn); break;
+                    case MONT_HOST_TO_MONT: st = to_mont(J.ctx, dout, d0, nu, R.krn); break;
+                    case MONT_HOST_FROM_MONT: st = from_mont(J.ctx, dout, d0, nu, R.krn); break;
+                    default: st = mont_mul_twiddle(J.ctx, dout, d0, Pj.dtab, nu, J.len, R.krn); break;
+                }
+                if (st != MONT_OK) return st;
             }
-            if (st != MONT_OK) return st;
             cudaEventRecord(R.k_done[slot], R.krn);
             cudaStreamWaitEvent(R.d2h, R.k_done[slot], 0);
-            if (cudaMemcpyAsync(J.out + off, dout, bytes, cudaMemcpyDeviceToHost, R.d2h) != cudaSuccess)
-                return MONT_ECUDA;
+            for (int j = G.j0; j < G.j1; ++j)
+                if (cudaMemcpyAsync(jobs[j].out + off, slot_buf(slot, G.dst[j - G.j0]), bytes, cudaMemcpyDeviceToHost,
+                                    R.d2h) != cudaSuccess)
+                    return MONT_ECUDA;
             cudaEventRecord(R.d2h_done[slot], R.d2h);
         }
-        if (P.dacc) {
-            cudaStreamWaitEvent(R.d2h, R.k_done[(g + kRing - 1) % kRing], 0);
-            if (cudaMemcpyAsync(J.acc_host, P.dacc, 8, cudaMemcpyDeviceToHost, R.d2h) != cudaSuccess)
-                return MONT_ECUDA;
+        for (int j = G.j0; j < G.j1; ++j) {
+            if (plan[j].dacc) {
+                cudaStreamWaitEvent(R.d2h, R.k_done[(g + kRing - 1) % kRing], 0);
+                if (cudaMemcpyAsync(jobs[j].acc_host, plan[j].dacc, 8, cudaMemcpyDeviceToHost, R.d2h) != cudaSuccess)
+                    return MONT_ECUDA;
+            }
         }
-        if (R.job_out[j]) cudaEventRecord(R.job_out[j], R.d2h);  // this job's outputs are in host memory
+        for (int j = G.j0; j < G.j1; ++j)
+            if (R.job_out[j]) cudaEventRecord(R.job_out[j], R.d2h);  // the group's outputs are in host memory
     }
     cudaEventRecord(R.done_k, R.krn);
     cudaEventRecord(R.done_d, R.d2h);
     cudaStreamWaitEvent(stream, R.done_k, 0);
     cudaStreamWaitEvent(stream, R.done_d, 0);
     return launch_status();
+}
+
+extern "C" mont_status_t mont_host_run_bytes(const mont_host_job_t *jobs, int njobs, unsigned long long *h2d_bytes,
+                                             unsigned long long *d2h_bytes) {
+    if (njobs < 0 || (njobs > 0 && !jobs) || !h2d_bytes || !d2h_bytes) return MONT_EINVAL_ARG;
+    *h2d_bytes = *d2h_bytes = 0;
+    if (njobs == 0) return MONT_OK;
+    static thread_local JobPlan plan[64];
+    static thread_local Group groups[64];
+    int ng = 0;
+    size_t reserved = 0;
+    const mont_status_t st = plan_run(jobs, njobs, nullptr, plan, groups, ng, reserved);
+    if (st != MONT_OK) return st;
+    for (int j = 0; j < njobs; ++j) {
+        const size_t bytes = plan[j].units * plan[j].unit_words * 4;
+        if (jobs[j].op == MONT_HOST_TWIDDLE) *h2d_bytes += jobs[j].len * 4;  // the table, once
+        *d2h_bytes += bytes + (jobs[j].op == MONT_HOST_MUL_VEC && jobs[j].acc_host ? 8 : 0);
+    }
+    for (int gi = 0; gi < ng; ++gi)
+        *h2d_bytes += (unsigned long long)groups[gi].nbuf_in * plan[groups[gi].j0].units * plan[groups[gi].j0].unit_words * 4;
+    return MONT_OK;
 }

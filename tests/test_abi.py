@@ -109,3 +109,32 @@ def test_validation_without_launch():
     assert L.mont_mul_vec_ex(pc, 0x1000, 0x2000, 0x3000, 8, C.byref(cfg), None) == 2
     assert L.synth_fill(None, 4, 1, 1, 0, 17, 0, 0, None) == 2
     assert L.synth_fill(0x1000, 4, 1, 1, 0, 17, 7, 0, None) == 2
+
+
+def test_host_run_bytes_fusion_plan():
+    """mont_host_run_bytes (host only): the executor's fusion plan, as bytes copied.
+    mul_vec(a, b) -> to_mont(a) -> from_mont(to_mont's out) is one group: a and b go up once each,
+    all three outputs come back; an unrelated job, a different n, or a job writing a buffer the
+    group already uses starts a new group."""
+    import torch
+    ctx = m.ctx_init(2013265921)
+    n = 1000
+    u = lambda k=n: torch.zeros(k, dtype=torch.uint32)
+    a, b, c, t, f, x, y = u(), u(), u(), u(), u(), u(), u()
+    acc = torch.zeros(1, dtype=torch.int64)
+    jobs = [m.host_job("mul_vec", ctx, c, a, b, acc=acc), m.host_job("to_mont", ctx, t, a),
+            m.host_job("from_mont", ctx, f, t)]
+    assert m.host_run_bytes(jobs) == (2 * 4 * n, 3 * 4 * n + 8)
+    # an unrelated job over the same n: its own group (its input is uploaded)
+    assert m.host_run_bytes(jobs + [m.host_job("to_mont", ctx, y, x)]) == (3 * 4 * n, 4 * 4 * n + 8)
+    # writing a buffer the group reads: not fused, so a is uploaded again for it
+    assert m.host_run_bytes(jobs + [m.host_job("to_mont", ctx, a, a)]) == (3 * 4 * n, 4 * 4 * n + 8)
+    # a different n never fuses: the half-length from_mont uploads its input
+    h = u(n // 2)
+    assert m.host_run_bytes(jobs[:1] + [m.host_job("from_mont", ctx, h, u(n // 2))]) == (2 * 4 * n + 2 * n,
+                                                                                         4 * n + 2 * n + 8)
+    # twiddle: table once + rows; never fused
+    tx, to, tw = torch.zeros((3, 64), dtype=torch.uint32), torch.zeros((3, 64), dtype=torch.uint32), u(64)
+    assert m.host_run_bytes([m.host_job("twiddle", ctx, to, tx, tw)]) == (3 * 64 * 4 + 64 * 4, 3 * 64 * 4)
+    with pytest.raises(m.MontError):
+        m.host_run_bytes([m.host_job("from_mont", ctx, f, t, depends_on=0)])  # depends on itself

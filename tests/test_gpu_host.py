@@ -137,3 +137,34 @@ def test_host_run_many_jobs(m):
         assert np.array_equal(o5.numpy(), oracle.power(P1_, base, e))
         assert np.array_equal(o6.numpy(), oracle.twiddle(P, x, tw))
         assert np.array_equal(o7.numpy(), a)
+
+def test_host_run_fused_group(m):
+    """Jobs over the same n that share host buffers form one fusion group: a shared input is
+    uploaded once per chunk and an output consumed by a later job is read from the device; every
+    output still lands in host memory.  Also an in-place host job, which must not join."""
+    P = 2013265921
+    ctx = m.ctx_init(P)
+    n = (1 << 20) + 5
+    a, b = synth.c2_inputs(P, 0, n)
+    ha, hb = host(a), host(b)
+    o1, o3, o4, o8 = empty(n), empty(n), empty(n), empty(n)
+    acc = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+    hip = host(b)  # in-place target
+    jobs = [m.host_job("mul_vec", ctx, o1, ha, hb, acc=acc),
+            m.host_job("to_mont", ctx, o3, ha),
+            m.host_job("from_mont", ctx, o4, o3),
+            m.host_job("mul_vec", ctx, o8, o4, hb),
+            m.host_job("to_mont", ctx, hip, hip)]
+    ref1 = oracle.mont_mul(P, a, b)
+    for ws_mb in (1, 7, 64):
+        for o in (o1, o3, o4, o8):
+            o.zero_()
+        hip.copy_(torch.from_numpy(b))
+        acc.zero_()
+        m.host_run(jobs, m.host_workspace("mul_vec", 0, min_bytes=ws_mb << 20))
+        torch.cuda.synchronize()
+        assert np.array_equal(o1.numpy(), ref1) and int(acc.item()) == oracle.raw_sum(ref1)
+        assert np.array_equal(o3.numpy(), oracle.to_mont(P, a))
+        assert np.array_equal(o4.numpy(), a)
+        assert np.array_equal(o8.numpy(), ref1)
+        assert np.array_equal(hip.numpy(), oracle.to_mont(P, b))
