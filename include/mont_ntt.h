@@ -39,7 +39,12 @@ mont_status_t mont_ntt(const mont_ctx_t *ctx, uint32_t *data, size_t batch, int 
 /* mont_ntt with an explicit kernel: variant 0 = decimation in frequency (the
  * default: natural-order input read straight into registers, bit reversal in
  * the final shared-memory gather), 1 = decimation in time (bit-reversed load),
- * 2 = one butterfly per thread per stage in shared memory (reference). */
+ * 2 = one butterfly per thread per stage in shared memory (reference),
+ * 3 = variant 0 with precomputed-quotient twiddle products: `tw` is then the
+ * PAIR table of mont_ntt_twiddles_pq (8-byte aligned, else MONT_EINVAL_ARG;
+ * log_n >= 5, else MONT_EUNSUPPORTED) and each butterfly computes
+ * x w mod P as x w - hi(x w') P (Shoup), one high product instead of REDC's
+ * two.  All variants give identical outputs. */
 mont_status_t mont_ntt_ex(const mont_ctx_t *ctx, uint32_t *data, size_t batch, int log_n, const uint32_t *tw,
                           uint32_t scale, int variant, cudaStream_t stream);
 
@@ -47,6 +52,14 @@ mont_status_t mont_ntt_ex(const mont_ctx_t *ctx, uint32_t *data, size_t batch, i
  * pos < 2^(s-1): N - 1 entries (device pointer), each an independent
  * square-and-multiply on the GPU.  1 <= log_n <= 30. */
 mont_status_t mont_ntt_twiddles(const mont_ctx_t *ctx, uint32_t *tw, uint32_t w, int log_n, cudaStream_t stream);
+
+/* Pair table for mont_ntt_ex variant 3: for each entry e of the table above
+ * (same index e, same exponent), tw2[2e] = w^x mod P (plain, canonical) and
+ * tw2[2e + 1] = floor(w^x 2^32 / P) -- which equals to_mont(w^x) * P' mod 2^32,
+ * so it comes from the Montgomery context with one multiply.  2 (N - 1) words,
+ * device pointer, 8-byte aligned.  1 <= log_n <= 30. */
+mont_status_t mont_ntt_twiddles_pq(const mont_ctx_t *ctx, uint32_t *tw2, uint32_t w, int log_n,
+                                   cudaStream_t stream);
 
 /* ---- large transforms, 2^16 <= N <= 2^30 (six-step) ----
  * N = N1 N2 with N1 = 2^floor(log_n/2), N2 = 2^ceil(log_n/2) (both <= 2^15):

@@ -87,6 +87,7 @@ SIGNATURES = {
 
 SIGNATURES["mont_ntt"] = (C.c_int, [_CTX, _P, _S, C.c_int, _P, C.c_uint32, _P])
 SIGNATURES["mont_ntt_twiddles"] = (C.c_int, [_CTX, _P, C.c_uint32, C.c_int, _P])
+SIGNATURES["mont_ntt_twiddles_pq"] = (C.c_int, [_CTX, _P, C.c_uint32, C.c_int, _P])
 SIGNATURES["mont_ntt_ex"] = (C.c_int, [_CTX, _P, _S, C.c_int, _P, C.c_uint32, C.c_int, _P])
 SIGNATURES["mont_dot"] = (C.c_int, [_CTX, _P, _P, _P, _S, _S, _P])
 SIGNATURES["mont_ntt_plan_words"] = (C.c_size_t, [C.c_int])
@@ -380,6 +381,15 @@ def ntt_twiddles(ctx: Ctx, w: int, log_n: int, device="cuda", stream=None):
     tw = torch.empty((1 << log_n) - 1, dtype=torch.uint32, device=device)
     _check(lib().mont_ntt_twiddles(C.byref(ctx), _ptr(tw), w, log_n, _stream_handle(stream)), "mont_ntt_twiddles")
     return tw
+
+
+def ntt_twiddles_pq(ctx: Ctx, w: int, log_n: int, device="cuda", stream=None):
+    """Pair table (plain w^x, floor(w^x 2^32 / P)) x (N - 1) for mont_ntt_ex variant 3."""
+    torch = _torch()
+    tw2 = torch.empty(2 * ((1 << log_n) - 1), dtype=torch.uint32, device=device)
+    _check(lib().mont_ntt_twiddles_pq(C.byref(ctx), _ptr(tw2), w, log_n, _stream_handle(stream)),
+           "mont_ntt_twiddles_pq")
+    return tw2
 
 
 def ntt(ctx: Ctx, data, tw, scale: int | None = None, stream=None, variant: int | None = None):

@@ -157,7 +157,12 @@ __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
 // bit-reversed result is unscrambled by the final shared-memory gather -- one
 // shared-memory pass fewer than the DIT kernel above.  Butterfly:
 // (u, v) -> (u + v, (u - v) w^pos), stages from pair distance N/2 down to 1.
-template <int LOG_N>
+// PQ = true (mont_ntt_ex variant 3): tw is the pair table of mont_ntt_twiddles_pq and each
+// butterfly multiplies by the precomputed-quotient (Shoup) product: q = hi(x w'), x w - q P in
+// [0, 2P) from LOW words only -- one high product instead of REDC's two (4 FMAHeavy issue slots
+// instead of 5, one ALU op fewer); w' = floor(w 2^32 / P) is the Montgomery form of w times P'
+// mod 2^32.
+template <int LOG_N, bool PQ = false>
 __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
     k_ntt_dif(Ctx c, uint32_t *data, size_t batch, const uint32_t *__restrict__ tw, uint32_t scale, Tw2D t2) {
     constexpr uint32_t N = 1u << LOG_N, T = N >> 5;
@@ -202,6 +207,12 @@ __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
                     // pos = 0 (tl is empty when wlo = 0): the twiddle is w^0 = 1, so the product is
                     // skipped (a compile-time decision; 30 of the last trip's 64 butterflies at 2^14)
                     v[k1] = mod_sub(a, d, c.p);
+                } else if (PQ) {
+                    const uint2 wq = __ldg(reinterpret_cast<const uint2 *>(tw) + ((1u << b) - 1u) + tl + (j << wlo));
+                    const uint32_t x = a - d + c.p;           // (0, 2P): any x < 2^32 is allowed
+                    const uint32_t q = __umulhi(x, wq.y);     // floor(x w' / 2^32)
+                    const uint32_t r = x * wq.x - q * c.p;    // x w - q P in [0, 2P), exact mod 2^32
+                    v[k1] = umin(r, r - c.p);
                 } else {
                     const uint32_t w = __ldg(twb + (j << wlo));
                     // REDC needs only (a - d) w < 2^32 P, so a - d + P in (0, 2P) goes in unreduced:
@@ -233,7 +244,7 @@ __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
     }
 }
 
-template <int LOG_N>
+template <int LOG_N, bool PQ = false>
 static mont_status_t launch_ntt_dif(const Ctx &c, uint32_t *data, size_t batch, const uint32_t *tw, uint32_t scale,
                                     cudaStream_t stream, Tw2D t2) {
     constexpr uint32_t N = 1u << LOG_N, T = N >> 5;
@@ -242,9 +253,9 @@ static mont_status_t launch_ntt_dif(const Ctx &c, uint32_t *data, size_t batch, 
     const size_t grid = (batch + rpc - 1) / rpc;
     if (grid > 0x7fffffffu) return MONT_EUNSUPPORTED;
     if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(k_ntt_dif<LOG_N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        cudaFuncSetAttribute(k_ntt_dif<LOG_N, PQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return MONT_ECUDA;
-    k_ntt_dif<LOG_N><<<(unsigned)grid, rpc * T, smem, stream>>>(c, data, batch, tw, scale, t2);
+    k_ntt_dif<LOG_N, PQ><<<(unsigned)grid, rpc * T, smem, stream>>>(c, data, batch, tw, scale, t2);
     return launch_status();
 }
 
@@ -280,6 +291,26 @@ __global__ void __launch_bounds__(256) k_ntt_twiddles(Ctx c, uint32_t *tw, uint3
     }
 }
 
+// pair table for variant 3: tw2[2e] = w^x (plain), tw2[2e + 1] = floor(w^x 2^32 / P) = to_mont(w^x) P'
+// mod 2^32, with e and x as in k_ntt_twiddles
+__global__ void __launch_bounds__(256) k_ntt_twiddles_pq(Ctx c, uint32_t *tw2, uint32_t w, int log_n) {
+    const size_t total = ((size_t)1 << log_n) - 1;
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        const int sm1 = 63 - __clzll((unsigned long long)(e + 1));
+        const size_t pos = e + 1 - ((size_t)1 << sm1);
+        const unsigned long long ex = (unsigned long long)pos << (log_n - 1 - sm1);
+        const uint32_t x = redc(w, c.r2, c.p, c.pinv);
+        uint32_t acc = c.r1;
+        for (int sh = 63 - __clzll(ex | 1ull); sh >= 0; --sh) {
+            acc = redc(acc, acc, c.p, c.pinv);
+            if ((ex >> sh) & 1ull) acc = redc(acc, x, c.p, c.pinv);
+        }
+        // acc = w^x 2^32 mod P (canonical): w^x 2^32 = q P + acc, so q = -acc P^-1 mod 2^32
+        tw2[2 * e] = redc1(acc, c.p, c.pinv);
+        tw2[2 * e + 1] = acc * (0u - c.pinv);
+    }
+}
+
 // tiled transpose of an R x C row-major uint32 matrix (32 x 32 tiles through
 // padded shared memory; coalesced 128-byte rows on both sides)
 __global__ void __launch_bounds__(256) k_transpose(uint32_t *dst, const uint32_t *src, size_t R, size_t C) {
@@ -308,11 +339,13 @@ static mont_status_t transpose(uint32_t *dst, const uint32_t *src, size_t R, siz
 
 #define MONT_NTT_CASE(L)                                                                           \
     case L:                                                                                        \
-        return dif ? launch_ntt_dif<L>(c, data, batch, tw, scale, s, t2)                          \
-                   : launch_ntt_r32<L>(c, data, batch, tw, scale, s, t2);
+        return kind == 0   ? launch_ntt_dif<L>(c, data, batch, tw, scale, s, t2)                  \
+               : kind == 3 ? launch_ntt_dif<L, true>(c, data, batch, tw, scale, s, t2)            \
+                           : launch_ntt_r32<L>(c, data, batch, tw, scale, s, t2);
 
+// kind: 0 = DIF (REDC twiddles), 1 = DIT, 3 = DIF with precomputed-quotient twiddles
 static mont_status_t ntt_rows(const Ctx &c, uint32_t *data, size_t batch, int log_n, const uint32_t *tw,
-                              uint32_t scale, cudaStream_t s, Tw2D t2, bool dif = true) {
+                              uint32_t scale, cudaStream_t s, Tw2D t2, int kind = 0) {
     switch (log_n) {
         MONT_NTT_CASE(5)
         MONT_NTT_CASE(6)
@@ -422,12 +455,14 @@ extern "C" mont_status_t mont_ntt_ex(const mont_ctx_t *ctx, uint32_t *data, size
     if (log_n < 1 || log_n > 15) return MONT_EUNSUPPORTED;
     if (batch == 0) return MONT_OK;
     if (!data || !tw || ((uintptr_t)data & 3u) || ((uintptr_t)tw & 3u) || scale >= ctx->p) return MONT_EINVAL_ARG;
-    if (batch > 0x7fffffffu || variant < 0 || variant > 2) return variant < 0 || variant > 2 ? MONT_EINVAL_ARG
+    if (batch > 0x7fffffffu || variant < 0 || variant > 3) return variant < 0 || variant > 3 ? MONT_EINVAL_ARG
                                                                                              : MONT_EUNSUPPORTED;
+    if (variant == 3 && ((uintptr_t)tw & 7u)) return MONT_EINVAL_ARG;  // pair table: 8-byte entries
     const uint32_t N = 1u << log_n;
+    if (variant == 3 && log_n < 5) return MONT_EUNSUPPORTED;
     if (log_n >= 5 && variant != 2)
         return ntt_rows(to_dev(ctx), data, batch, log_n, tw, scale, stream, Tw2D{nullptr, nullptr, 0, 0, 0, 0},
-                        variant == 0);
+                        variant);
     int threads = (int)(N / 2 < 1024 ? N / 2 : 1024);
     if (threads < 32) threads = 32;
     const size_t smem = (size_t)N * 4;
@@ -441,4 +476,18 @@ extern "C" mont_status_t mont_ntt_ex(const mont_ctx_t *ctx, uint32_t *data, size
 extern "C" mont_status_t mont_ntt(const mont_ctx_t *ctx, uint32_t *data, size_t batch, int log_n, const uint32_t *tw,
                                   uint32_t scale, cudaStream_t stream) {
     return mont_ntt_ex(ctx, data, batch, log_n, tw, scale, 0, stream);
+}
+
+extern "C" mont_status_t mont_ntt_twiddles_pq(const mont_ctx_t *ctx, uint32_t *tw2, uint32_t w, int log_n,
+                                              cudaStream_t stream) {
+    if (!ctx_ok(ctx)) return ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
+    if (log_n < 1 || log_n > 30) return MONT_EUNSUPPORTED;
+    if (!tw2 || ((uintptr_t)tw2 & 7u)) return MONT_EINVAL_ARG;
+    const int sms = sm_count();
+    if (sms <= 0) return MONT_ECUDA;
+    size_t grid = ((((size_t)1 << log_n) - 1) + 255) / 256;
+    if (grid > (size_t)sms * 8) grid = (size_t)sms * 8;
+    if (grid == 0) grid = 1;
+    k_ntt_twiddles_pq<<<(unsigned)grid, 256, 0, stream>>>(to_dev(ctx), tw2, w, log_n);
+    return launch_status();
 }

@@ -27,13 +27,21 @@ def tables(m, P, N):
     return ctx, w, winv, tw, twi, ninv_m
 
 
+def pq_tables(m, ctx, w, winv, log_n):
+    return m.ntt_twiddles_pq(ctx, w, log_n), m.ntt_twiddles_pq(ctx, winv, log_n)
+
+
 @pytest.mark.parametrize("P", list(GEN))
 @pytest.mark.parametrize("log_n", [1, 2, 3, 5, 6, 8, 10, 11, 12])
-@pytest.mark.parametrize("variant", [None, 1, 2])
+@pytest.mark.parametrize("variant", [None, 1, 2, 3])
 def test_ntt_vs_dft(m, P, log_n, variant):
     N = 1 << log_n
     batch = 3
     ctx, w, winv, tw, twi, ninv_m = tables(m, P, N)
+    if variant == 3:
+        if log_n < 5:
+            pytest.skip("variant 3 needs log_n >= 5")
+        tw, twi = pq_tables(m, ctx, w, winv, log_n)
     x = synth.uniform(42, 21, P, 0, batch * N).reshape(batch, N)
     x[0, :2] = [0, P - 1]
     d = torch.from_numpy(x).cuda()
@@ -45,11 +53,13 @@ def test_ntt_vs_dft(m, P, log_n, variant):
 
 
 @pytest.mark.parametrize("log_n", [13, 14, 15])
-@pytest.mark.parametrize("variant", [None, 1])
+@pytest.mark.parametrize("variant", [None, 1, 3])
 def test_ntt_large_properties(m, log_n, variant):
     P = 998244353
     N = 1 << log_n
     ctx, w, winv, tw, twi, ninv_m = tables(m, P, N)
+    if variant == 3:
+        tw, twi = pq_tables(m, ctx, w, winv, log_n)
     x = synth.uniform(42, 22, P, 0, 2 * N).reshape(2, N)
     d = torch.from_numpy(x).cuda()
     m.ntt(ctx, d, tw, variant=variant)
@@ -154,3 +164,32 @@ def test_ntt_large_matches_small_path(m):
     X = m.ntt_large(ctx, torch.from_numpy(e.copy()).cuda(), plan).cpu().numpy()
     for k in (0, 1, 2, 12345, N - 1):
         assert int(X[k]) == pow(w, k, P)
+
+
+@pytest.mark.parametrize("P", list(GEN))
+@pytest.mark.parametrize("log_n", [1, 5, 12])
+def test_ntt_twiddles_pq_layout(m, P, log_n):
+    """Pair table: entry e = (w^x, floor(w^x 2^32 / P)) with x the stage-major exponent, checked
+    with Python big integers (pow, //), independent of the library's Montgomery derivation."""
+    N = 1 << log_n
+    ctx = m.ctx_init(P)
+    w = oracle.root_of_unity(P, GEN[P], N)
+    tw2 = m.ntt_twiddles_pq(ctx, w, log_n).cpu().numpy().reshape(-1, 2)
+    for s_ in range(1, log_n + 1):
+        h = 1 << (s_ - 1)
+        for pos in range(h):
+            x = pow(w, pos * (N // (2 * h)), P)
+            assert int(tw2[h - 1 + pos, 0]) == x
+            assert int(tw2[h - 1 + pos, 1]) == (x << 32) // P
+
+
+def test_ntt_pq_rejects(m):
+    P = 2013265921
+    ctx, w, winv, tw, twi, ninv_m = tables(m, P, 64)
+    tw2 = m.ntt_twiddles_pq(ctx, w, 6)
+    d = torch.zeros((2, 64), dtype=torch.uint32, device="cuda")
+    with pytest.raises(m.MontError):
+        m.ntt(ctx, d, tw2[1:], variant=3)   # 4-byte aligned only
+    d4 = torch.zeros((2, 16), dtype=torch.uint32, device="cuda")
+    with pytest.raises(m.MontError):
+        m.ntt(ctx, d4, m.ntt_twiddles_pq(ctx, pow(w, 4, P), 4), variant=3)  # log_n < 5
