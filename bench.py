@@ -522,14 +522,14 @@ def time_e2e(wl: Workload, steps: int):
 
 # ----------------------------------------------------------- CPU baseline
 
-def cpu_baseline(kind: str, target_s: float = 1.5, nsteps: int = 1):
+def cpu_baseline(kind: str, target_s: float = 1.5, nsteps: int = 1, threads: int = 0):
     """The oracle (oracle/, plain naive-% definitions, all host cores) on a bounded
     sample of the same workload.  Returns (Gmulmod/s, cores, sample text, seconds)."""
     import numpy as np
 
     import oracle
     import synth
-    cores = os.cpu_count() or 1
+    cores = threads or os.cpu_count() or 1
     memo = {}
 
     def gen(fn, *a, **kw):  # inputs are generated once per sample size, outside the timed region
@@ -804,6 +804,10 @@ def main():
         v, cores, sample, secs, frac = cpu_baseline(wl.kind)
         line["cpu_baseline"] = {"value": float(f"{v:.4g}"), "unit": "Gmulmod/s", "cores": cores, "kind": "oracle",
                                 "sample": sample, "seconds": round(secs, 3)}
+        if cores > 1:  # the oracle on one thread too (a smaller sample)
+            v1, _, sample1, _, _ = cpu_baseline(wl.kind, target_s=1.0, threads=1)
+            line["cpu_baseline"]["single_thread"] = {"value": float(f"{v1:.4g}"), "unit": "Gmulmod/s",
+                                                     "sample": sample1}
     print(json.dumps(line), flush=True)
     if dist.is_initialized():
         dist.destroy_process_group()
