@@ -147,6 +147,24 @@ def test_c4_fullsize(m):
     assert np.array_equal(out.cpu().numpy()[idx], oracle.power(P1, hb, he))
 
 
+def test_c4_fullsize_lane_launch(m):
+    """configs[3] in the launch bench.py's two-lane step times (variant 10, 8 ladders per thread,
+    persistent grid of 2 CTAs per SM): sampled outputs against the oracle, and every element equal
+    to the default launch's."""
+    n = 1 << 24
+    ctx = m.ctx_init(P1)
+    base = gen(n, 3, P1, 1, m=m)
+    e = gen(n, 4, P1, 2, m=m)
+    out = m.pow_vec(ctx, base, e, cfg=m.Launch(ctas_per_sm=2, variant=10))
+    ref = m.pow_vec(ctx, base, e)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    idx = sample_idx(n, 20_000)
+    hb = synth.uniform_at(42, 3, P1, idx.astype(np.uint64), low=1)
+    he = synth.exponents_at(42, 4, idx.astype(np.uint64))
+    assert np.array_equal(out.cpu().numpy()[idx], oracle.power(P1, hb, he))
+
+
 def test_to_from_fullsize(m):
     n = 1 << 26
     a = gen(n, 1, P0, 0, True, m=m)
