@@ -744,7 +744,8 @@ def main():
         if bound == "hbm":
             gbs = nbytes / (t * 1e-3) / 1e9
             r.update({"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",
-                      "frac": round(gbs / hbm_peak, 4), "bytes_per_launch": nbytes})
+                      "frac": round(gbs / hbm_peak, 4), "bytes_per_launch": nbytes,
+                      "frac_nominal_8tbs": round(gbs / 8000.0, 4)})
         else:
             # integer-multiply (FMAHeavy) pipe: the measured REDC floor is 5 FMAHeavy issue
             # slots per product -> 64/5 products per clk per SM.
@@ -754,7 +755,10 @@ def main():
             ach = mm / (t * 1e-3) / 1e12
             r.update({"bound": "alu", "achieved": round(ach, 4), "peak": round(peak, 4), "unit": "Tmulmod/s",
                       "frac": round(ach / peak, 4),
-                      "peak_basis": f"{sms} SMs x 64 FMAHeavy lanes/clk / 5 issue slots per REDC x {clk/1e6:.0f} MHz"})
+                      "peak_basis": f"{sms} SMs x 64 FMAHeavy lanes/clk / 5 issue slots per REDC x {clk/1e6:.0f} MHz",
+                      # SURVEY §8(d)'s other denominator: 4 multiplies per REDC at the full IMAD rate
+                      # (IMAD.WIDE/IMAD.HI measured half rate on B200, so this one is not reachable)
+                      "frac_imad_div4": round(ach / (sms * 64 / 4 * clk / 1e12), 4)})
         r["traffic"] = ncu_traffic(name)
         rooflines.append(r)
     dom = max(range(len(per_ms)), key=lambda i: per_ms[i])
