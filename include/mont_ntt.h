@@ -61,14 +61,23 @@ mont_status_t mont_ntt_twiddles(const mont_ctx_t *ctx, uint32_t *tw, uint32_t w,
 mont_status_t mont_ntt_twiddles_pq(const mont_ctx_t *ctx, uint32_t *tw2, uint32_t w, int log_n,
                                    cudaStream_t stream);
 
-/* ---- large transforms, 2^16 <= N <= 2^30 (six-step) ----
- * N = N1 N2 with N1 = 2^floor(log_n/2), N2 = 2^ceil(log_n/2) (both <= 2^15):
- * transpose, N2 transforms of length N1 with the twiddle w^(n2 k1) applied in
- * their epilogue (the configs[2] "twiddle multiply of one NTT stage", here 2-D
- * and generated from two half tables), transpose, N1 transforms of length N2,
- * transpose to natural order.  HBM traffic 5 x 8 bytes per element.
+/* ---- large transforms, 2^16 <= N <= 2^30 ----
+ * N = N1 N2, x viewed as the N1 x N2 row-major matrix x[n1][n2].
+ * 2^22 <= N <= 2^27: three passes over HBM.  (1) N2 column transforms of
+ *   length N1 = 2^12 straight down the matrix (8 adjacent columns per CTA, so
+ *   every row access is one full 32-byte sector; no transpose), each output
+ *   (k1, n2) times the 2-D twiddle w^(n2 k1) (the configs[2] "twiddle multiply
+ *   of one NTT stage", generated from two half tables), in place; (2) N1 row
+ *   transforms of length N2 = N / 2^12; (3) one transpose to natural order.
+ *   Both transform passes multiply by their twiddles with precomputed
+ *   quotients (the pair tables of mont_ntt_twiddles_pq).  HBM traffic 3 x 8
+ *   bytes per element.
+ * otherwise: six-step -- N1 = 2^floor(log_n/2), N2 = 2^ceil(log_n/2): transpose,
+ *   N2 transforms of length N1 with the 2-D twiddle in their epilogue,
+ *   transpose, N1 transforms of length N2, transpose to natural order.  HBM
+ *   traffic 5 x 8 bytes per element.
  *
- * plan: device buffer of mont_ntt_plan_words(log_n) words, filled by
+ * plan: device buffer of mont_ntt_plan_words(log_n) words, 8-byte aligned, filled by
  *       mont_ntt_plan_init for a primitive N-th root w (w^-1: inverse).
  * in  : the N inputs (canonical); DESTROYED (used as scratch).
  * out : the N outputs, natural order; must not overlap `in`.

@@ -244,6 +244,120 @@ __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
     }
 }
 
+// ---- column-mode DIF transform: the first pass of the 3-pass large transform.
+// The data is an R x ld row-major matrix; CTA b transforms the C adjacent
+// columns [b C, b C + C), each a length-N = 2^LOG_N transform down the rows
+// (stride ld), in place, then multiplies element (k1, col) by the 2-D twiddle
+// w^(col k1) of the large transform (Tw2D).  Two thread->(column, t) maps:
+//   G (global phases: the trip-0 load, the final store): lanes span the C
+//     columns of 32/C consecutive rows, so every warp access is 32/C fully used
+//     segments of C*4 contiguous bytes (no transpose pass needed);
+//   S (the shared-memory trips): lanes span 32 consecutive t of one column, as
+//     in k_ntt_dif.
+// Column col keeps its N words at sm[col N + (swz(a) ^ (col << CSH))]: the XOR
+// moves the C columns of a G-mode warp access onto different banks (checked
+// exhaustively for every access pattern by scripts/ntt_col_banks.py).
+template <int LOG_N, int C, bool PQ>
+__global__ void __launch_bounds__(C * (1 << LOG_N) / 32, C * (1 << LOG_N) / 32 <= 512 ? 2 : 1)
+    k_ntt_col(Ctx c, uint32_t *data, size_t ld, const uint32_t *__restrict__ tw, Tw2D t2) {
+    constexpr uint32_t N = 1u << LOG_N, T = N >> 5;
+    constexpr int CSH = (C == 16) ? 1 : (C == 8) ? 2 : 3;  // log2(32 / C)
+    static_assert(C == 4 || C == 8 || C == 16, "C: 4, 8 or 16 columns per CTA");
+    constexpr int NTRIP = (LOG_N + 4) / 5;
+    extern __shared__ uint32_t sm[];
+    const size_t col0 = (size_t)blockIdx.x * C;
+    const uint32_t cg = threadIdx.x % C, tg = threadIdx.x / C;  // map G
+    const uint32_t cs = threadIdx.x / T, ts = threadIdx.x % T;  // map S
+    uint32_t v[32];
+#pragma unroll
+    for (int trip = 0; trip < NTRIP; ++trip) {
+        const uint32_t col = trip == 0 ? cg : cs, t = trip == 0 ? tg : ts;
+        uint32_t *s = sm + col * N;
+        const uint32_t fx = (col << CSH) & 31u;
+        const int top = LOG_N - 5 * trip;
+        const int wlo = top - 5 > 0 ? top - 5 : 0;
+        const uint32_t tl = t & ((1u << wlo) - 1u);
+        const uint32_t base = tl | ((t >> wlo) << (wlo + 5));
+        const uint32_t sb = swz(base) ^ fx;
+        if (trip == 0) {
+            // running pointer: one 64-bit add per load instead of 32 live 64-bit addresses
+            const uint32_t *g = data + col0 + col + (size_t)base * ld;
+            const size_t step = ld << wlo;
+#pragma unroll
+            for (int k = 0; k < 32; ++k, g += step) v[k] = ld_stream1(g);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) v[k] = s[sb ^ swz((uint32_t)k << wlo)];
+        }
+#pragma unroll
+        for (int lb = 4; lb >= 0; --lb) {
+            const int b = wlo + lb;
+            if (b >= top) continue;
+            const uint32_t *twb = tw + ((1u << b) - 1u) + tl;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int k0 = ((q >> lb) << (lb + 1)) | (q & ((1 << lb) - 1));
+                const int k1 = k0 | (1 << lb);
+                const uint32_t j = (uint32_t)(k0 & ((1 << lb) - 1));
+                const uint32_t a = v[k0], d = v[k1];
+                v[k0] = mod_add(a, d, c.p);
+                if (wlo == 0 && j == 0) {
+                    v[k1] = mod_sub(a, d, c.p);
+                } else if (PQ) {  // precomputed-quotient product, as in k_ntt_dif<.., true>
+                    const uint2 wq = __ldg(reinterpret_cast<const uint2 *>(tw) + ((1u << b) - 1u) + tl + (j << wlo));
+                    const uint32_t x = a - d + c.p;
+                    const uint32_t r = x * wq.x - __umulhi(x, wq.y) * c.p;
+                    v[k1] = umin(r, r - c.p);
+                } else {
+                    v[k1] = redc(a - d + c.p, __ldg(twb + (j << wlo)), c.p, c.pinv);
+                }
+            }
+        }
+        // each thread writes back exactly the 32 words it read this trip: no barrier before the store
+#pragma unroll
+        for (int k = 0; k < 32; ++k) s[sb ^ swz((uint32_t)k << wlo)] = v[k];
+        __syncthreads();
+    }
+    // final gather in map H: lanes span the C columns of 32/C rows as in map G, but those rows
+    // are T/(32/C) apart (t = j T/(32/C) + warp), so their bit-reversed positions differ in
+    // the bits the swizzle folds onto the low banks and the column XOR keeps all 32 lanes apart.
+    // X[idx] of column cg sits at the bit-reversed position.
+    {
+        constexpr uint32_t R = 32 / C;                 // rows per warp
+        const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+        const uint32_t ch = lane % C, th = (lane / C) * (T / R) + wid;
+        const uint32_t *s = sm + ch * N;
+        const uint32_t fx = (ch << CSH) & 31u;
+        const uint32_t bt = swz(__brev(th) >> (32 - LOG_N)) ^ fx;
+        const uint64_t colg = (uint64_t)(col0 + ch);
+        uint32_t *g = data + col0 + ch + (size_t)th * ld;
+        const size_t step = ld * T;
+        uint64_t e = (colg * th) & t2.mask;            // exponent col * idx, idx = th + k T
+        const uint64_t de = (colg * T) & t2.mask;
+#pragma unroll
+        for (int k = 0; k < 32; ++k, g += step, e = (e + de) & t2.mask) {
+            const uint32_t x = s[bt ^ swz(__brev((uint32_t)k * T) >> (32 - LOG_N))];
+            const uint32_t we = redc(__ldg(t2.hi + (e >> t2.shift)), __ldg(t2.lo + (e & t2.lomask)), c.p, c.pinv);
+            st_stream1(g, redc(x, we, c.p, c.pinv));
+        }
+    }
+}
+
+template <int LOG_N, int C, bool PQ>
+static mont_status_t launch_ntt_col(const Ctx &c, uint32_t *data, size_t ld, const uint32_t *tw, Tw2D t2,
+                                    cudaStream_t stream) {
+    constexpr uint32_t N = 1u << LOG_N;
+    const size_t smem = (size_t)C * N * 4;
+    if (ld % C) return MONT_EUNSUPPORTED;
+    const size_t grid = ld / C;
+    if (grid > 0x7fffffffu) return MONT_EUNSUPPORTED;
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(k_ntt_col<LOG_N, C, PQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return MONT_ECUDA;
+    k_ntt_col<LOG_N, C, PQ><<<(unsigned)grid, C * (N >> 5), smem, stream>>>(c, data, ld, tw, t2);
+    return launch_status();
+}
+
 template <int LOG_N, bool PQ = false>
 static mont_status_t launch_ntt_dif(const Ctx &c, uint32_t *data, size_t batch, const uint32_t *tw, uint32_t scale,
                                     cudaStream_t stream, Tw2D t2) {
@@ -363,9 +477,13 @@ static mont_status_t ntt_rows(const Ctx &c, uint32_t *data, size_t batch, int lo
 }
 #undef MONT_NTT_CASE
 
-// split of a large transform: N = N1 * N2, log N1 = a <= log N2 = b <= 15
+// split of a large transform: N = N1 * N2.  2^22..2^27: the 3-pass form (column pass over
+// N1 = 2^12 rows, 8 columns = one 32-byte sector per row per CTA, so N2 / 8 >= 128 CTAs; row pass
+// over N2 = 2^10..2^15; one transpose); otherwise the six-step form with N1 = 2^floor(log_n / 2)
+// (both <= 2^15).
+static bool ntt_three_pass(int log_n) { return log_n >= 22 && log_n <= 27; }
 static void ntt_split(int log_n, int &a, int &b, int &sh) {
-    a = log_n / 2;
+    a = ntt_three_pass(log_n) ? 12 : log_n / 2;
     b = log_n - a;
     sh = (log_n + 1) / 2;  // two-level table split of the exponent
 }
@@ -384,26 +502,46 @@ static uint32_t host_powmod(uint32_t x, uint64_t e, uint32_t p) {
 
 using namespace mont;
 
+// plan layout: [column table][row table][2-D low table 2^sh][2-D high table 2^(log_n - sh)];
+// the 3-pass form's column and row tables are pair tables (mont_ntt_twiddles_pq, 2 words per
+// entry, 8-byte aligned), the six-step form's Montgomery tables (1 word per entry)
+struct PlanLayout {
+    int a, b, sh;
+    bool pq;
+    size_t tw1, tw2, tlo, thi, words;
+};
+static PlanLayout plan_layout(int log_n) {
+    PlanLayout L;
+    ntt_split(log_n, L.a, L.b, L.sh);
+    L.pq = ntt_three_pass(log_n);
+    const size_t e = L.pq ? 2 : 1;
+    L.tw1 = 0;
+    L.tw2 = L.tw1 + e * (((size_t)1 << L.a) - 1);
+    L.tlo = L.tw2 + e * (((size_t)1 << L.b) - 1);
+    L.thi = L.tlo + ((size_t)1 << L.sh);
+    L.words = L.thi + ((size_t)1 << (log_n - L.sh));
+    return L;
+}
+
 extern "C" size_t mont_ntt_plan_words(int log_n) {
     if (log_n < 16 || log_n > 30) return 0;
-    int a, b, sh;
-    ntt_split(log_n, a, b, sh);
-    return ((size_t)1 << a) - 1 + ((size_t)1 << b) - 1 + ((size_t)1 << sh) + ((size_t)1 << (log_n - sh));
+    return plan_layout(log_n).words;
 }
 
 extern "C" mont_status_t mont_ntt_plan_init(const mont_ctx_t *ctx, uint32_t *plan, uint32_t w, int log_n,
                                             cudaStream_t stream) {
     if (!ctx_ok(ctx)) return ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
     if (log_n < 16 || log_n > 30) return MONT_EUNSUPPORTED;
-    if (!plan || ((uintptr_t)plan & 3u)) return MONT_EINVAL_ARG;
-    int a, b, sh;
-    ntt_split(log_n, a, b, sh);
+    if (!plan || ((uintptr_t)plan & 7u)) return MONT_EINVAL_ARG;
+    const PlanLayout L = plan_layout(log_n);
+    const int a = L.a, b = L.b, sh = L.sh;
     const uint32_t p = ctx->p;
-    uint32_t *tw1 = plan, *tw2 = tw1 + ((1u << a) - 1), *tlo = tw2 + ((1u << b) - 1), *thi = tlo + (1u << sh);
+    uint32_t *tw1 = plan + L.tw1, *tw2 = plan + L.tw2, *tlo = plan + L.tlo, *thi = plan + L.thi;
     mont_status_t st;
     // column transforms have length N1 = 2^a: root w^(N2); row transforms N2 = 2^b: root w^(N1)
-    if ((st = mont_ntt_twiddles(ctx, tw1, host_powmod(w, 1ull << b, p), a, stream)) != MONT_OK) return st;
-    if ((st = mont_ntt_twiddles(ctx, tw2, host_powmod(w, 1ull << a, p), b, stream)) != MONT_OK) return st;
+    auto table = L.pq ? mont_ntt_twiddles_pq : mont_ntt_twiddles;
+    if ((st = table(ctx, tw1, host_powmod(w, 1ull << b, p), a, stream)) != MONT_OK) return st;
+    if ((st = table(ctx, tw2, host_powmod(w, 1ull << a, p), b, stream)) != MONT_OK) return st;
     if ((st = mont_twiddle_table(ctx, tlo, w, (size_t)1 << sh, stream)) != MONT_OK) return st;
     return mont_twiddle_table(ctx, thi, host_powmod(w, 1ull << sh, p), (size_t)1 << (log_n - sh), stream);
 }
@@ -412,17 +550,26 @@ extern "C" mont_status_t mont_ntt_large(const mont_ctx_t *ctx, uint32_t *out, ui
                                         const uint32_t *plan, uint32_t scale, cudaStream_t stream) {
     if (!ctx_ok(ctx)) return ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
     if (log_n < 16 || log_n > 30) return MONT_EUNSUPPORTED;
-    if (!out || !in || !plan || out == in || (((uintptr_t)out | (uintptr_t)in | (uintptr_t)plan) & 3u) ||
+    if (!out || !in || !plan || out == in || (((uintptr_t)out | (uintptr_t)in) & 3u) || ((uintptr_t)plan & 7u) ||
         scale >= ctx->p)
         return MONT_EINVAL_ARG;
-    int a, b, sh;
-    ntt_split(log_n, a, b, sh);
+    const PlanLayout L = plan_layout(log_n);
+    const int a = L.a, b = L.b, sh = L.sh;
     const size_t N1 = (size_t)1 << a, N2 = (size_t)1 << b;
-    const uint32_t *tw1 = plan, *tw2 = tw1 + (N1 - 1), *tlo = tw2 + (N2 - 1), *thi = tlo + ((size_t)1 << sh);
+    const uint32_t *tw1 = plan + L.tw1, *tw2 = plan + L.tw2, *tlo = plan + L.tlo, *thi = plan + L.thi;
     const Ctx c = to_dev(ctx);
     const Tw2D none{nullptr, nullptr, 0, 0, 0, 0};
     const Tw2D t2{tlo, thi, ((uint64_t)1 << log_n) - 1, (1u << sh) - 1u, sh, 0};
     mont_status_t st;
+    if (ntt_three_pass(log_n)) {
+        // x as N1 x N2 [n1][n2]: N2 column transforms of length N1 down the rows, in place, each
+        // output (k1, n2) times w^(n2 k1) -> [k1][n2]; then N1 row transforms of length N2 with
+        // the output scale -> [k1][k2]; X[k1 + N1 k2] = [k1][k2]: one transpose to natural order
+        // (both passes multiply by the twiddles with precomputed quotients: pair tables)
+        if ((st = launch_ntt_col<12, 8, true>(c, in, N2, tw1, t2, stream)) != MONT_OK) return st;
+        if ((st = ntt_rows(c, in, N1, b, tw2, scale, stream, none, 3)) != MONT_OK) return st;
+        return transpose(out, in, N1, N2, stream);
+    }
     // x as N1 x N2 [n1][n2] -> out as N2 x N1 [n2][n1]
     if ((st = transpose(out, in, N1, N2, stream)) != MONT_OK) return st;
     // N2 column transforms of length N1, then the twiddle w^(n2 k1)

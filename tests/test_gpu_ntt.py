@@ -128,9 +128,12 @@ def test_ntt_twiddle_table_layout(m, log_n):
 
 
 @pytest.mark.parametrize("P", list(GEN))
-@pytest.mark.parametrize("log_n", [16, 17, 20, 23])
+@pytest.mark.parametrize("log_n", [16, 17, 20, 22, 23, 24, 26, 27])
 def test_ntt_large(m, P, log_n):
-    """Six-step transform: sampled outputs by definition (oracle.dft_at), inverse round trip."""
+    """Large transform (six-step for 2^16..2^21, 3-pass column/row/transpose for 2^22..2^27): sampled
+    outputs by definition (oracle.dft_at), inverse round trip."""
+    if (P - 1) % (1 << log_n):
+        pytest.skip("no primitive 2^log_n-th root of unity mod P")
     N = 1 << log_n
     ctx = m.ctx_init(P)
     w = oracle.root_of_unity(P, GEN[P], N)
