@@ -450,11 +450,10 @@ def time_steps(wl: Workload, K: int):
     end.record(s)
     end.synchronize()
     total_ms = start.elapsed_time(end)
-    per = [0.0] * nl
-    for k in range(K):
-        for i in range(nl):
-            per[i] += evs[k][i].elapsed_time(evs[k][i + 1])
-    return total_ms, [p / K for p in per]
+    # per launch: the median over the K steps (one late host enqueue inflates a single
+    # event interval with GPU idle time; the step total above is unaffected by the choice)
+    per = [statistics.median(evs[k][i].elapsed_time(evs[k][i + 1]) for k in range(K)) for i in range(nl)]
+    return total_ms, per
 
 
 def time_e2e(wl: Workload, steps: int):
