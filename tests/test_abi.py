@@ -136,5 +136,7 @@ def test_host_run_bytes_fusion_plan():
     # twiddle: table once + rows; never fused
     tx, to, tw = torch.zeros((3, 64), dtype=torch.uint32), torch.zeros((3, 64), dtype=torch.uint32), u(64)
     assert m.host_run_bytes([m.host_job("twiddle", ctx, to, tx, tw)]) == (3 * 64 * 4 + 64 * 4, 3 * 64 * 4)
+    # the same host buffer as both operands (a squaring) is uploaded once
+    assert m.host_run_bytes([m.host_job("mul_vec", ctx, c, a, a)]) == (4 * n, 4 * n)
     with pytest.raises(m.MontError):
         m.host_run_bytes([m.host_job("from_mont", ctx, f, t, depends_on=0)])  # depends on itself

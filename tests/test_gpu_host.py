@@ -147,17 +147,18 @@ def test_host_run_fused_group(m):
     n = (1 << 20) + 5
     a, b = synth.c2_inputs(P, 0, n)
     ha, hb = host(a), host(b)
-    o1, o3, o4, o8 = empty(n), empty(n), empty(n), empty(n)
+    o1, o3, o4, o8, o9 = empty(n), empty(n), empty(n), empty(n), empty(n)
     acc = torch.zeros(1, dtype=torch.int64, pin_memory=True)
     hip = host(b)  # in-place target
     jobs = [m.host_job("mul_vec", ctx, o1, ha, hb, acc=acc),
             m.host_job("to_mont", ctx, o3, ha),
             m.host_job("from_mont", ctx, o4, o3),
             m.host_job("mul_vec", ctx, o8, o4, hb),
-            m.host_job("to_mont", ctx, hip, hip)]
+            m.host_job("to_mont", ctx, hip, hip),
+            m.host_job("mul_vec", ctx, o9, ha, ha)]       # both operands one host buffer
     ref1 = oracle.mont_mul(P, a, b)
     for ws_mb in (1, 7, 64):
-        for o in (o1, o3, o4, o8):
+        for o in (o1, o3, o4, o8, o9):
             o.zero_()
         hip.copy_(torch.from_numpy(b))
         acc.zero_()
@@ -168,3 +169,4 @@ def test_host_run_fused_group(m):
         assert np.array_equal(o4.numpy(), a)
         assert np.array_equal(o8.numpy(), ref1)
         assert np.array_equal(hip.numpy(), oracle.to_mont(P, b))
+        assert np.array_equal(o9.numpy(), oracle.mont_mul(P, a, a))
