@@ -24,7 +24,17 @@ extern "C" {
  *                 from_mont_ex, mb_triad, mb_copy : 0 = flat grid (one
  *                                   tile of threads*unroll uint4 per CTA),
  *                                   1 = persistent grid-stride over tiles
- *                                   with grid = SMs * ctas_per_sm
+ *                                   with grid = SMs * ctas_per_sm,
+ *                                   2 = flat grid, each CTA's tile staged by
+ *                                   cp.async.bulk (chunk words per operand,
+ *                                   default 8192),
+ *                                   3 = persistent bulk-copy pipeline: grid =
+ *                                   SMs * ctas_per_sm, a 4-stage TMA load
+ *                                   ring + TMA stores of chunk-word tiles
+ *                                   (default 2048), threads <= 256, so few
+ *                                   warps stream at full bandwidth
+ *                                   (variants 2 and 3: 16-byte co-aligned
+ *                                   operands, else the 32-bit path)
  *                 mont_pow_vec_ex : 0 = 2-bit fixed window, table in
  *                                   registers; 1 = binary ladder with
  *                                   selects; 2 = 3-bit window, registers;

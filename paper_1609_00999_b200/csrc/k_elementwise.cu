@@ -168,6 +168,82 @@ __global__ void __launch_bounds__(256) k_map2_tma(Op op, uint32_t *c, const uint
     if (SUM) block_sum_to(acc, s);
 }
 
+// Persistent bulk-copy pipeline (variant 3): one or two CTAs per SM stream
+// tiles through an S-stage shared-memory ring.  Thread 0 keeps S tile loads in
+// flight with cp.async.bulk (each stage completes on its own mbarrier by
+// transaction bytes) and writes each result tile back with a bulk store from
+// one of two output buffers; the other threads only compute (LDS.128, REDC,
+// STS.128).  Memory-level parallelism comes from the copy engine, not from
+// resident warps, so the kernel streams with 4-8 warps per SM and leaves the
+// SM's remaining warp slots and issue cycles to a co-running compute kernel
+// (the pow ladder in bench.py's two-lane step).  Tile t goes to CTA
+// t mod gridDim.x; one __syncthreads per tile.
+template <int NIN, int S, class Op, bool SUM>
+__global__ void __launch_bounds__(256) k_map_pipe(Op op, uint32_t *c, const uint32_t *a, const uint32_t *b,
+                                                   uint32_t head, size_t n4, uint32_t tail, unsigned long long *acc,
+                                                   uint32_t tile4) {
+    extern __shared__ __align__(128) uint4 sm[];
+    __shared__ __align__(8) uint64_t full[S];
+    uint4 *sin = sm;                          // [S][NIN][tile4]
+    uint4 *sout = sm + (size_t)S * NIN * tile4;  // [2][tile4]
+    const uint4 *a4 = reinterpret_cast<const uint4 *>(a + head);
+    const uint4 *b4 = reinterpret_cast<const uint4 *>((NIN == 2 ? b : a) + head);
+    uint4 *c4 = reinterpret_cast<uint4 *>(c + head);
+    const size_t ntiles = (n4 + tile4 - 1) / tile4;
+    auto load = [&](size_t t, int st) {
+        const uint32_t cnt = (uint32_t)(n4 - t * tile4 < tile4 ? n4 - t * tile4 : tile4);
+        mbar_expect_tx(&full[st], cnt * 16u * NIN);
+        bulk_g2s(sin + (size_t)st * NIN * tile4, a4 + t * tile4, cnt * 16u, &full[st]);
+        if (NIN == 2) bulk_g2s(sin + ((size_t)st * NIN + 1) * tile4, b4 + t * tile4, cnt * 16u, &full[st]);
+    };
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < S; ++st) mbar_init(&full[st], 1);
+        fence_mbar_init();
+        for (int st = 0; st < S; ++st) {
+            const size_t t = blockIdx.x + (size_t)st * gridDim.x;
+            if (t < ntiles) load(t, st);
+        }
+    }
+    unsigned long long s = 0;
+    if (blockIdx.x == 0 && threadIdx.x < head + tail) {
+        const size_t i = threadIdx.x < head ? threadIdx.x : head + 4 * n4 + (threadIdx.x - head);
+        uint32_t r;
+        if constexpr (NIN == 2) r = op(a[i], b[i]);
+        else r = op(a[i]);
+        c[i] = r;
+        s += r;
+    }
+    __syncthreads();
+    uint32_t it = 0;
+    for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int st = (int)(it % S);
+        const uint32_t cnt = (uint32_t)(n4 - t * tile4 < tile4 ? n4 - t * tile4 : tile4);
+        mbar_wait(&full[st], (it / S) & 1u);
+        const uint4 *ia = sin + (size_t)st * NIN * tile4, *ib = ia + tile4;
+        uint4 *ob = sout + (size_t)(it & 1u) * tile4;
+        for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+            uint4 r;
+            if constexpr (NIN == 2) r = apply4(op, ia[i], ib[i]);
+            else r = apply4(op, ia[i]);
+            ob[i] = r;
+            if (SUM) s += sum4(r);
+        }
+        fence_proxy_async_smem();
+        // thread 0: the store issued last iteration (from the other output buffer) must have
+        // finished reading it before anyone writes that buffer next iteration
+        if (threadIdx.x == 0) bulk_wait_read0();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            bulk_s2g(c4 + t * tile4, ob, cnt * 16u);
+            bulk_commit();
+            const size_t tn = t + (size_t)S * gridDim.x;  // refill this stage: everyone has read it
+            if (tn < ntiles) load(tn, st);
+        }
+    }
+    if (threadIdx.x == 0) bulk_wait0();  // the last stores read shared memory: finish before exit
+    if (SUM) block_sum_to(acc, s);
+}
+
 // 32-bit path for operands that do not share an address mod 16
 template <int U, class Op, bool SUM>
 __global__ void __launch_bounds__(512) k_map2_scalar(Op op, uint32_t *c, const uint32_t *a, const uint32_t *b,
@@ -268,6 +344,25 @@ static mont_status_t launch_map2(const Op &op, uint32_t *c, const uint32_t *a, c
     if (sms <= 0) return MONT_ECUDA;
     const uintptr_t pa = (uintptr_t)a, pb = (uintptr_t)b, pc = (uintptr_t)c;
     const bool flat = L.variant == 0;
+    if (L.variant == 3 && same_mod16(pa, pb) && same_mod16(pa, pc)) {  // persistent bulk-copy pipeline
+        const uint32_t head = head_elems(pa, n);
+        const size_t n4 = (n - head) / 4;
+        const uint32_t tail = (uint32_t)((n - head) % 4);
+        const uint32_t tile4 = (uint32_t)((L.chunk > 0 ? L.chunk : 2048) / 4);
+        constexpr int S = 4;
+        const size_t smem = ((size_t)S * 2 + 2) * tile4 * 16;
+        if (tile4 == 0 || smem > 227 * 1024 || L.threads > 256) return MONT_EINVAL_ARG;
+        const size_t ntiles = (n4 + tile4 - 1) / tile4;
+        size_t grid = (size_t)sms * (L.ctas_per_sm > 0 ? L.ctas_per_sm : 1);
+        if (grid > ntiles) grid = ntiles;
+        if (grid == 0) grid = 1;
+        // (always set: the static mbarriers come on top of the dynamic size)
+        if (cudaFuncSetAttribute(k_map_pipe<2, S, Op, SUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+            return MONT_ECUDA;
+        k_map_pipe<2, S, Op, SUM><<<(unsigned)grid, L.threads, smem, s>>>(op, c, a, b, head, n4, tail, acc, tile4);
+        return launch_status();
+    }
     if (L.variant == 2 && same_mod16(pa, pb) && same_mod16(pa, pc)) {  // bulk-copy (TMA) staged tiles
         const uint32_t head = head_elems(pa, n);
         const size_t n4 = (n - head) / 4;
@@ -322,6 +417,25 @@ static mont_status_t launch_map1(const Op &op, uint32_t *out, const uint32_t *in
     const int sms = sm_count();
     if (sms <= 0) return MONT_ECUDA;
     const uintptr_t pi = (uintptr_t)in, po = (uintptr_t)out;
+    if (L.variant == 3 && same_mod16(pi, po)) {  // persistent bulk-copy pipeline
+        const uint32_t head = head_elems(pi, n);
+        const size_t n4 = (n - head) / 4;
+        const uint32_t tail = (uint32_t)((n - head) % 4);
+        const uint32_t tile4 = (uint32_t)((L.chunk > 0 ? L.chunk : 2048) / 4);
+        constexpr int S = 4;
+        const size_t smem = ((size_t)S + 2) * tile4 * 16;
+        if (tile4 == 0 || smem > 227 * 1024 || L.threads > 256) return MONT_EINVAL_ARG;
+        const size_t ntiles = (n4 + tile4 - 1) / tile4;
+        size_t grid = (size_t)sms * (L.ctas_per_sm > 0 ? L.ctas_per_sm : 1);
+        if (grid > ntiles) grid = ntiles;
+        if (grid == 0) grid = 1;
+        if (cudaFuncSetAttribute(k_map_pipe<1, S, Op, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess)
+            return MONT_ECUDA;
+        k_map_pipe<1, S, Op, false><<<(unsigned)grid, L.threads, smem, s>>>(op, out, in, nullptr, head, n4, tail,
+                                                                            nullptr, tile4);
+        return launch_status();
+    }
     if (same_mod16(pi, po)) {
         const uint32_t head = head_elems(pi, n);
         const size_t n4 = (n - head) / 4;

@@ -40,6 +40,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
     } while (!done);
 }
 
+// shared -> global bulk copy (TMA store path, SASS UBLKCP), tracked by bulk groups
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// all committed bulk stores have finished READING their shared-memory source
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// all committed bulk stores are complete (writes performed)
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// order this thread's generic-proxy shared-memory writes before later async-proxy reads (bulk store)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // ---- cluster launch control (sm_100): hardware work stealing.  A running CTA
 // asks the scheduler to cancel a not-yet-launched CTA of the same grid and, on
 // success, processes that CTA's work itself -- a persistent kernel with dynamic

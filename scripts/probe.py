@@ -346,3 +346,30 @@ if args.what in ("tw2",):
     cfg = m.Launch(threads=512, unroll=2)
     med, _ = timeit(lambda: m.to_mont(ctx, x.view(-1), out=o.view(-1), cfg=cfg))
     out(what="to_mont 512x2", us=med * 1e6, gbs=8 * batch * L / med / 1e9)
+
+if args.what in ("pipe",):
+    # variant 3 (persistent bulk-copy pipeline) vs the flat default, standalone
+    P = 2013265921
+    ctx = m.ctx_init(P)
+    n = 1 << 26
+    a = torch.empty(n, dtype=torch.uint32, device=dev)
+    b = torch.empty(n, dtype=torch.uint32, device=dev)
+    m.synth_fill(a, 42, 1, 0, P)
+    m.synth_fill(b, 42, 2, 0, P)
+    c = torch.empty_like(a)
+    acc = torch.zeros(1, dtype=torch.int64, device=dev)
+    cfgs = [None] + [m.Launch(threads=t, ctas_per_sm=k, unroll=1, variant=3, chunk=ch)
+                     for t in (128, 256) for k in (1, 2) for ch in (1024, 2048, 4096)]
+    for cfg in cfgs:
+        try:
+            med, best = timeit(lambda: m.mul_vec_checksum(ctx, a, b, out=c, acc=acc, cfg=cfg))
+        except Exception as ex:  # noqa: BLE001
+            out(what="pipe_mulvec", cfg=str(cfg and (cfg.threads, cfg.ctas_per_sm, cfg.chunk)), err=str(ex))
+            continue
+        out(what="pipe_mulvec", cfg=None if cfg is None else (cfg.threads, cfg.ctas_per_sm, cfg.chunk),
+            us=med * 1e6, gbs=12 * n / med / 1e9)
+    for cfg in [None] + [m.Launch(threads=t, ctas_per_sm=k, unroll=1, variant=3, chunk=ch)
+                         for t in (128, 256) for k in (1, 2) for ch in (2048, 4096)]:
+        med, best = timeit(lambda: m.to_mont(ctx, a, out=c, cfg=cfg))
+        out(what="pipe_tomont", cfg=None if cfg is None else (cfg.threads, cfg.ctas_per_sm, cfg.chunk),
+            us=med * 1e6, gbs=8 * n / med / 1e9)

@@ -97,7 +97,7 @@ def test_mul_vec_one_operand_noncanonical(m):
 
 @pytest.mark.parametrize("oa,ob,oc", [(1, 1, 1), (2, 2, 2), (3, 3, 3), (0, 1, 2), (1, 0, 0), (3, 0, 1), (0, 0, 3)])
 @pytest.mark.parametrize("n", [0, 1, 2, 3, 5, 6, 9, 1023, 40_000 + 3])
-@pytest.mark.parametrize("variant", [0, 2])
+@pytest.mark.parametrize("variant", [0, 2, 3])
 def test_mul_vec_alignment(m, oa, ob, oc, n, variant):
     P = 998244353
     a, b = synth.c2_inputs(P, 7, n)
@@ -125,13 +125,25 @@ def test_mul_vec_in_place(m):
 @pytest.mark.parametrize("threads,ctas,unroll,variant,chunk", [(32, 1, 1, 0, 0), (128, 2, 2, 0, 0), (256, 8, 8, 0, 0),
                                                                (512, 4, 4, 1, 0), (512, 1, 8, 1, 0), (64, 32, 4, 0, 0),
                                                                (256, 4, 1, 2, 0), (256, 4, 1, 2, 1024),
-                                                               (256, 4, 1, 2, 16384), (256, 4, 1, 2, 4)])
+                                                               (256, 4, 1, 2, 16384), (256, 4, 1, 2, 4),
+                                                               (128, 1, 1, 3, 0), (256, 2, 1, 3, 0), (32, 1, 1, 3, 4),
+                                                               (128, 1, 1, 3, 512), (256, 1, 1, 3, 4096)])
 def test_mul_vec_launch_configs(m, threads, ctas, unroll, variant, chunk):
     P = 2013265921
     a, b = synth.c2_inputs(P, 0, 300_007)
     cfg = m.Launch(threads=threads, ctas_per_sm=ctas, unroll=unroll, variant=variant, chunk=chunk)
     c = m.mul_vec(m.ctx_init(P), dev(a), dev(b), cfg=cfg)
     assert np.array_equal(host(c), oracle.mont_mul(P, a, b))
+
+
+def test_mul_vec_pipe_rejects(m):
+    """variant 3: a tile ring that does not fit in shared memory, or more than 256 threads."""
+    P = 2013265921
+    a = dev(synth.c2_inputs(P, 0, 4096)[0])
+    for cfg in (m.Launch(threads=256, ctas_per_sm=1, unroll=1, variant=3, chunk=8192),
+                m.Launch(threads=512, ctas_per_sm=1, unroll=1, variant=3, chunk=1024)):
+        with pytest.raises(m.MontError):
+            m.mul_vec(m.ctx_init(P), a, a, cfg=cfg)
 
 
 def test_mul_vec_empty(m):
@@ -314,7 +326,8 @@ def test_mul_vec_checksum_fused(m, n, off):
     assert int(acc.item()) == 2 * oracle.raw_sum(ref)
 
 
-@pytest.mark.parametrize("threads,unroll,variant", [(256, 1, 0), (512, 4, 0), (128, 2, 1), (256, 8, 1), (256, 1, 2)])
+@pytest.mark.parametrize("threads,unroll,variant", [(256, 1, 0), (512, 4, 0), (128, 2, 1), (256, 8, 1), (256, 1, 2),
+                                                    (128, 1, 3), (256, 1, 3)])
 def test_mul_vec_checksum_configs(m, threads, unroll, variant):
     P = 998244353
     a, b = synth.c2_inputs(P, 0, 300_001)
@@ -324,7 +337,8 @@ def test_mul_vec_checksum_configs(m, threads, unroll, variant):
     assert np.array_equal(host(c), ref) and int(acc.item()) == oracle.raw_sum(ref)
 
 
-@pytest.mark.parametrize("unroll,threads,variant", [(1, 256, 0), (2, 256, 0), (4, 512, 0), (2, 128, 1)])
+@pytest.mark.parametrize("unroll,threads,variant", [(1, 256, 0), (2, 256, 0), (4, 512, 0), (2, 128, 1), (1, 128, 3),
+                                                    (1, 256, 3)])
 def test_to_from_mont_configs(m, unroll, threads, variant):
     P = 469762049
     x = synth.uniform(42, 9, P, 0, 123_457)
