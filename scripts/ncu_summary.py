@@ -47,6 +47,8 @@ KIND = {  # ncu kernel name prefix -> bench.py kernel label prefix
     "k_sum": "mont_checksum",
     "k_ntt_r32": "mont_ntt",
     "k_ntt_dif": "mont_ntt",
+    "k_ntt_dif_pq": "mont_ntt[variant 3]",
+    "k_ntt_col": "mont_ntt_large[column pass]",
 }
 
 

@@ -17,3 +17,13 @@ done
 CMD2="python bench.py --workload ntt --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --soak 0"
 $CMD2 > $OUT/plain_ntt.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"^k_ntt_dif" -s 3 -c 1 -o $OUT/prof_k_ntt_dif $CMD2 > $OUT/ncu_k_ntt.log 2>&1
 echo "ncu full k_ntt rc=$?"
+# NEXT-row kernels from the probe (after a plain run of the same probe): the precomputed-quotient
+# DIF rows at 2^14 (the probe times REDC DIF x13, DIT x13, then the PQ DIF) and the 3-pass large transform's column kernel at 2^26
+python scripts/probe.py --what ntt --logn 14 > $OUT/plain_probe_ntt.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:"^k_ntt_dif" -s 13 -c 1 \
+      -o $OUT/prof_k_ntt_dif_pq python scripts/probe.py --what ntt --logn 14 > $OUT/ncu_k_ntt_pq.log 2>&1
+echo "ncu full k_ntt_dif pq rc=$?"
+python scripts/probe.py --what nttlarge > $OUT/plain_probe_nttlarge.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:"k_ntt_col" -s 26 -c 1 \
+      -o $OUT/prof_k_ntt_col python scripts/probe.py --what nttlarge > $OUT/ncu_k_ntt_col.log 2>&1
+echo "ncu full k_ntt_col rc=$?"
