@@ -74,8 +74,9 @@ mont_status_t mont_ntt_twiddles_pq(const mont_ctx_t *ctx, uint32_t *tw2, uint32_
  *   bytes per element.
  * otherwise: six-step -- N1 = 2^floor(log_n/2), N2 = 2^ceil(log_n/2): transpose,
  *   N2 transforms of length N1 with the 2-D twiddle in their epilogue,
- *   transpose, N1 transforms of length N2, transpose to natural order.  HBM
- *   traffic 5 x 8 bytes per element.
+ *   transpose, N1 transforms of length N2, transpose to natural order (both
+ *   transform passes with precomputed-quotient twiddles too).  HBM traffic
+ *   5 x 8 bytes per element.
  *
  * plan: device buffer of mont_ntt_plan_words(log_n) words, 8-byte aligned, filled by
  *       mont_ntt_plan_init for a primitive N-th root w (w^-1: inverse).

@@ -503,8 +503,8 @@ static uint32_t host_powmod(uint32_t x, uint64_t e, uint32_t p) {
 using namespace mont;
 
 // plan layout: [column table][row table][2-D low table 2^sh][2-D high table 2^(log_n - sh)];
-// the 3-pass form's column and row tables are pair tables (mont_ntt_twiddles_pq, 2 words per
-// entry, 8-byte aligned), the six-step form's Montgomery tables (1 word per entry)
+// the column and row tables are pair tables (mont_ntt_twiddles_pq, 2 words per entry, 8-byte
+// aligned); the 2-D tables hold Montgomery forms (REDC of two of them gives the factor)
 struct PlanLayout {
     int a, b, sh;
     bool pq;
@@ -513,7 +513,7 @@ struct PlanLayout {
 static PlanLayout plan_layout(int log_n) {
     PlanLayout L;
     ntt_split(log_n, L.a, L.b, L.sh);
-    L.pq = ntt_three_pass(log_n);
+    L.pq = true;  // both forms multiply by precomputed-quotient twiddles
     const size_t e = L.pq ? 2 : 1;
     L.tw1 = 0;
     L.tw2 = L.tw1 + e * (((size_t)1 << L.a) - 1);
@@ -573,11 +573,11 @@ extern "C" mont_status_t mont_ntt_large(const mont_ctx_t *ctx, uint32_t *out, ui
     // x as N1 x N2 [n1][n2] -> out as N2 x N1 [n2][n1]
     if ((st = transpose(out, in, N1, N2, stream)) != MONT_OK) return st;
     // N2 column transforms of length N1, then the twiddle w^(n2 k1)
-    if ((st = ntt_rows(c, out, N2, a, tw1, c.r1, stream, t2)) != MONT_OK) return st;
+    if ((st = ntt_rows(c, out, N2, a, tw1, c.r1, stream, t2, 3)) != MONT_OK) return st;
     // back to N1 x N2 [k1][n2]
     if ((st = transpose(in, out, N2, N1, stream)) != MONT_OK) return st;
     // N1 row transforms of length N2 -> [k1][k2], with the output scale
-    if ((st = ntt_rows(c, in, N1, b, tw2, scale, stream, none)) != MONT_OK) return st;
+    if ((st = ntt_rows(c, in, N1, b, tw2, scale, stream, none, 3)) != MONT_OK) return st;
     // X[k1 + N1 k2] = [k1][k2]: transpose to N2 x N1 -> natural order in out
     return transpose(out, in, N1, N2, stream);
 }
