@@ -62,6 +62,8 @@ mont_status_t mont_ntt_twiddles_pq(const mont_ctx_t *ctx, uint32_t *tw2, uint32_
                                    cudaStream_t stream);
 
 /* ---- large transforms, 2^16 <= N <= 2^30 ----
+ * (An N-point transform needs N | P - 1; for odd P < 2^31 that allows at most
+ * N = 2^27, P = 15 * 2^27 + 1 = 2013265921: no prime c 2^k + 1 < 2^31 has k >= 28.)
  * N = N1 N2, x viewed as the N1 x N2 row-major matrix x[n1][n2].
  * 2^22 <= N <= 2^27: three passes over HBM.  (1) N2 column transforms of
  *   length N1 = 2^12 straight down the matrix (8 adjacent columns per CTA, so
