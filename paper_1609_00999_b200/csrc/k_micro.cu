@@ -36,6 +36,8 @@ __device__ __forceinline__ void op(uint32_t &x, uint64_t &w, uint32_t c, int32_t
         asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x) : "r"(c), "r"((uint32_t)p));  // LOP3 (ALU)
     } else if (KIND == 13) {
         asm volatile("min.u32 %0, %0, %1;" : "+r"(x) : "r"(c));             // VIMNMX (ALU)
+    } else if (KIND == 15) {
+        x = fredc_p1(x, x, (uint32_t)p);                                   // Alg. 3, c = 7 as shifts
     } else if (KIND == 14) {
         asm volatile("shf.l.wrap.b32 %0, %0, %0, %1;" : "+r"(x) : "r"(c));  // SHF (ALU)
     }
@@ -60,6 +62,12 @@ __global__ void __launch_bounds__(256) k_imad(uint32_t *sink, int iters, uint32_
                 if (KIND == 11) {  // 3 integer Montgomery chains : 1 FP64 Barrett chain
                     if (k % 4 == 3) op<8>(x[k], w[k], c, p, pinv, d[k]);
                     else op<3>(x[k], w[k], c, p, pinv, d[k]);
+                } else if (KIND == 16) {  // 7 Montgomery chains : 1 shift-Fourier chain (canonical)
+                    if (k == 7) op<15>(x[k], w[k], c, p, pinv, d[k]);
+                    else op<3>(x[k], w[k], c, p, pinv, d[k]);
+                } else if (KIND == 17) {  // 3 : 1
+                    if (k % 4 == 3) op<15>(x[k], w[k], c, p, pinv, d[k]);
+                    else op<3>(x[k], w[k], c, p, pinv, d[k]);
                 } else if (KIND == 12) {  // 1 : 1
                     if (k % 2 == 1) op<8>(x[k], w[k], c, p, pinv, d[k]);
                     else op<3>(x[k], w[k], c, p, pinv, d[k]);
@@ -81,7 +89,7 @@ using namespace mont;
 
 extern "C" mont_status_t mb_imad(uint32_t *sink, int kind, int iters, const mont_launch_t *cfg, cudaStream_t stream,
                                  unsigned long long *threads_launched) {
-    if (!sink || kind < 0 || kind > 14 || iters < 1) return MONT_EINVAL_ARG;
+    if (!sink || kind < 0 || kind > 17 || iters < 1) return MONT_EINVAL_ARG;
     const int sms = sm_count();
     if (sms <= 0) return MONT_ECUDA;
     const int ctas = (cfg && cfg->ctas_per_sm > 0) ? cfg->ctas_per_sm : 8;
@@ -105,7 +113,10 @@ extern "C" mont_status_t mb_imad(uint32_t *sink, int kind, int iters, const mont
         case 11: k_imad<11><<<grid, 256, 0, stream>>>(sink, iters, c, (int32_t)p, (int32_t)pinv); break;
         case 12: k_imad<12><<<grid, 256, 0, stream>>>(sink, iters, c, (int32_t)p, (int32_t)pinv); break;
         case 13: k_imad<13><<<grid, 256, 0, stream>>>(sink, iters, c, (int32_t)p, (int32_t)pinv); break;
-        default: k_imad<14><<<grid, 256, 0, stream>>>(sink, iters, c, (int32_t)p, (int32_t)pinv); break;
+        case 14: k_imad<14><<<grid, 256, 0, stream>>>(sink, iters, c, (int32_t)p, (int32_t)pinv); break;
+        case 15: k_imad<15><<<grid, 256, 0, stream>>>(sink, iters, c, (int32_t)p, (int32_t)pinv); break;
+        case 16: k_imad<16><<<grid, 256, 0, stream>>>(sink, iters, c, (int32_t)p, (int32_t)pinv); break;
+        default: k_imad<17><<<grid, 256, 0, stream>>>(sink, iters, c, (int32_t)p, (int32_t)pinv); break;
     }
     if (threads_launched) *threads_launched = (unsigned long long)grid * 256ull;
     return launch_status();

@@ -214,3 +214,38 @@ __device__ __forceinline__ uint32_t fredc(uint32_t a, uint32_t b, const FourierD
 }
 
 }  // namespace mont
+
+namespace mont {
+
+// ---- Alg. 3 for P1 = 7 * 2^26 + 1 with the multiplications by c = 7 written as shifts and
+// subtracts in PTX (so neither NVVM nor ptxas turns them back into IMADs): one IMAD.WIDE (a b)
+// on the FMAHeavy pipe, everything else on the ALU.  Canonical in and out.  Exploratory: the
+// K8 microbenchmark measures it alone and in a lane mix with the Montgomery chain.
+__device__ __forceinline__ uint32_t fredc_p1(uint32_t a, uint32_t b, uint32_t p) {
+    const uint64_t T = mul_wide_u32(a, b);
+    const uint32_t q1 = hi32(T), r1 = (uint32_t)T;
+    uint32_t q2, v;
+    // u = 7 r1 = (r1 << 3) - r1 (35 bits); q2 = u >> 6; v = u mod 64
+    asm("{\n\t.reg .u32 s, lo, hi;\n\t"
+        "shl.b32 s, %2, 3;\n\t"
+        "sub.cc.u32 lo, s, %2;\n\t"
+        "shr.u32 hi, %2, 29;\n\t"
+        "subc.u32 hi, hi, 0;\n\t"
+        "shf.r.clamp.b32 %0, lo, hi, 6;\n\t"
+        "and.b32 %1, lo, 63;\n\t}"
+        : "=r"(q2), "=r"(v)
+        : "r"(r1));
+    uint32_t q3p;  // 7 v 2^20 + P = (v << 23) - (v << 20) + P
+    asm("{\n\t.reg .u32 x, y;\n\t"
+        "shl.b32 x, %1, 23;\n\t"
+        "shl.b32 y, %1, 20;\n\t"
+        "sub.u32 x, x, y;\n\t"
+        "add.u32 %0, x, %2;\n\t}"
+        : "=r"(q3p)
+        : "r"(v), "r"(p));
+    uint32_t t = q1 - q2 + q3p;  // t + P in [1, 3P - 1]
+    t = umin(t, t - p);
+    return umin(t, t - p);
+}
+
+}  // namespace mont

@@ -3,6 +3,7 @@ sweeps.  Prints one JSON object per measurement.  Used to pick library defaults
 (DESIGN.md §6); not part of the product."""
 import argparse
 import json
+import os
 import sys
 import time
 from pathlib import Path
@@ -50,8 +51,10 @@ if args.what in ("all", "imad"):
     sink = torch.empty(sms * 32 * 256, dtype=torch.uint32, device=dev)
     names = {0: "IMAD", 1: "IMAD.HI", 2: "IMAD.WIDE(hoisted)", 3: "sredc", 4: "redc", 5: "sredc_mulhi",
              6: "sredc_hiadd", 7: "DFMA", 8: "fmulmod", 9: "IADD", 10: "LOP3", 11: "mix3:1", 12: "mix1:1",
-             13: "VIMNMX(fused 3-in)", 14: "SHF"}
-    for kind in range(15):
+             13: "VIMNMX(fused 3-in)", 14: "SHF", 15: "fredc_p1(Alg.3 shifts)", 16: "mix7:1 sredc:fredc_p1",
+             17: "mix3:1 sredc:fredc_p1"}
+    kinds = [int(k) for k in os.environ.get("PROBE_KINDS", "").split(",") if k] or list(range(18))
+    for kind in kinds:
         for ctas in (4, 8):
             iters = 2000
             nthr = C.c_ulonglong(0)
