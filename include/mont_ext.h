@@ -107,7 +107,9 @@ mont_status_t synth_fill(uint32_t *out, size_t n, uint64_t seed, uint32_t stream
  *   canonical REDC, 5 = REDC from mul.lo/mul.hi, 6 = REDC with an IMAD.HI
  *   64-bit addend, 7 = DFMA, 8 = the FP64 Barrett product, 9 = IADD,
  *   10 = LOP3, 11 = 3 Montgomery : 1 FP64 chains, 12 = 1 : 1, 13 = VIMNMX,
- *   14 = SHF), writing one word per thread to sink[] (which must hold
+ *   14 = SHF, 15 = PAPER.md Alg. 3 for P = 7 2^26 + 1 with c = 7 as shifts,
+ *   16 = 7 Montgomery : 1 Alg.-3 chains, 17 = 3 : 1; kind > 17 is
+ *   MONT_EINVAL_ARG), writing one word per thread to sink[] (which must hold
  *   SMs * ctas_per_sm * 256 words); the caller times it and divides the
  *   executed count (threads * iters * 64) by the time.
  *   grid = SMs * ctas_per_sm, 256 threads (cfg may be NULL: 8 CTAs/SM). */
