@@ -66,11 +66,12 @@ mont_status_t mont_ntt_twiddles_pq(const mont_ctx_t *ctx, uint32_t *tw2, uint32_
  * N = 2^27, P = 15 * 2^27 + 1 = 2013265921: no prime c 2^k + 1 < 2^31 has k >= 28.)
  * N = N1 N2, x viewed as the N1 x N2 row-major matrix x[n1][n2].
  * 2^22 <= N <= 2^27: three passes over HBM.  (1) N2 column transforms of
- *   length N1 = 2^12 straight down the matrix (8 adjacent columns per CTA, so
+ *   length N1 = 2^11 (2^12 for N = 2^22 and 2^27) straight down the matrix
+ *   (8 adjacent columns per CTA, so
  *   every row access is one full 32-byte sector; no transpose), each output
  *   (k1, n2) times the 2-D twiddle w^(n2 k1) (the configs[2] "twiddle multiply
  *   of one NTT stage", generated from two half tables), in place; (2) N1 row
- *   transforms of length N2 = N / 2^12; (3) one transpose to natural order.
+ *   transforms of length N2 = N / N1; (3) one transpose to natural order.
  *   Both transform passes multiply by their twiddles with precomputed
  *   quotients (the pair tables of mont_ntt_twiddles_pq).  HBM traffic 3 x 8
  *   bytes per element.

@@ -478,12 +478,15 @@ static mont_status_t ntt_rows(const Ctx &c, uint32_t *data, size_t batch, int lo
 #undef MONT_NTT_CASE
 
 // split of a large transform: N = N1 * N2.  2^22..2^27: the 3-pass form (column pass over
-// N1 = 2^12 rows, 8 columns = one 32-byte sector per row per CTA, so N2 / 8 >= 128 CTAs; row pass
-// over N2 = 2^10..2^15; one transpose); otherwise the six-step form with N1 = 2^floor(log_n / 2)
+// N1 = 2^11 or 2^12 rows, 8 columns = one 32-byte sector per row per CTA; row pass over
+// N2 = 2^10..2^15; one transpose); otherwise the six-step form with N1 = 2^floor(log_n / 2)
 // (both <= 2^15).
 static bool ntt_three_pass(int log_n) { return log_n >= 22 && log_n <= 27; }
+// Column length: 2^11 (8 x 8 KiB per CTA, 2 CTAs/SM) for 2^23..2^26, 2^12 (1 CTA/SM) for 2^22
+// (where 2^11 leaves only 2^11 / 8 = 256 column CTAs) and 2^27 (rows are capped at 2^15);
+// measured per size, profiles/r01_probe_ntt_large_3pass.jsonl.
 static void ntt_split(int log_n, int &a, int &b, int &sh) {
-    a = ntt_three_pass(log_n) ? 12 : log_n / 2;
+    a = ntt_three_pass(log_n) ? ((log_n == 22 || log_n == 27) ? 12 : 11) : log_n / 2;
     b = log_n - a;
     sh = (log_n + 1) / 2;  // two-level table split of the exponent
 }
@@ -566,7 +569,9 @@ extern "C" mont_status_t mont_ntt_large(const mont_ctx_t *ctx, uint32_t *out, ui
         // output (k1, n2) times w^(n2 k1) -> [k1][n2]; then N1 row transforms of length N2 with
         // the output scale -> [k1][k2]; X[k1 + N1 k2] = [k1][k2]: one transpose to natural order
         // (both passes multiply by the twiddles with precomputed quotients: pair tables)
-        if ((st = launch_ntt_col<12, 8, true>(c, in, N2, tw1, t2, stream)) != MONT_OK) return st;
+        st = a == 11 ? launch_ntt_col<11, 8, true>(c, in, N2, tw1, t2, stream)
+                     : launch_ntt_col<12, 8, true>(c, in, N2, tw1, t2, stream);
+        if (st != MONT_OK) return st;
         if ((st = ntt_rows(c, in, N1, b, tw2, scale, stream, none, 3)) != MONT_OK) return st;
         return transpose(out, in, N1, N2, stream);
     }

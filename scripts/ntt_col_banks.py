@@ -59,7 +59,7 @@ def check(LOG_N, C):
 
 if __name__ == "__main__":
     bad = 0
-    for LOG_N in (12,):  # the instantiated column kernel (k_ntt_col<12, 8, PQ>), and C = 4
+    for LOG_N in (11, 12):  # the instantiated column kernels (k_ntt_col<11|12, 8, PQ>), and C = 4
         for C in (8, 4):
             w = check(LOG_N, C)
             print(f"log_n={LOG_N} C={C}: worst {w}-way")

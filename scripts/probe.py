@@ -313,7 +313,7 @@ if args.what in ("hostrun",):
 if args.what in ("nttlarge",):
     P = 2013265921
     ctx = m.ctx_init(P)
-    for log_n in (20, 22, 24, 26, 27):
+    for log_n in ((args.logn,) if args.logn else (20, 22, 23, 24, 25, 26, 27)):
         N = 1 << log_n
         w = pow(31, (P - 1) // N, P)
         plan = m.ntt_plan(ctx, w, log_n)

@@ -67,6 +67,7 @@ def test_dif_row_kernel_conflict_free(log_n):
     assert worst == 1
 
 
-def test_column_kernel_conflict_free():
+@pytest.mark.parametrize("log_n", [11, 12])
+def test_column_kernel_conflict_free(log_n):
     banks = _load("ntt_col_banks")
-    assert banks.check(12, 8) == 1
+    assert banks.check(log_n, 8) == 1
