@@ -521,6 +521,17 @@ def time_e2e(wl: Workload, steps: int):
 
 # ----------------------------------------------------------- CPU baseline
 
+def cpu_model() -> str:
+    """/proc/cpuinfo model name of the host the oracle ran on."""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(kind: str, target_s: float = 1.5, nsteps: int = 1, threads: int = 0):
     """The oracle (oracle/, plain naive-% definitions, all host cores) on a bounded
     sample of the same workload.  Returns (Gmulmod/s, cores, sample text, seconds)."""
@@ -806,7 +817,7 @@ def main():
     if world == 1 and not args.no_cpu_baseline:
         v, cores, sample, secs, frac = cpu_baseline(wl.kind)
         line["cpu_baseline"] = {"value": float(f"{v:.4g}"), "unit": "Gmulmod/s", "cores": cores, "kind": "oracle",
-                                "sample": sample, "seconds": round(secs, 3)}
+                                "sample": sample, "seconds": round(secs, 3), "cpu_model": cpu_model()}
         if cores > 1:  # the oracle on one thread too (a smaller sample)
             v1, _, sample1, _, _ = cpu_baseline(wl.kind, target_s=1.0, threads=1)
             line["cpu_baseline"]["single_thread"] = {"value": float(f"{v1:.4g}"), "unit": "Gmulmod/s",
