@@ -850,7 +850,7 @@ def main_reference(args, rank, world):
             "config": {"workload": f"bounded sample of the '{kind}' workload (oracle/ on host cores)",
                        "sample_fraction": frac},
             "cpu_baseline": {"value": float(f"{value:.4g}"), "unit": "Gmulmod/s", "cores": cores, "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": round(value, 4), "unit": "Gmulmod/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
