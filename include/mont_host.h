@@ -78,6 +78,12 @@ mont_status_t mont_mul_twiddle_host(const mont_ctx_t *ctx, uint32_t *out_host, c
  * that device chunk (no trip through host memory), and every job's output is
  * downloaded.  Results are those of running the jobs one after another.
  *
+ * Chunk order: groups stream in job order, but up to 3 consecutive groups
+ * are interleaved chunk by chunk so that the H2D and D2H byte counts stay
+ * balanced (a download-heavy group beside upload-heavy ones keeps both
+ * directions of the link busy).  Groups whose host buffers overlap (one writes
+ * what the other reads or writes) are never interleaved: job order decides.
+ *
  * Dependencies: jobs in different groups are independent unless `depends_on`
  * >= 0: then the job's group starts its input copies only after job
  * `depends_on` (an earlier index) has all its outputs in host memory -- needed

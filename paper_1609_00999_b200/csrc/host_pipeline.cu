@@ -439,57 +439,59 @@ extern "C" mont_status_t mont_host_run(const mont_host_job_t *jobs, int njobs, v
     }
     size_t g = 0;  // global chunk counter -> ring slot
     int slot_out0[kRing];  // per slot: first output buffer of the chunk that used it last
-    for (int gi = 0; gi < ng; ++gi) {
+    // one chunk of group gi at unit offset u0 through ring slot g % kRing
+    auto issue = [&](int gi, size_t u0) -> mont_status_t {
         const Group &G = groups[gi];
         const JobPlan &P = plan[G.j0];  // all jobs of a group share n, unit size and chunk
-        for (int j = G.j0; j < G.j1; ++j) {  // dependencies on earlier groups' host outputs
-            const int d = jobs[j].depends_on;
-            if (d >= 0 && d < G.j0) cudaStreamWaitEvent(R.h2d, R.job_out[d], 0);
-        }
-        for (size_t u0 = 0; u0 < P.units; u0 += P.chunk, ++g) {
-            const int slot = (int)(g % kRing);
-            const size_t nu = P.units - u0 < P.chunk ? P.units - u0 : P.chunk;
-            const size_t off = u0 * P.unit_words, bytes = nu * P.unit_words * 4;
-            // the slot's previous chunk must be done with the buffers this upload overwrites: its
-            // kernels, and also its downloads when some of them were outputs there (a group with
-            // more inputs than the one before it)
-            if (g >= (size_t)kRing)
-                cudaStreamWaitEvent(R.h2d, G.nbuf_in > slot_out0[slot] ? R.d2h_done[slot] : R.k_done[slot], 0);
-            slot_out0[slot] = G.nbuf_in;
-            for (int b = 0; b < G.nbuf_in; ++b)
-                if (cudaMemcpyAsync(slot_buf(slot, b), G.in_host[b] + off, bytes, cudaMemcpyHostToDevice, R.h2d) !=
-                    cudaSuccess)
-                    return MONT_ECUDA;
-            cudaEventRecord(R.h2d_done[slot], R.h2d);
-            cudaStreamWaitEvent(R.krn, R.h2d_done[slot], 0);
-            if (g >= (size_t)kRing) cudaStreamWaitEvent(R.krn, R.d2h_done[slot], 0);
-            for (int j = G.j0; j < G.j1; ++j) {
-                const mont_host_job_t &J = jobs[j];
-                const JobPlan &Pj = plan[j];
-                uint32_t *d0 = slot_buf(slot, G.src[j - G.j0][0]);
-                uint32_t *d1 = Pj.nin == 2 ? slot_buf(slot, G.src[j - G.j0][1]) : nullptr;
-                uint32_t *dout = slot_buf(slot, G.dst[j - G.j0]);
-                mont_status_t st;
-                switch (J.op) {
-                    case MONT_HOST_MUL_VEC:
-                        st = Pj.dacc ? mont_mul_vec_checksum(J.ctx, dout, d0, d1, nu, Pj.dacc, R.krn)
-                                     : mont_mul_vec(J.ctx, dout, d0, d1, nu, R.krn);
-                        break;
-                    case MONT_HOST_POW_VEC: st = mont_pow_vec(J.ctx, dout, d0, d1, nu, R.krn); break;
-                    case MONT_HOST_TO_MONT: st = to_mont(J.ctx, dout, d0, nu, R.krn); break;
-                    case MONT_HOST_FROM_MONT: st = from_mont(J.ctx, dout, d0, nu, R.krn); break;
-                    default: st = mont_mul_twiddle(J.ctx, dout, d0, Pj.dtab, nu, J.len, R.krn); break;
-                }
-                if (st != MONT_OK) return st;
+        const int slot = (int)(g % kRing);
+        const size_t nu = P.units - u0 < P.chunk ? P.units - u0 : P.chunk;
+        const size_t off = u0 * P.unit_words, bytes = nu * P.unit_words * 4;
+        // the slot's previous chunk must be done with the buffers this upload overwrites: its
+        // kernels, and also its downloads when some of them were outputs there (a group with
+        // more inputs than the one before it)
+        if (g >= (size_t)kRing)
+            cudaStreamWaitEvent(R.h2d, G.nbuf_in > slot_out0[slot] ? R.d2h_done[slot] : R.k_done[slot], 0);
+        slot_out0[slot] = G.nbuf_in;
+        for (int b = 0; b < G.nbuf_in; ++b)
+            if (cudaMemcpyAsync(slot_buf(slot, b), G.in_host[b] + off, bytes, cudaMemcpyHostToDevice, R.h2d) !=
+                cudaSuccess)
+                return MONT_ECUDA;
+        cudaEventRecord(R.h2d_done[slot], R.h2d);
+        cudaStreamWaitEvent(R.krn, R.h2d_done[slot], 0);
+        if (g >= (size_t)kRing) cudaStreamWaitEvent(R.krn, R.d2h_done[slot], 0);
+        for (int j = G.j0; j < G.j1; ++j) {
+            const mont_host_job_t &J = jobs[j];
+            const JobPlan &Pj = plan[j];
+            uint32_t *d0 = slot_buf(slot, G.src[j - G.j0][0]);
+            uint32_t *d1 = Pj.nin == 2 ? slot_buf(slot, G.src[j - G.j0][1]) : nullptr;
+            uint32_t *dout = slot_buf(slot, G.dst[j - G.j0]);
+            mont_status_t st;
+            switch (J.op) {
+                case MONT_HOST_MUL_VEC:
+                    st = Pj.dacc ? mont_mul_vec_checksum(J.ctx, dout, d0, d1, nu, Pj.dacc, R.krn)
+                                 : mont_mul_vec(J.ctx, dout, d0, d1, nu, R.krn);
+                    break;
+                case MONT_HOST_POW_VEC: st = mont_pow_vec(J.ctx, dout, d0, d1, nu, R.krn); break;
+                case MONT_HOST_TO_MONT: st = to_mont(J.ctx, dout, d0, nu, R.krn); break;
+                case MONT_HOST_FROM_MONT: st = from_mont(J.ctx, dout, d0, nu, R.krn); break;
+                default: st = mont_mul_twiddle(J.ctx, dout, d0, Pj.dtab, nu, J.len, R.krn); break;
             }
-            cudaEventRecord(R.k_done[slot], R.krn);
-            cudaStreamWaitEvent(R.d2h, R.k_done[slot], 0);
-            for (int j = G.j0; j < G.j1; ++j)
-                if (cudaMemcpyAsync(jobs[j].out + off, slot_buf(slot, G.dst[j - G.j0]), bytes, cudaMemcpyDeviceToHost,
-                                    R.d2h) != cudaSuccess)
-                    return MONT_ECUDA;
-            cudaEventRecord(R.d2h_done[slot], R.d2h);
+            if (st != MONT_OK) return st;
         }
+        cudaEventRecord(R.k_done[slot], R.krn);
+        cudaStreamWaitEvent(R.d2h, R.k_done[slot], 0);
+        for (int j = G.j0; j < G.j1; ++j)
+            if (cudaMemcpyAsync(jobs[j].out + off, slot_buf(slot, G.dst[j - G.j0]), bytes, cudaMemcpyDeviceToHost,
+                                R.d2h) != cudaSuccess)
+                return MONT_ECUDA;
+        cudaEventRecord(R.d2h_done[slot], R.d2h);
+        ++g;
+        return MONT_OK;
+    };
+    // after a group's last chunk: checksums and completion events (kernels run in issue order on
+    // R.krn, so the latest k_done covers every kernel of the group)
+    auto finish = [&](int gi) -> mont_status_t {
+        const Group &G = groups[gi];
         for (int j = G.j0; j < G.j1; ++j) {
             if (plan[j].dacc) {
                 cudaStreamWaitEvent(R.d2h, R.k_done[(g + kRing - 1) % kRing], 0);
@@ -499,6 +501,89 @@ extern "C" mont_status_t mont_host_run(const mont_host_job_t *jobs, int njobs, v
         }
         for (int j = G.j0; j < G.j1; ++j)
             if (R.job_out[j]) cudaEventRecord(R.job_out[j], R.d2h);  // the group's outputs are in host memory
+        return MONT_OK;
+    };
+    // Chunk order: groups stream in job order, but up to kWin consecutive ready groups are
+    // interleaved chunk by chunk, each step taking the chunk that keeps the H2D and D2H byte
+    // counts closest (the link is duplex: a download-heavy group next to upload-heavy ones keeps
+    // both directions busy).  A group that depends on an earlier group's host outputs becomes
+    // ready only after that group's last chunk (its completion event) has been issued.
+    constexpr int kWin = 3;
+    static thread_local size_t next_u0[64];
+    static thread_local bool started[64], done[64];
+    static thread_local int group_of[64];
+    for (int gi = 0; gi < ng; ++gi) {
+        next_u0[gi] = 0;
+        started[gi] = done[gi] = false;
+        for (int j = groups[gi].j0; j < groups[gi].j1; ++j) group_of[j] = gi;
+    }
+    // groups whose host buffers overlap (one writes what the other reads or writes) keep job
+    // order: the later one starts only after the earlier one has issued its last chunk
+    auto overlap = [](const void *p, size_t pb, const void *q, size_t qb) {
+        const char *a = (const char *)p, *b = (const char *)q;
+        return p && q && pb && qb && a < b + qb && b < a + pb;
+    };
+    auto conflict = [&](int ga, int gb) {
+        const Group &A = groups[ga], &B = groups[gb];
+        const size_t ba = plan[A.j0].units * plan[A.j0].unit_words * 4, bb = plan[B.j0].units * plan[B.j0].unit_words * 4;
+        for (int ja = A.j0; ja < A.j1; ++ja)
+            for (int jb = B.j0; jb < B.j1; ++jb) {
+                const void *ra[3] = {jobs[ja].in0, plan[ja].nin == 2 ? jobs[ja].in1 : nullptr, jobs[ja].out};
+                const void *rb[3] = {jobs[jb].in0, plan[jb].nin == 2 ? jobs[jb].in1 : nullptr, jobs[jb].out};
+                for (int x = 0; x < 3; ++x)
+                    if (overlap(jobs[ja].out, ba, rb[x], bb) || overlap(jobs[jb].out, bb, ra[x], ba)) return true;
+            }
+        return false;
+    };
+    unsigned long long cum_in = 0, cum_out = 0;
+    int remaining = ng;
+    while (remaining > 0) {
+        int cand[kWin], nc = 0;
+        for (int gi = 0; gi < ng && nc < kWin; ++gi) {
+            if (done[gi]) continue;
+            bool ready = true;
+            for (int j = groups[gi].j0; j < groups[gi].j1; ++j) {
+                const int d = jobs[j].depends_on;
+                if (d >= 0 && group_of[d] != gi && !done[group_of[d]]) ready = false;
+            }
+            for (int c = 0; c < nc && ready; ++c) ready = !conflict(cand[c], gi);
+            if (!ready) break;  // keep job order: nothing past a group still waiting
+            cand[nc++] = gi;
+        }
+        int best = cand[0];
+        unsigned long long best_cost = ~0ull;
+        for (int c = 0; c < nc; ++c) {
+            const Group &G = groups[cand[c]];
+            const JobPlan &P = plan[G.j0];
+            const size_t nu = P.units - next_u0[cand[c]] < P.chunk ? P.units - next_u0[cand[c]] : P.chunk;
+            const unsigned long long b = (unsigned long long)nu * P.unit_words * 4;
+            const unsigned long long in = cum_in + b * G.nbuf_in, out = cum_out + b * (G.j1 - G.j0);
+            const unsigned long long cost = in > out ? in : out;
+            if (cost < best_cost) best_cost = cost, best = cand[c];
+        }
+        const Group &G = groups[best];
+        const JobPlan &P = plan[G.j0];
+        if (!started[best]) {
+            started[best] = true;
+            for (int j = G.j0; j < G.j1; ++j) {  // dependencies on earlier groups' host outputs
+                const int d = jobs[j].depends_on;
+                if (d >= 0 && d < G.j0) cudaStreamWaitEvent(R.h2d, R.job_out[d], 0);
+            }
+        }
+        mont_status_t st;
+        if (P.units > 0) {
+            const size_t u0 = next_u0[best];
+            const size_t nu = P.units - u0 < P.chunk ? P.units - u0 : P.chunk;
+            if ((st = issue(best, u0)) != MONT_OK) return st;
+            next_u0[best] = u0 + nu;
+            cum_in += (unsigned long long)nu * P.unit_words * 4 * G.nbuf_in;
+            cum_out += (unsigned long long)nu * P.unit_words * 4 * (G.j1 - G.j0);
+        }
+        if (next_u0[best] >= P.units) {
+            if ((st = finish(best)) != MONT_OK) return st;
+            done[best] = true;
+            --remaining;
+        }
     }
     cudaEventRecord(R.done_k, R.krn);
     cudaEventRecord(R.done_d, R.d2h);

@@ -170,3 +170,32 @@ def test_host_run_fused_group(m):
         assert np.array_equal(o8.numpy(), ref1)
         assert np.array_equal(hip.numpy(), oracle.to_mont(P, b))
         assert np.array_equal(o9.numpy(), oracle.mont_mul(P, a, a))
+
+
+def test_host_run_interleaving_keeps_host_buffer_order(m):
+    """Independent groups are interleaved chunk by chunk, but a group that overwrites a host
+    buffer an earlier group reads (write after read) still sees job order; so does one that
+    rewrites an earlier group's output (write after write)."""
+    P = 2013265921
+    ctx = m.ctx_init(P)
+    n1, n2 = (1 << 20) + 7, (1 << 19) + 3
+    a = synth.uniform(42, 31, P, 0, n1)
+    c = synth.uniform(42, 32, P, 0, n2)
+    x, y = synth.c2_inputs(P, 3, n2)
+    hA, hC, hx, hy = host(a), host(c), host(x), host(y)
+    hB, hD, hE = empty(n1), empty(n2), empty(n2)
+    hA2 = hA[:n2]                                               # a view: the first n2 words of A
+    jobs = [m.host_job("to_mont", ctx, hB, hA),                 # reads A
+            m.host_job("mul_vec", ctx, hD, hx, hy),             # independent: may interleave
+            m.host_job("from_mont", ctx, hA2, hC),              # then overwrites A's first n2 words
+            m.host_job("mul_vec", ctx, hE, hC, hC),             # independent
+            m.host_job("to_mont", ctx, hD, hy)]                 # rewrites D (after the mul_vec above)
+    for ws_mb in (1, 5, 64):
+        hA.copy_(torch.from_numpy(a))
+        m.host_run(jobs, m.host_workspace("mul_vec", 0, min_bytes=ws_mb << 20))
+        torch.cuda.synchronize()
+        assert np.array_equal(hB.numpy(), oracle.to_mont(P, a))
+        assert np.array_equal(hA.numpy()[:n2], oracle.from_mont(P, c))
+        assert np.array_equal(hA.numpy()[n2:], a[n2:])
+        assert np.array_equal(hE.numpy(), oracle.mont_mul(P, c, c))
+        assert np.array_equal(hD.numpy(), oracle.to_mont(P, y))
