@@ -509,6 +509,9 @@ def time_e2e(wl: Workload, steps: int):
     cur = torch.cuda.current_stream()
     m.host_run(jobs, ws)
     torch.cuda.synchronize()
+    import torch.distributed as dist
+    if dist.is_initialized():  # all ranks share the host's memory system: start them together
+        dist.barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(cur)
