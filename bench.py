@@ -786,7 +786,8 @@ def main():
     roof["kernel"] = dom_r["kernel"]
     roof["peak_kind"] = peak_kind if dom_r["bound"] == "hbm" else "derived (DESIGN.md §6)"
     roof["duration"] = ("median over the K timed steps of a serial pass with CUDA events around each launch "
-                        "(same kernels and launch configurations as the graph-replayed step)")
+                        "(the HBM kernels in the launch configurations of the graph-replayed step; pow in its "
+                        "standalone flat grid)")
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "Gmulmod/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
