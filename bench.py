@@ -432,6 +432,23 @@ def time_steps_graph(wl: Workload, g, K: int):
     return start.elapsed_time(end)
 
 
+def time_steps_flushed(wl: Workload, K: int):
+    """configs[0] fits in L2 (768 KiB): each of the K steps is timed alone between CUDA events,
+    after a 256 MiB write that evicts the 126 MB L2.  The flush is queued before the start event,
+    so the GPU is busy while the host enqueues the step and the interval holds only the step."""
+    torch = wl.torch
+    s = torch.cuda.current_stream()
+    flush = torch.empty(64 << 20, dtype=torch.int32, device=s.device)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for k, (e0, e1) in enumerate(evs):
+        flush.fill_(k)
+        e0.record(s)
+        wl.step()
+        e1.record(s)
+    torch.cuda.synchronize()
+    return sum(e0.elapsed_time(e1) for e0, e1 in evs)
+
+
 def time_steps(wl: Workload, K: int):
     """K serial steps between CUDA events on the launching stream; per-launch events too."""
     torch = wl.torch
@@ -711,7 +728,9 @@ def main():
     torch.cuda.synchronize()
     # the reported number: K steps with the runtime's two-lane schedule
     graph = None
-    if args.graph and not args.serial:
+    if wl.kind == "c1":
+        total_ms = time_steps_flushed(wl, args.steps)
+    elif args.graph and not args.serial:
         graph = capture_step_graph(wl)
         for _ in range(3):
             graph.replay()
@@ -739,6 +758,19 @@ def main():
         box_checksums = shard.combine_checksums(local[:len(prim)], prim)
     else:
         box_checksums = None
+    latency_us = None
+    if wl.kind == "c1":  # configs[0] is launch-latency bound -- report one call's latency
+        lat = []
+        for _ in range(50):
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            ev0.record()
+            wl.step()
+            ev1.record()
+            ev1.synchronize()
+            lat.append(((time.perf_counter() - t0) * 1e6, ev0.elapsed_time(ev1) * 1e3))
+        latency_us = {"host_call_to_completion": round(statistics.median(h for h, _ in lat), 2),
+                      "device_events": round(statistics.median(d for _, d in lat), 2)}
     e2e_ms = None
     if not args.no_e2e and world >= 1:
         e2e_ms = time_e2e(wl, max(1, args.e2e_steps))
@@ -800,10 +832,16 @@ def main():
                                 "c1": "configs[0] mul_vec n=65536 with fixed edge values (launch-latency bound)",
                                 "ntt": "SURVEY 8(f) NEXT #1: in-place forward NTT of the configs[2] batch, 4096 x 2^14"}[wl.kind],
                    "parallelism": f"dp{world} (contiguous global-index slices, no data-path collective)",
-                   "l2": "inputs larger than L2 (step working set ~3.3 GiB vs 126 MB L2)",
+                   "l2": ("L2 flushed before every timed step (256 MiB write; the 768 KiB inputs fit in L2)"
+                          if wl.kind == "c1" else
+                          "inputs larger than L2 (working set per step: " +
+                          {"step": "~3.3 GiB", "c2": "2.3 GiB", "c3": "512 MiB", "c4": "192 MiB",
+                           "c5": f"{12 * (N_C5 // world) / 2**30:.0f} GiB", "ntt": "256 MiB"}[wl.kind] +
+                          " vs 126 MB L2)"),
                    "mulmods_per_step_per_rank": wl.mulmods, **wl.config},
         "gpu_launches": len(wl.launches) * args.steps,
-        "schedule": ("serial, one stream" if args.serial else
+        "schedule": ("each step alone between CUDA events after an L2 flush" if wl.kind == "c1" else
+                     "serial, one stream" if args.serial else
                      "two lanes: HBM-bound launches on one stream, the IMAD-bound pow on another" +
                      (", replayed as one CUDA graph" if args.graph else "")),
         "ms_per_step_serial": round(serial_ms / args.steps, 5),
@@ -812,6 +850,8 @@ def main():
         "clocks": {k: clocks.get(k) for k in ("sm_mhz", "sm_max_mhz", "reasons", "samples", "samples_under_load")},
         "parity": {"checks": checks, "box_checksums": box_checksums},
     }
+    if latency_us is not None:
+        line["latency_us"] = latency_us
     if e2e_ms is not None:
         line["e2e"] = {"value": round(mulmods_job / (e2e_ms * 1e-3) / 1e9, 3), "unit": "Gmulmod/s",
                        "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": wl.e2e_h2d,
