@@ -37,14 +37,17 @@ mont_status_t mont_ntt(const mont_ctx_t *ctx, uint32_t *data, size_t batch, int 
                        uint32_t scale, cudaStream_t stream);
 
 /* mont_ntt with an explicit kernel: variant 0 = decimation in frequency (the
- * default: natural-order input read straight into registers, bit reversal in
- * the final shared-memory gather), 1 = decimation in time (bit-reversed load),
+ * default: natural-order input read straight into registers, shared memory in
+ * a padded layout with the bit reversal done by the last trip's stores),
+ * 1 = decimation in time (bit-reversed load, XOR-swizzled layout),
  * 2 = one butterfly per thread per stage in shared memory (reference),
  * 3 = variant 0 with precomputed-quotient twiddle products: `tw` is then the
- * PAIR table of mont_ntt_twiddles_pq (8-byte aligned, else MONT_EINVAL_ARG;
- * log_n >= 5, else MONT_EUNSUPPORTED) and each butterfly computes
- * x w mod P as x w - hi(x w') P (Shoup), one high product instead of REDC's
- * two.  All variants give identical outputs. */
+ * PAIR table of mont_ntt_twiddles_pq (8-byte aligned, else MONT_EINVAL_ARG)
+ * and each butterfly computes x w mod P as x w - hi(x w') P (Shoup), one high
+ * product instead of REDC's two,
+ * 4 / 5 = variants 0 / 3 with the XOR-swizzled shared layout (bit reversal in
+ * the final gather; for measurement).  Variants 3-5 need log_n >= 5, else
+ * MONT_EUNSUPPORTED.  All variants give identical outputs. */
 mont_status_t mont_ntt_ex(const mont_ctx_t *ctx, uint32_t *data, size_t batch, int log_n, const uint32_t *tw,
                           uint32_t scale, int variant, cudaStream_t stream);
 

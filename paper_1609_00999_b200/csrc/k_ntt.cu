@@ -162,15 +162,36 @@ __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
 // [0, 2P) from LOW words only -- one high product instead of REDC's two (4 FMAHeavy issue slots
 // instead of 5, one ALU op fewer); w' = floor(w 2^32 / P) is the Montgomery form of w times P'
 // mod 2^32.
-template <int LOG_N, bool PQ = false>
+// Shared-memory layouts of the DIF kernel.  XOR swizzle (default): word a at swz(a), combined per
+// access with one LOP3.  PADDED (PAD = true): word a at a + (a >> 5), one pad word per 32; because
+// every access address splits into a per-thread part and a per-k part with disjoint bits, the
+// layout is additive -- f(base | k) = f(base) + f(k) -- so the per-k part is an immediate offset of
+// the LDS/STS and the LOP3s disappear.  The padded layout is conflict-free for every pattern only
+// if the bit reversal happens in the LAST trip's stores (results land in natural order) instead of
+// in the final gather (checked exhaustively for log N = 5..15 by tests/test_ntt_layout.py).
+template <bool PAD>
+__device__ __forceinline__ uint32_t lay(uint32_t a) { return PAD ? a + (a >> 5) : swz(a); }
+template <bool PAD>
+__device__ __forceinline__ uint32_t lay_comb(uint32_t thread_part, uint32_t k_part) {
+    return PAD ? thread_part + k_part : thread_part ^ k_part;
+}
+template <int BITS>
+__host__ __device__ constexpr uint32_t brev_bits(uint32_t x) {
+    uint32_t r = 0;
+    for (int i = 0; i < BITS; ++i) r |= ((x >> i) & 1u) << (BITS - 1 - i);
+    return r;
+}
+
+template <int LOG_N, bool PQ = false, bool PAD = false>
 __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
     k_ntt_dif(Ctx c, uint32_t *data, size_t batch, const uint32_t *__restrict__ tw, uint32_t scale, Tw2D t2) {
     constexpr uint32_t N = 1u << LOG_N, T = N >> 5;
+    constexpr uint32_t NP = PAD ? N + (N >> 5) : N;  // words per row in shared memory
     extern __shared__ uint32_t sm[];
     const uint32_t rl = threadIdx.x / T, t = threadIdx.x % T;
     const size_t row = (size_t)blockIdx.x * (blockDim.x / T) + rl;
     const bool live = row < batch;
-    uint32_t *s = sm + (size_t)rl * N;
+    uint32_t *s = sm + (size_t)rl * NP;
     uint32_t *g = data + row * N;
     uint32_t v[32];
     constexpr int NTRIP = (LOG_N + 4) / 5;
@@ -181,7 +202,7 @@ __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
         const int wlo = top - 5 > 0 ? top - 5 : 0;
         const uint32_t tl = t & ((1u << wlo) - 1u);
         const uint32_t base = tl | ((t >> wlo) << (wlo + 5));
-        const uint32_t sb = swz(base);
+        const uint32_t sb = lay<PAD>(base);
         if (trip == 0) {
             if (live) {
 #pragma unroll
@@ -189,7 +210,7 @@ __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
             }
         } else {
 #pragma unroll
-            for (int k = 0; k < 32; ++k) v[k] = s[sb ^ swz((uint32_t)k << wlo)];
+            for (int k = 0; k < 32; ++k) v[k] = s[lay_comb<PAD>(sb, lay<PAD>((uint32_t)k << wlo))];
         }
 #pragma unroll
         for (int lb = 4; lb >= 0; --lb) {
@@ -221,18 +242,27 @@ __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
                 }
             }
         }
+        if (PAD && trip == NTRIP - 1) {
+            // last trip: the transform's outputs are in bit-reversed order; store each at its
+            // natural index brev(pos) (other threads' words: everyone must have loaded first)
+            if (NTRIP > 1) __syncthreads();
+            const uint32_t bb = lay<PAD>(brev_bits<LOG_N>(base));
 #pragma unroll
-        for (int k = 0; k < 32; ++k) s[sb ^ swz((uint32_t)k << wlo)] = v[k];
+            for (int k = 0; k < 32; ++k) s[bb + lay<PAD>(brev_bits<LOG_N>((uint32_t)k << wlo))] = v[k];
+        } else {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) s[lay_comb<PAD>(sb, lay<PAD>((uint32_t)k << wlo))] = v[k];
+        }
         __syncthreads();
     }
     if (live) {
-        // X[idx] sits at the bit-reversed position
-        const uint32_t bt = swz(__brev(t) >> (32 - LOG_N));
+        // X[idx] sits at the bit-reversed position (swizzled layout) or at idx (padded layout)
+        const uint32_t bt = PAD ? lay<PAD>(t) : swz(__brev(t) >> (32 - LOG_N));
         const uint64_t rowg = (uint64_t)(row + t2.row0);
 #pragma unroll
         for (int k = 0; k < 32; ++k) {
             const uint32_t idx = t + (uint32_t)k * T;
-            uint32_t x = s[bt ^ swz(__brev((uint32_t)k * T) >> (32 - LOG_N))];
+            uint32_t x = PAD ? s[bt + lay<PAD>((uint32_t)k * T)] : s[bt ^ swz(__brev((uint32_t)k * T) >> (32 - LOG_N))];
             if (t2.lo) {
                 const uint64_t e = (rowg * idx) & t2.mask;
                 const uint32_t we = redc(__ldg(t2.hi + (e >> t2.shift)), __ldg(t2.lo + (e & t2.lomask)), c.p, c.pinv);
@@ -257,10 +287,18 @@ __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
 // Column col keeps its N words at sm[col N + (swz(a) ^ (col << CSH))]: the XOR
 // moves the C columns of a G-mode warp access onto different banks (checked
 // exhaustively for every access pattern by scripts/ntt_col_banks.py).
-template <int LOG_N, int C, bool PQ>
+// PAD = true (the default): column c keeps its words at c (N + N/32 + 4) + a + (a >> 5) -- the
+// padded, additive layout of k_ntt_dif<.., PAD> with a 4-word column skew; the last trip stores
+// in natural order and the final gather (map G) reads natural order (all patterns conflict-free:
+// tests/test_ntt_layout.py).
+template <int LOG_N, int C>
+constexpr uint32_t col_stride(bool pad) { return pad ? (1u << LOG_N) + (1u << (LOG_N - 5)) + 4u : (1u << LOG_N); }
+
+template <int LOG_N, int C, bool PQ, bool PAD = true>
 __global__ void __launch_bounds__(C * (1 << LOG_N) / 32, C * (1 << LOG_N) / 32 <= 512 ? 2 : 1)
     k_ntt_col(Ctx c, uint32_t *data, size_t ld, const uint32_t *__restrict__ tw, Tw2D t2) {
     constexpr uint32_t N = 1u << LOG_N, T = N >> 5;
+    constexpr uint32_t NPC = col_stride<LOG_N, C>(PAD);
     constexpr int CSH = (C == 16) ? 1 : (C == 8) ? 2 : 3;  // log2(32 / C)
     static_assert(C == 4 || C == 8 || C == 16, "C: 4, 8 or 16 columns per CTA");
     constexpr int NTRIP = (LOG_N + 4) / 5;
@@ -272,13 +310,13 @@ __global__ void __launch_bounds__(C * (1 << LOG_N) / 32, C * (1 << LOG_N) / 32 <
 #pragma unroll
     for (int trip = 0; trip < NTRIP; ++trip) {
         const uint32_t col = trip == 0 ? cg : cs, t = trip == 0 ? tg : ts;
-        uint32_t *s = sm + col * N;
+        uint32_t *s = sm + col * NPC;
         const uint32_t fx = (col << CSH) & 31u;
         const int top = LOG_N - 5 * trip;
         const int wlo = top - 5 > 0 ? top - 5 : 0;
         const uint32_t tl = t & ((1u << wlo) - 1u);
         const uint32_t base = tl | ((t >> wlo) << (wlo + 5));
-        const uint32_t sb = swz(base) ^ fx;
+        const uint32_t sb = PAD ? lay<true>(base) : (swz(base) ^ fx);
         if (trip == 0) {
             // running pointer: one 64-bit add per load instead of 32 live 64-bit addresses
             const uint32_t *g = data + col0 + col + (size_t)base * ld;
@@ -287,7 +325,7 @@ __global__ void __launch_bounds__(C * (1 << LOG_N) / 32, C * (1 << LOG_N) / 32 <
             for (int k = 0; k < 32; ++k, g += step) v[k] = ld_stream1(g);
         } else {
 #pragma unroll
-            for (int k = 0; k < 32; ++k) v[k] = s[sb ^ swz((uint32_t)k << wlo)];
+            for (int k = 0; k < 32; ++k) v[k] = s[lay_comb<PAD>(sb, lay<PAD>((uint32_t)k << wlo))];
         }
 #pragma unroll
         for (int lb = 4; lb >= 0; --lb) {
@@ -313,9 +351,17 @@ __global__ void __launch_bounds__(C * (1 << LOG_N) / 32, C * (1 << LOG_N) / 32 <
                 }
             }
         }
-        // each thread writes back exactly the 32 words it read this trip: no barrier before the store
+        if (PAD && trip == NTRIP - 1) {
+            // last trip: store each result at its natural index (other threads' words: barrier first)
+            if (NTRIP > 1) __syncthreads();
+            const uint32_t bb = lay<true>(brev_bits<LOG_N>(base));
 #pragma unroll
-        for (int k = 0; k < 32; ++k) s[sb ^ swz((uint32_t)k << wlo)] = v[k];
+            for (int k = 0; k < 32; ++k) s[bb + lay<true>(brev_bits<LOG_N>((uint32_t)k << wlo))] = v[k];
+        } else {
+            // each thread writes back exactly the 32 words it read this trip: no barrier before the store
+#pragma unroll
+            for (int k = 0; k < 32; ++k) s[lay_comb<PAD>(sb, lay<PAD>((uint32_t)k << wlo))] = v[k];
+        }
         __syncthreads();
     }
     // final gather in map H: lanes span the C columns of 32/C rows as in map G, but those rows
@@ -325,10 +371,11 @@ __global__ void __launch_bounds__(C * (1 << LOG_N) / 32, C * (1 << LOG_N) / 32 <
     {
         constexpr uint32_t R = 32 / C;                 // rows per warp
         const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
-        const uint32_t ch = lane % C, th = (lane / C) * (T / R) + wid;
-        const uint32_t *s = sm + ch * N;
+        // padded layout: map G (natural order is conflict-free there); swizzled: map H
+        const uint32_t ch = PAD ? cg : lane % C, th = PAD ? tg : (lane / C) * (T / R) + wid;
+        const uint32_t *s = sm + ch * NPC;
         const uint32_t fx = (ch << CSH) & 31u;
-        const uint32_t bt = swz(__brev(th) >> (32 - LOG_N)) ^ fx;
+        const uint32_t bt = PAD ? lay<true>(th) : (swz(__brev(th) >> (32 - LOG_N)) ^ fx);
         const uint64_t colg = (uint64_t)(col0 + ch);
         uint32_t *g = data + col0 + ch + (size_t)th * ld;
         const size_t step = ld * T;
@@ -336,7 +383,7 @@ __global__ void __launch_bounds__(C * (1 << LOG_N) / 32, C * (1 << LOG_N) / 32 <
         const uint64_t de = (colg * T) & t2.mask;
 #pragma unroll
         for (int k = 0; k < 32; ++k, g += step, e = (e + de) & t2.mask) {
-            const uint32_t x = s[bt ^ swz(__brev((uint32_t)k * T) >> (32 - LOG_N))];
+            const uint32_t x = PAD ? s[bt + lay<true>((uint32_t)k * T)] : s[bt ^ swz(__brev((uint32_t)k * T) >> (32 - LOG_N))];
             const uint32_t we = redc(__ldg(t2.hi + (e >> t2.shift)), __ldg(t2.lo + (e & t2.lomask)), c.p, c.pinv);
             st_stream1(g, redc(x, we, c.p, c.pinv));
         }
@@ -346,30 +393,30 @@ __global__ void __launch_bounds__(C * (1 << LOG_N) / 32, C * (1 << LOG_N) / 32 <
 template <int LOG_N, int C, bool PQ>
 static mont_status_t launch_ntt_col(const Ctx &c, uint32_t *data, size_t ld, const uint32_t *tw, Tw2D t2,
                                     cudaStream_t stream) {
-    constexpr uint32_t N = 1u << LOG_N;
-    const size_t smem = (size_t)C * N * 4;
+    const size_t smem = (size_t)C * col_stride<LOG_N, C>(true) * 4;
     if (ld % C) return MONT_EUNSUPPORTED;
     const size_t grid = ld / C;
     if (grid > 0x7fffffffu) return MONT_EUNSUPPORTED;
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(k_ntt_col<LOG_N, C, PQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return MONT_ECUDA;
-    k_ntt_col<LOG_N, C, PQ><<<(unsigned)grid, C * (N >> 5), smem, stream>>>(c, data, ld, tw, t2);
+    k_ntt_col<LOG_N, C, PQ><<<(unsigned)grid, C * ((1u << LOG_N) >> 5), smem, stream>>>(c, data, ld, tw, t2);
     return launch_status();
 }
 
-template <int LOG_N, bool PQ = false>
+template <int LOG_N, bool PQ = false, bool PAD = false>
 static mont_status_t launch_ntt_dif(const Ctx &c, uint32_t *data, size_t batch, const uint32_t *tw, uint32_t scale,
                                     cudaStream_t stream, Tw2D t2) {
     constexpr uint32_t N = 1u << LOG_N, T = N >> 5;
     constexpr uint32_t rpc = T >= 256 ? 1u : 256u / T;
-    const size_t smem = (size_t)rpc * N * 4;
+    const size_t smem = (size_t)rpc * (PAD ? N + (N >> 5) : N) * 4;
     const size_t grid = (batch + rpc - 1) / rpc;
     if (grid > 0x7fffffffu) return MONT_EUNSUPPORTED;
     if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(k_ntt_dif<LOG_N, PQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        cudaFuncSetAttribute(k_ntt_dif<LOG_N, PQ, PAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
         return MONT_ECUDA;
-    k_ntt_dif<LOG_N, PQ><<<(unsigned)grid, rpc * T, smem, stream>>>(c, data, batch, tw, scale, t2);
+    k_ntt_dif<LOG_N, PQ, PAD><<<(unsigned)grid, rpc * T, smem, stream>>>(c, data, batch, tw, scale, t2);
     return launch_status();
 }
 
@@ -453,11 +500,14 @@ static mont_status_t transpose(uint32_t *dst, const uint32_t *src, size_t R, siz
 
 #define MONT_NTT_CASE(L)                                                                           \
     case L:                                                                                        \
-        return kind == 0   ? launch_ntt_dif<L>(c, data, batch, tw, scale, s, t2)                  \
-               : kind == 3 ? launch_ntt_dif<L, true>(c, data, batch, tw, scale, s, t2)            \
+        return kind == 0   ? launch_ntt_dif<L, false, true>(c, data, batch, tw, scale, s, t2)     \
+               : kind == 3 ? launch_ntt_dif<L, true, true>(c, data, batch, tw, scale, s, t2)      \
+               : kind == 4 ? launch_ntt_dif<L, false, false>(c, data, batch, tw, scale, s, t2)    \
+               : kind == 5 ? launch_ntt_dif<L, true, false>(c, data, batch, tw, scale, s, t2)     \
                            : launch_ntt_r32<L>(c, data, batch, tw, scale, s, t2);
 
-// kind: 0 = DIF (REDC twiddles), 1 = DIT, 3 = DIF with precomputed-quotient twiddles
+// kind: 0 = DIF (REDC twiddles), 1 = DIT, 3 = DIF with precomputed-quotient twiddles (both in the
+// padded shared layout); 4 / 5 = 0 / 3 in the XOR-swizzled layout (kept for measurement)
 static mont_status_t ntt_rows(const Ctx &c, uint32_t *data, size_t batch, int log_n, const uint32_t *tw,
                               uint32_t scale, cudaStream_t s, Tw2D t2, int kind = 0) {
     switch (log_n) {
@@ -607,11 +657,12 @@ extern "C" mont_status_t mont_ntt_ex(const mont_ctx_t *ctx, uint32_t *data, size
     if (log_n < 1 || log_n > 15) return MONT_EUNSUPPORTED;
     if (batch == 0) return MONT_OK;
     if (!data || !tw || ((uintptr_t)data & 3u) || ((uintptr_t)tw & 3u) || scale >= ctx->p) return MONT_EINVAL_ARG;
-    if (batch > 0x7fffffffu || variant < 0 || variant > 3) return variant < 0 || variant > 3 ? MONT_EINVAL_ARG
+    if (batch > 0x7fffffffu || variant < 0 || variant > 5) return variant < 0 || variant > 5 ? MONT_EINVAL_ARG
                                                                                              : MONT_EUNSUPPORTED;
-    if (variant == 3 && ((uintptr_t)tw & 7u)) return MONT_EINVAL_ARG;  // pair table: 8-byte entries
+    const bool pair = variant == 3 || variant == 5;
+    if (pair && ((uintptr_t)tw & 7u)) return MONT_EINVAL_ARG;  // pair table: 8-byte entries
     const uint32_t N = 1u << log_n;
-    if (variant == 3 && log_n < 5) return MONT_EUNSUPPORTED;
+    if (variant >= 3 && log_n < 5) return MONT_EUNSUPPORTED;
     if (log_n >= 5 && variant != 2)
         return ntt_rows(to_dev(ctx), data, batch, log_n, tw, scale, stream, Tw2D{nullptr, nullptr, 0, 0, 0, 0},
                         variant);

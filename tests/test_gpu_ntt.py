@@ -33,14 +33,14 @@ def pq_tables(m, ctx, w, winv, log_n):
 
 @pytest.mark.parametrize("P", list(GEN))
 @pytest.mark.parametrize("log_n", [1, 2, 3, 5, 6, 8, 10, 11, 12])
-@pytest.mark.parametrize("variant", [None, 1, 2, 3])
+@pytest.mark.parametrize("variant", [None, 1, 2, 3, 4, 5])
 def test_ntt_vs_dft(m, P, log_n, variant):
     N = 1 << log_n
     batch = 3
     ctx, w, winv, tw, twi, ninv_m = tables(m, P, N)
-    if variant == 3:
-        if log_n < 5:
-            pytest.skip("variant 3 needs log_n >= 5")
+    if variant in (3, 4, 5) and log_n < 5:
+        pytest.skip("variants 3-5 need log_n >= 5")
+    if variant in (3, 5):
         tw, twi = pq_tables(m, ctx, w, winv, log_n)
     x = synth.uniform(42, 21, P, 0, batch * N).reshape(batch, N)
     x[0, :2] = [0, P - 1]
@@ -53,12 +53,12 @@ def test_ntt_vs_dft(m, P, log_n, variant):
 
 
 @pytest.mark.parametrize("log_n", [13, 14, 15])
-@pytest.mark.parametrize("variant", [None, 1, 3])
+@pytest.mark.parametrize("variant", [None, 1, 3, 4, 5])
 def test_ntt_large_properties(m, log_n, variant):
     P = 998244353
     N = 1 << log_n
     ctx, w, winv, tw, twi, ninv_m = tables(m, P, N)
-    if variant == 3:
+    if variant in (3, 5):
         tw, twi = pq_tables(m, ctx, w, winv, log_n)
     x = synth.uniform(42, 22, P, 0, 2 * N).reshape(2, N)
     d = torch.from_numpy(x).cuda()
