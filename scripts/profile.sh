@@ -23,7 +23,7 @@ python scripts/probe.py --what ntt --logn 14 > $OUT/plain_probe_ntt.log 2>&1 && 
   ncu --set full --clock-control none --import-source on -k regex:"^k_ntt_dif" -s 13 -c 1 \
       -o $OUT/prof_k_ntt_dif_pq python scripts/probe.py --what ntt --logn 14 > $OUT/ncu_k_ntt_pq.log 2>&1
 echo "ncu full k_ntt_dif pq rc=$?"
-python scripts/probe.py --what nttlarge > $OUT/plain_probe_nttlarge.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"k_ntt_col" -s 26 -c 1 \
-      -o $OUT/prof_k_ntt_col python scripts/probe.py --what nttlarge > $OUT/ncu_k_ntt_col.log 2>&1
+python scripts/probe.py --what nttlarge --logn 26 > $OUT/plain_probe_nttlarge.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:"k_ntt_col" -s 3 -c 1 \
+      -o $OUT/prof_k_ntt_col python scripts/probe.py --what nttlarge --logn 26 > $OUT/ncu_k_ntt_col.log 2>&1
 echo "ncu full k_ntt_col rc=$?"
