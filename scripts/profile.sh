@@ -27,3 +27,10 @@ python scripts/probe.py --what nttlarge --logn 26 > $OUT/plain_probe_nttlarge.lo
   ncu --set full --clock-control none --import-source on -k regex:"k_ntt_col" -s 3 -c 1 \
       -o $OUT/prof_k_ntt_col python scripts/probe.py --what nttlarge --logn 26 > $OUT/ncu_k_ntt_col.log 2>&1
 echo "ncu full k_ntt_col rc=$?"
+# summarise on the box (the .ncu-rep files are too large to bring back): profiles/ summaries into
+# $OUT/prof_out/, then drop the reports
+python scripts/ncu_summary.py --round r01 --src $OUT > /dev/null 2>&1; echo "summary rc=$?"
+mkdir -p $OUT/prof_out
+cp profiles/r01_ncu_summary.md profiles/r01_launches.csv profiles/ncu_summary.json $OUT/prof_out/
+tail -1 $OUT/bench_final.log > $OUT/prof_out/r01_bench_step.json
+rm -f $OUT/*.ncu-rep
