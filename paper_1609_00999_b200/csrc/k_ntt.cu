@@ -1,15 +1,21 @@
 // k_ntt.cu -- batched radix-2 NTT with Montgomery twiddle products
 // (include/mont_ntt.h).
 //
-// One CTA per row: the row is loaded from HBM once in bit-reversed order into
-// shared memory, all log_n butterfly stages run there (one __syncthreads per
-// stage), and the row is written back once -- 8 B of HBM traffic per element
-// and (N/2) log_n Montgomery products per row.  Twiddles come from the
-// caller's Montgomery-form table through the read-only path (L1-resident
+// Every row is read from and written to HBM once -- 8 B of traffic per element
+// and (N/2) log_n twiddle products per row.  Kernels:
+//   k_ntt_dif  (default) decimation in frequency, 32 elements per thread, five
+//              stages per trip through shared memory, padded additive layout
+//              (the bit reversal happens in the last trip's stores);
+//   k_ntt_r32  decimation in time, XOR-swizzled layout (variant 1);
+//   k_ntt_smem one butterfly per thread per stage, the reference (variant 2);
+//   k_ntt_col  the large transform's column pass (8 columns per CTA);
+// plus the twiddle-table builders and the transpose of the large transform.
+// Twiddles come from the caller's table through the read-only path (L1-resident
 // across the CTAs of an SM).  The butterfly multiplies a PLAIN residue by a
 // Montgomery-form twiddle, so REDC(v, w-bar) = v w mod P stays plain
 // (REDC(x-bar, y-bar) of two residues is the residue of xy; one
-// plain operand makes the product plain).
+// plain operand makes the product plain); variant 3 instead multiplies by the
+// plain twiddle with its precomputed quotient (Shoup).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
