@@ -4,6 +4,10 @@
 // compute stream and D2H(i-1) on a second copy stream, with per-slot events
 // enforcing buffer reuse.  Host<->device traffic is the bound (PCIe), so the
 // goal is simply that both copy directions and the SMs are busy at once.
+// mont_host_run runs many jobs through one such ring: jobs sharing host buffers
+// form fusion groups (a shared input goes up once, a chained result is read on
+// the device), and consecutive groups are interleaved chunk by chunk to keep
+// both link directions loaded (see include/mont_host.h).
 #include <cuda_runtime.h>
 #include <stdint.h>
 

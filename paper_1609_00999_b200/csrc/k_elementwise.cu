@@ -11,7 +11,8 @@
 // non-coherent path and stored evict-first.  Default shape: a flat grid, one
 // tile of threads * U chunks per CTA (the block scheduler balances fast and
 // slow SMs); variant 1 deals tiles round-robin to a persistent grid of
-// SMs * k CTAs, variant 2 stages each CTA's tiles with cp.async.bulk (TMA).
+// SMs * k CTAs, variant 2 stages each CTA's tiles with cp.async.bulk (TMA),
+// variant 3 is a persistent bulk-copy pipeline (TMA load ring + bulk stores).
 // All U loads of a tile are issued before any arithmetic (memory-level
 // parallelism); the REDC is 5 FMAHeavy issue slots + 2 ALU ops per residue and
 // hides under the HBM stream (~25 % FMAHeavy at full bandwidth).
