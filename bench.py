@@ -757,6 +757,25 @@ def main():
         box_checksums = shard.combine_checksums(local[:len(prim)], prim)
     else:
         box_checksums = None
+    # SURVEY §8(d)'s third HBM denominator: a triad (c = a ^ b, 12 B per element, the mul_vec
+    # launch shape, no modular arithmetic) over 2^26 words, measured in this run
+    triad_gbs = None
+    if wl.kind in ("step", "c2", "c5"):
+        import ctypes as _C
+        n_t = 1 << 26
+        ta, tb, tc = (torch.empty(n_t, dtype=torch.uint32, device="cuda") for _ in range(3))
+        st = torch.cuda.current_stream()
+        launch = lambda: wl.m.lib().mb_triad(tc.data_ptr(), ta.data_ptr(), tb.data_ptr(), n_t, None, st.cuda_stream)
+        for _ in range(3):
+            launch()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+        for e0, e1 in ev:
+            e0.record(st)
+            launch()
+            e1.record(st)
+        torch.cuda.synchronize()
+        triad_gbs = 12 * n_t / (statistics.median(e0.elapsed_time(e1) for e0, e1 in ev) * 1e-3) / 1e9
+        del ta, tb, tc
     latency_us = None
     if wl.kind == "c1":  # configs[0] is launch-latency bound -- report one call's latency
         lat = []
@@ -816,6 +835,9 @@ def main():
     roof = {k: dom_r[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")}
     roof["kernel"] = dom_r["kernel"]
     roof["peak_kind"] = peak_kind if dom_r["bound"] == "hbm" else "derived (DESIGN.md §6)"
+    if triad_gbs is not None and dom_r["bound"] == "hbm":
+        roof["triad_gbs"] = round(triad_gbs, 1)
+        roof["frac_triad"] = round(dom_r["achieved"] / triad_gbs, 4)
     roof["duration"] = ("median over the K timed steps of a serial pass with CUDA events around each launch "
                         "(the HBM kernels in the launch configurations of the graph-replayed step; pow in its "
                         "standalone flat grid)")
