@@ -434,11 +434,12 @@ def time_steps_graph(wl: Workload, g, K: int):
 
 def time_steps_flushed(wl: Workload, K: int):
     """configs[0] fits in L2 (768 KiB): each of the K steps is timed alone between CUDA events,
-    after a 256 MiB write that evicts the 126 MB L2.  The flush is queued before the start event,
-    so the GPU is busy while the host enqueues the step and the interval holds only the step."""
+    after a 512 MiB write that evicts the 126 MB L2.  The flush (~80 us of GPU time) is queued
+    before the start event, so the GPU is still busy while the host enqueues the step and the
+    interval holds only the step."""
     torch = wl.torch
     s = torch.cuda.current_stream()
-    flush = torch.empty(64 << 20, dtype=torch.int32, device=s.device)
+    flush = torch.empty(128 << 20, dtype=torch.int32, device=s.device)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     for k, (e0, e1) in enumerate(evs):
         flush.fill_(k)
@@ -853,7 +854,7 @@ def main():
                                 "c1": "configs[0] mul_vec n=65536 with fixed edge values (launch-latency bound)",
                                 "ntt": "SURVEY 8(f) NEXT #1: in-place forward NTT of the configs[2] batch, 4096 x 2^14"}[wl.kind],
                    "parallelism": f"dp{world} (contiguous global-index slices, no data-path collective)",
-                   "l2": ("L2 flushed before every timed step (256 MiB write; the 768 KiB inputs fit in L2)"
+                   "l2": ("L2 flushed before every timed step (512 MiB write; the 768 KiB inputs fit in L2)"
                           if wl.kind == "c1" else
                           "inputs larger than L2 (working set per step: " +
                           {"step": "~3.3 GiB", "c2": "2.3 GiB", "c3": "512 MiB", "c4": "192 MiB",
