@@ -199,3 +199,33 @@ def test_host_run_interleaving_keeps_host_buffer_order(m):
         assert np.array_equal(hA.numpy()[n2:], a[n2:])
         assert np.array_equal(hE.numpy(), oracle.mont_mul(P, c, c))
         assert np.array_equal(hD.numpy(), oracle.to_mont(P, y))
+
+
+def test_host_run_job_limit(m):
+    """64 jobs in one run (the executor's limit), a mix of ops and sizes; 65 are refused."""
+    P = 998244353
+    ctx = m.ctx_init(P)
+    rng = np.random.default_rng(7)
+    jobs, refs, outs = [], [], []
+    for j in range(64):
+        n = int(rng.integers(1, 5000))
+        a, b = synth.c2_inputs(P, 1000 * j, n)
+        ha, hb, ho = host(a), host(b), empty(n)
+        kind = j % 3
+        if kind == 0:
+            jobs.append(m.host_job("mul_vec", ctx, ho, ha, hb))
+            refs.append(oracle.mont_mul(P, a, b))
+        elif kind == 1:
+            jobs.append(m.host_job("to_mont", ctx, ho, ha))
+            refs.append(oracle.to_mont(P, a))
+        else:
+            jobs.append(m.host_job("from_mont", ctx, ho, ha))
+            refs.append(oracle.from_mont(P, a))
+        outs.append(ho)
+    ws = m.host_workspace("mul_vec", 0, min_bytes=4 << 20)
+    m.host_run(jobs, ws)
+    torch.cuda.synchronize()
+    for o, r in zip(outs, refs):
+        assert np.array_equal(o.numpy(), r)
+    with pytest.raises(m.MontError):
+        m.host_run(jobs + jobs[:1], ws)
