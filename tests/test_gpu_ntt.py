@@ -32,7 +32,7 @@ def pq_tables(m, ctx, w, winv, log_n):
 
 
 @pytest.mark.parametrize("P", list(GEN))
-@pytest.mark.parametrize("log_n", [1, 2, 3, 5, 6, 8, 10, 11, 12])
+@pytest.mark.parametrize("log_n", [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12])
 @pytest.mark.parametrize("variant", [None, 1, 2, 3, 4, 5])
 def test_ntt_vs_dft(m, P, log_n, variant):
     N = 1 << log_n
