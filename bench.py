@@ -520,7 +520,12 @@ def time_e2e(wl: Workload, steps: int):
         jobs.append(m.host_job("mul_vec", wl.ctx[P0], hc, ha, hb, acc=acc))
         keep += [ha, hb, hc, acc]
     if hasattr(wl, "ntt_x"):
-        return None  # NTT has no host-buffer form
+        # the forward transform of host rows (mont_host_run NTT jobs: rows streamed through the ring
+        # and transformed in place in the slot), the table copied once per run
+        hx, ho = pin(wl.ntt_x0), empty(wl.ntt_x0)
+        htw = pin(wl.ntt_tw)
+        jobs.append(m.host_job("ntt", wl.ctx[P0], ho, hx, htw))
+        keep += [hx, ho, htw]
     # bytes actually copied per step, as the library plans them (after fusion)
     wl.e2e_h2d, wl.e2e_d2h = m.host_run_bytes(jobs)
     ws = m.host_workspace("twiddle", TW_LEN, min_bytes=512 << 20)

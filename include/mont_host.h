@@ -36,11 +36,12 @@ typedef enum mont_host_op {
     MONT_HOST_TO_MONT = 1,      /* 1 in, 1 out                                */
     MONT_HOST_FROM_MONT = 2,    /* 1 in, 1 out                                */
     MONT_HOST_POW_VEC = 3,      /* 2 in, 1 out                                */
-    MONT_HOST_TWIDDLE = 4       /* 1 in, 1 out (+ the table, copied once)     */
+    MONT_HOST_TWIDDLE = 4,      /* 1 in, 1 out (+ the table, copied once)     */
+    MONT_HOST_NTT = 5           /* rows in, rows out (+ the table, copied once); mont_host_run only */
 } mont_host_op_t;
 
-/* Smallest workspace (bytes) accepted for `op`; len = twiddle row length
- * (ignored otherwise). */
+/* Smallest workspace (bytes) accepted for `op`; len = twiddle row length or
+ * NTT transform length (ignored otherwise). */
 size_t mont_host_min_workspace(mont_host_op_t op, size_t len);
 
 /* c = REDC(a, b) elementwise (mont_mul_vec); if acc_host != NULL also
@@ -97,12 +98,16 @@ typedef struct mont_host_job {
     int op;                        /* mont_host_op_t                                       */
     const mont_ctx_t *ctx;
     uint32_t *out;                 /* host                                                 */
-    const uint32_t *in0;           /* host: a / x / base                                   */
-    const uint32_t *in1;           /* host: b / exp / the len-word twiddle table (TWIDDLE) */
-    size_t n;                      /* elements (TWIDDLE: rows)                             */
-    size_t len;                    /* TWIDDLE: row length, else ignored                    */
+    const uint32_t *in0;           /* host: a / x / base / the NTT rows                    */
+    const uint32_t *in1;           /* host: b / exp / the len-word twiddle table (TWIDDLE) /
+                                      the (len - 1)-word mont_ntt_twiddles table (NTT)     */
+    size_t n;                      /* elements (TWIDDLE, NTT: rows)                        */
+    size_t len;                    /* TWIDDLE: row length; NTT: transform length 2^k,
+                                      2 <= 2^k <= 2^15; else ignored                       */
     unsigned long long *acc_host;  /* MUL_VEC: optional sum of out (overwritten)           */
     int depends_on;                /* index of an earlier job whose outputs this reads, or -1 */
+    uint32_t scale;                /* NTT: output factor in Montgomery form as in mont_ntt
+                                      (0 selects R mod P, i.e. no scaling); else ignored   */
 } mont_host_job_t;
 
 mont_status_t mont_host_run(const mont_host_job_t *jobs, int njobs, void *ws, size_t ws_bytes,

@@ -107,13 +107,14 @@ SIGNATURES.update({
     "barrett_pow_vec": (C.c_int, [_BCTX, _P, _P, _P, _S, _P]),
 })
 
-HOST_OPS = {"mul_vec": 0, "to_mont": 1, "from_mont": 2, "pow_vec": 3, "twiddle": 4}
+HOST_OPS = {"mul_vec": 0, "to_mont": 1, "from_mont": 2, "pow_vec": 3, "twiddle": 4, "ntt": 5}
 
 
 class HostJob(C.Structure):
     """mont_host_job_t (include/mont_host.h)."""
     _fields_ = [("op", C.c_int), ("ctx", _CTX), ("out", C.c_void_p), ("in0", C.c_void_p), ("in1", C.c_void_p),
-                ("n", C.c_size_t), ("len", C.c_size_t), ("acc_host", C.c_void_p), ("depends_on", C.c_int)]
+                ("n", C.c_size_t), ("len", C.c_size_t), ("acc_host", C.c_void_p), ("depends_on", C.c_int),
+                ("scale", C.c_uint32)]
 
 
 SIGNATURES["mont_host_run"] = (C.c_int, [C.POINTER(HostJob), C.c_int, _P, _S, _P])
@@ -472,17 +473,20 @@ def barrett_pow_vec(ctx: BarrettCtx, base, exp, out=None, stream=None):
     return out
 
 
-def host_job(op: str, ctx: Ctx, out, in0, in1=None, acc=None, depends_on: int = -1) -> HostJob:
-    """Describe one operation on HOST tensors for host_run(); twiddle: in0 = x (batch, len), in1 = tw."""
+def host_job(op: str, ctx: Ctx, out, in0, in1=None, acc=None, depends_on: int = -1, scale: int = 0) -> HostJob:
+    """Describe one operation on HOST tensors for host_run(); twiddle: in0 = x (batch, len), in1 = tw;
+    ntt: in0 = rows (batch, N), in1 = the (N - 1)-word mont_ntt_twiddles table (a host copy), scale = the
+    Montgomery-form output factor (0: none)."""
     j = HostJob()
     j.op = HOST_OPS[op]
     j.ctx = C.pointer(ctx)
     j.out, j.in0 = _ptr(_host_u32(out, "out")), _ptr(_host_u32(in0, "in0"))
     j.in1 = _ptr(_host_u32(in1, "in1")) if in1 is not None else None
-    if op == "twiddle":
+    if op in ("twiddle", "ntt"):
         j.n, j.len = in0.shape[0], in0.shape[1]
     else:
         j.n, j.len = in0.numel(), 0
+    j.scale = int(scale)
     j.acc_host = _ptr(acc) if acc is not None else None
     j.depends_on = int(depends_on)
     j._keep = (ctx, out, in0, in1, acc)  # keep the referenced objects alive

@@ -13,6 +13,7 @@
 
 #include "../../include/mont_ext.h"
 #include "../../include/mont_host.h"
+#include "../../include/mont_ntt.h"
 #include "abi_util.h"
 
 namespace mont {
@@ -144,6 +145,8 @@ extern "C" size_t mont_host_min_workspace(mont_host_op_t op, size_t len) {
         case MONT_HOST_TO_MONT:
         case MONT_HOST_FROM_MONT: return min_ws(1, 1, 0);
         case MONT_HOST_TWIDDLE: return align_up(len * 4) + (size_t)kSlots * 2 * align_up(len * 4) + kAlign;
+        case MONT_HOST_NTT:  // mont_host_run: the table + 4 ring slots of 3 one-row buffers
+            return len < 2 ? 0 : align_up((len - 1) * 4) + (size_t)4 * 3 * align_up(len * 4) + kAlign;
     }
     return 0;
 }
@@ -334,9 +337,17 @@ mont_status_t plan_run(const mont_host_job_t *jobs, int njobs, void *ws, JobPlan
                 P.dtab = (uint32_t *)((char *)ws + reserved);
                 reserved += align_up(J.len * 4);
                 break;
+            case MONT_HOST_NTT:  // rows of len = 2^k words, transformed in place in the slot
+                if (J.len < 2 || J.len > 32768 || (J.len & (J.len - 1)) || (J.scale && J.scale >= J.ctx->p))
+                    return MONT_EINVAL_ARG;
+                P.nin = 1; P.unit_words = J.len; P.units = J.n;
+                P.dtab = (uint32_t *)((char *)ws + reserved);
+                reserved += align_up((J.len - 1) * 4);
+                break;
             default: return MONT_EINVAL_ARG;
         }
-        if (J.n && (!J.out || !J.in0 || (P.nin == 2 && !J.in1) || (J.op == MONT_HOST_TWIDDLE && !J.in1)))
+        if (J.n && (!J.out || !J.in0 || (P.nin == 2 && !J.in1) ||
+                    ((J.op == MONT_HOST_TWIDDLE || J.op == MONT_HOST_NTT) && !J.in1)))
             return MONT_EINVAL_ARG;
         if (J.depends_on >= j || J.depends_on < -1) return MONT_EINVAL_ARG;
         if (J.op == MONT_HOST_MUL_VEC && J.acc_host) {
@@ -394,7 +405,8 @@ mont_status_t plan_run(const mont_host_job_t *jobs, int njobs, void *ws, JobPlan
                 ++G.nbuf;
             }
         }
-        G.dst[j - G.j0] = G.nbuf++;
+        if (J.op == MONT_HOST_NTT) G.dst[j - G.j0] = G.src[j - G.j0][0];  // in place (never fused)
+        else G.dst[j - G.j0] = G.nbuf++;
     }
     return MONT_OK;
 }
@@ -436,8 +448,9 @@ extern "C" mont_status_t mont_host_run(const mont_host_job_t *jobs, int njobs, v
     cudaStreamWaitEvent(R.d2h, R.start, 0);
     // prologue: tables in, accumulators zeroed
     for (int j = 0; j < njobs; ++j) {
-        if (plan[j].dtab &&
-            cudaMemcpyAsync(plan[j].dtab, jobs[j].in1, jobs[j].len * 4, cudaMemcpyHostToDevice, R.h2d) != cudaSuccess)
+        const size_t tab_words = jobs[j].op == MONT_HOST_NTT ? jobs[j].len - 1 : jobs[j].len;
+        if (plan[j].dtab && jobs[j].n &&
+            cudaMemcpyAsync(plan[j].dtab, jobs[j].in1, tab_words * 4, cudaMemcpyHostToDevice, R.h2d) != cudaSuccess)
             return MONT_ECUDA;
         if (plan[j].dacc && cudaMemsetAsync(plan[j].dacc, 0, 8, R.krn) != cudaSuccess) return MONT_ECUDA;
     }
@@ -455,7 +468,7 @@ extern "C" mont_status_t mont_host_run(const mont_host_job_t *jobs, int njobs, v
         // more inputs than the one before it)
         if (g >= (size_t)kRing)
             cudaStreamWaitEvent(R.h2d, G.nbuf_in > slot_out0[slot] ? R.d2h_done[slot] : R.k_done[slot], 0);
-        slot_out0[slot] = G.nbuf_in;
+        slot_out0[slot] = jobs[G.j0].op == MONT_HOST_NTT ? 0 : G.nbuf_in;  // NTT: in place in buffer 0
         for (int b = 0; b < G.nbuf_in; ++b)
             if (cudaMemcpyAsync(slot_buf(slot, b), G.in_host[b] + off, bytes, cudaMemcpyHostToDevice, R.h2d) !=
                 cudaSuccess)
@@ -478,6 +491,12 @@ extern "C" mont_status_t mont_host_run(const mont_host_job_t *jobs, int njobs, v
                 case MONT_HOST_POW_VEC: st = mont_pow_vec(J.ctx, dout, d0, d1, nu, R.krn); break;
                 case MONT_HOST_TO_MONT: st = to_mont(J.ctx, dout, d0, nu, R.krn); break;
                 case MONT_HOST_FROM_MONT: st = from_mont(J.ctx, dout, d0, nu, R.krn); break;
+                case MONT_HOST_NTT: {
+                    int log_n = 0;
+                    while ((1ull << log_n) < J.len) ++log_n;
+                    st = mont_ntt(J.ctx, dout, nu, log_n, Pj.dtab, J.scale ? J.scale : J.ctx->r1, R.krn);
+                    break;
+                }
                 default: st = mont_mul_twiddle(J.ctx, dout, d0, Pj.dtab, nu, J.len, R.krn); break;
             }
             if (st != MONT_OK) return st;
@@ -610,6 +629,7 @@ extern "C" mont_status_t mont_host_run_bytes(const mont_host_job_t *jobs, int nj
     for (int j = 0; j < njobs; ++j) {
         const size_t bytes = plan[j].units * plan[j].unit_words * 4;
         if (jobs[j].op == MONT_HOST_TWIDDLE) *h2d_bytes += jobs[j].len * 4;  // the table, once
+        if (jobs[j].op == MONT_HOST_NTT && jobs[j].n) *h2d_bytes += (jobs[j].len - 1) * 4;
         *d2h_bytes += bytes + (jobs[j].op == MONT_HOST_MUL_VEC && jobs[j].acc_host ? 8 : 0);
     }
     for (int gi = 0; gi < ng; ++gi)

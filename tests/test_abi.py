@@ -136,6 +136,12 @@ def test_host_run_bytes_fusion_plan():
     # twiddle: table once + rows; never fused
     tx, to, tw = torch.zeros((3, 64), dtype=torch.uint32), torch.zeros((3, 64), dtype=torch.uint32), u(64)
     assert m.host_run_bytes([m.host_job("twiddle", ctx, to, tx, tw)]) == (3 * 64 * 4 + 64 * 4, 3 * 64 * 4)
+    # NTT rows: the (N - 1)-word table once, the rows up and back; never fused with others
+    rows, rows_out, ttab = torch.zeros((5, 256), dtype=torch.uint32), torch.zeros((5, 256), dtype=torch.uint32), u(255)
+    assert m.host_run_bytes([m.host_job("ntt", ctx, rows_out, rows, ttab)]) == (5 * 256 * 4 + 255 * 4, 5 * 256 * 4)
+    with pytest.raises(m.MontError):  # not a power of two
+        m.host_run_bytes([m.host_job("ntt", ctx, u(0).reshape(0, 0), torch.zeros((2, 96), dtype=torch.uint32),
+                                     u(95))])
     # the same host buffer as both operands (a squaring) is uploaded once
     assert m.host_run_bytes([m.host_job("mul_vec", ctx, c, a, a)]) == (4 * n, 4 * n)
     with pytest.raises(m.MontError):

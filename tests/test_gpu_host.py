@@ -229,3 +229,38 @@ def test_host_run_job_limit(m):
         assert np.array_equal(o.numpy(), r)
     with pytest.raises(m.MontError):
         m.host_run(jobs + jobs[:1], ws)
+
+
+@pytest.mark.parametrize("log_n", [1, 5, 10, 14])
+def test_host_run_ntt(m, log_n):
+    """NTT jobs from host buffers (rows streamed through the ring, transformed in place in the
+    slot): forward vs the oracle's definition DFT, inverse round trip through a second job, and
+    interleaved with an elementwise job."""
+    P = 2013265921
+    N = 1 << log_n
+    batch = 37 if log_n < 14 else 3
+    ctx = m.ctx_init(P)
+    w = oracle.root_of_unity(P, 31, N)
+    winv = oracle.inverse(w, P)
+    tw = m.ntt_twiddles(ctx, w, log_n).cpu()
+    twi = m.ntt_twiddles(ctx, winv, log_n).cpu()
+    ninv_m = int(oracle.to_mont(P, np.array([oracle.inverse(N, P)], np.uint32))[0])
+    x = synth.uniform(42, 51, P, 0, batch * N).reshape(batch, N)
+    hx = host(x)
+    hX = torch.empty((batch, N), dtype=torch.uint32, pin_memory=True)
+    hback = torch.empty((batch, N), dtype=torch.uint32, pin_memory=True)
+    a, b = synth.c2_inputs(P, 9, 3001)
+    ha, hb, hc = host(a), host(b), empty(3001)
+    jobs = [m.host_job("ntt", ctx, hX, hx, tw),
+            m.host_job("mul_vec", ctx, hc, ha, hb),
+            m.host_job("ntt", ctx, hback, hX, twi, depends_on=0, scale=ninv_m)]
+    for ws_mb in (1, 64):
+        m.host_run(jobs, m.host_workspace("ntt", N, min_bytes=ws_mb << 20))
+        torch.cuda.synchronize()
+        if log_n <= 10:
+            assert np.array_equal(hX.numpy(), oracle.dft(P, w, x))
+        else:
+            for k in (0, 1, N - 1, 12345 % N):
+                assert int(hX.numpy()[1, k]) == oracle.dft_at(P, w, x[1], k)
+        assert np.array_equal(hback.numpy(), x)
+        assert np.array_equal(hc.numpy(), oracle.mont_mul(P, a, b))
