@@ -91,7 +91,7 @@ int main(void) {
     size_t ws_bytes = 64u << 20;
     void *ws;
     if (cudaMalloc(&ws, ws_bytes)) return 1;
-    mont_host_job_t job = {MONT_HOST_MUL_VEC, &ctx, c, a, b, N, 0, &acc, -1};
+    mont_host_job_t job = {MONT_HOST_MUL_VEC, &ctx, c, a, b, N, 0, &acc, -1, 0};
     CHECK(mont_host_run(&job, 1, ws, ws_bytes, 0));
     cudaDeviceSynchronize();
     unsigned long long ref = 0;
