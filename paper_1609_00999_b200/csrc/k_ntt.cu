@@ -19,8 +19,6 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include <cooperative_groups.h>
-
 #include "../../include/mont_ntt.h"
 #include "abi_util.h"
 
@@ -412,144 +410,10 @@ static mont_status_t launch_ntt_col(const Ctx &c, uint32_t *data, size_t ld, con
     return launch_status();
 }
 
-// ---- 2^15-point rows on a 2-CTA thread-block cluster (default for log N = 15): each CTA owns
-// half of the row (16 Ki words + pads, 512 threads), so two rows' CTA pairs fit on an SM pair the
-// way 2^14 rows do, instead of one 1024-thread CTA with 132 KiB per SM.  Ownership by position
-// bit 14: trip 0 (window bits 10..14) reads the row from HBM and stores half of its results into
-// the partner CTA's shared memory (distributed shared memory, then a cluster barrier); trips 1
-// and 2 (bits 5..9, 0..4) stay local; the last trip's bit-reversed stores go to the owner of the
-// natural index's bit 14 (= the position's bit 0), so after another cluster barrier each CTA
-// writes one contiguous half of the row.  Padded additive layout (f(a) = a + (a >> 5)) on the
-// 14-bit local index; every pattern is bank-conflict-free (tests/test_ntt_layout.py).
-template <bool PQ>
-__device__ __forceinline__ void dif_stages(uint32_t (&v)[32], const Ctx &c, const uint32_t *__restrict__ tw,
-                                           uint32_t tl, int wlo, int top) {
-#pragma unroll
-    for (int lb = 4; lb >= 0; --lb) {
-        const int b = wlo + lb;
-        if (b >= top) continue;
-        const uint32_t *twb = tw + ((1u << b) - 1u) + tl;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            const int k0 = ((q >> lb) << (lb + 1)) | (q & ((1 << lb) - 1));
-            const int k1 = k0 | (1 << lb);
-            const uint32_t j = (uint32_t)(k0 & ((1 << lb) - 1));
-            const uint32_t a = v[k0], d = v[k1];
-            v[k0] = mod_add(a, d, c.p);
-            if (wlo == 0 && j == 0) {
-                v[k1] = mod_sub(a, d, c.p);
-            } else if (PQ) {
-                const uint2 wq = __ldg(reinterpret_cast<const uint2 *>(tw) + ((1u << b) - 1u) + tl + (j << wlo));
-                const uint32_t x = a - d + c.p;
-                const uint32_t r = x * wq.x - __umulhi(x, wq.y) * c.p;
-                v[k1] = umin(r, r - c.p);
-            } else {
-                v[k1] = redc(a - d + c.p, __ldg(twb + (j << wlo)), c.p, c.pinv);
-            }
-        }
-    }
-}
-
-template <bool PQ>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 2)
-    k_ntt_dif15c(Ctx c, uint32_t *data, size_t batch, const uint32_t *__restrict__ tw, uint32_t scale, Tw2D t2) {
-    namespace cg = cooperative_groups;
-    cg::cluster_group cluster = cg::this_cluster();
-    constexpr int LOG_N = 15;
-    constexpr uint32_t N = 1u << LOG_N, H = N >> 1;  // H words per CTA
-    extern __shared__ uint32_t sm[];
-    const uint32_t rank = cluster.block_rank(), t = threadIdx.x;
-    const size_t row = blockIdx.x >> 1;
-    uint32_t *g = data + row * N;
-    uint32_t *remote = cluster.map_shared_rank(sm, rank ^ 1u);  // the partner's shared memory
-    uint32_t v[32];
-    // trip 0: window bits [10, 15); thread tt = rank 512 + t owns positions tt | k << 10
-    {
-        const uint32_t tt = (rank << 9) | t;
-#pragma unroll
-        for (int k = 0; k < 32; ++k) v[k] = ld_stream1(g + tt + ((uint32_t)k << 10));
-        dif_stages<PQ>(v, c, tw, tt, 10, 15);
-        const uint32_t fb = lay<true>(tt);
-        // k < 16 -> CTA 0, k >= 16 -> CTA 1: local stores (STS) for this rank's half, DSMEM for the other
-        if (rank == 0) {
-#pragma unroll
-            for (int k = 0; k < 16; ++k) sm[fb + lay<true>((uint32_t)k << 10)] = v[k];
-#pragma unroll
-            for (int k = 16; k < 32; ++k) remote[fb + lay<true>((uint32_t)(k & 15) << 10)] = v[k];
-        } else {
-#pragma unroll
-            for (int k = 0; k < 16; ++k) remote[fb + lay<true>((uint32_t)k << 10)] = v[k];
-#pragma unroll
-            for (int k = 16; k < 32; ++k) sm[fb + lay<true>((uint32_t)(k & 15) << 10)] = v[k];
-        }
-    }
-    cluster.sync();
-    // trip 1: window bits [5, 10), local
-    {
-        const uint32_t tl = t & 31u, base = tl | ((t >> 5) << 10), sb = lay<true>(base);
-#pragma unroll
-        for (int k = 0; k < 32; ++k) v[k] = sm[sb + lay<true>((uint32_t)k << 5)];
-        dif_stages<PQ>(v, c, tw, tl, 5, 10);
-#pragma unroll
-        for (int k = 0; k < 32; ++k) sm[sb + lay<true>((uint32_t)k << 5)] = v[k];
-    }
-    __syncthreads();
-    // trip 2: window bits [0, 5), local; results stored at their natural index in its owner CTA
-    {
-        const uint32_t base = t << 5, sb = lay<true>(base);
-#pragma unroll
-        for (int k = 0; k < 32; ++k) v[k] = sm[sb + lay<true>((uint32_t)k)];
-        dif_stages<PQ>(v, c, tw, 0u, 0, 5);
-        cluster.sync();  // the partner may still be reading its trip-2 inputs
-        // position rank << 14 | base | k -> natural index rank | brev15(base) | brev5(k) << 10,
-        // owned by CTA (k & 1) at local index (rank | brev15(base)) + ((brev5(k) & 15) << 10)
-        const uint32_t fb = lay<true>(rank | brev_bits<15>(base));
-        // even k -> CTA 0, odd k -> CTA 1
-        if (rank == 0) {
-#pragma unroll
-            for (int k = 0; k < 32; k += 2) sm[fb + lay<true>((brev_bits<5>((uint32_t)k) & 15u) << 10)] = v[k];
-#pragma unroll
-            for (int k = 1; k < 32; k += 2) remote[fb + lay<true>((brev_bits<5>((uint32_t)k) & 15u) << 10)] = v[k];
-        } else {
-#pragma unroll
-            for (int k = 0; k < 32; k += 2) remote[fb + lay<true>((brev_bits<5>((uint32_t)k) & 15u) << 10)] = v[k];
-#pragma unroll
-            for (int k = 1; k < 32; k += 2) sm[fb + lay<true>((brev_bits<5>((uint32_t)k) & 15u) << 10)] = v[k];
-        }
-    }
-    cluster.sync();
-    // this CTA holds natural indices rank 2^14 + li: contiguous, coalesced stores
-    if (row < batch) {
-        const uint64_t rowg = (uint64_t)(row + t2.row0);
-#pragma unroll
-        for (int k = 0; k < 32; ++k) {
-            const uint32_t li = t + (uint32_t)k * 512u, idx = (rank << 14) | li;
-            uint32_t x = sm[lay<true>(t) + lay<true>((uint32_t)k * 512u)];
-            if (t2.lo) {
-                const uint64_t e = (rowg * idx) & t2.mask;
-                const uint32_t we = redc(__ldg(t2.hi + (e >> t2.shift)), __ldg(t2.lo + (e & t2.lomask)), c.p, c.pinv);
-                x = redc(x, we, c.p, c.pinv);
-            }
-            if (scale != c.r1) x = redc(x, scale, c.p, c.pinv);
-            st_stream1(g + idx, x);
-        }
-    }
-}
-
 template <int LOG_N, bool PQ = false, bool PAD = false>
 static mont_status_t launch_ntt_dif(const Ctx &c, uint32_t *data, size_t batch, const uint32_t *tw, uint32_t scale,
                                     cudaStream_t stream, Tw2D t2) {
     constexpr uint32_t N = 1u << LOG_N, T = N >> 5;
-    if (LOG_N == 15 && PAD) {  // 2-CTA cluster per row
-        constexpr uint32_t H = N >> 1;
-        const size_t smem15 = (size_t)(H + (H >> 5)) * 4;
-        if (batch * 2 > 0x7fffffffu) return MONT_EUNSUPPORTED;
-        if (cudaFuncSetAttribute(k_ntt_dif15c<PQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem15) !=
-            cudaSuccess)
-            return MONT_ECUDA;
-        k_ntt_dif15c<PQ><<<(unsigned)(batch * 2), 512, smem15, stream>>>(c, data, batch, tw, scale, t2);
-        return launch_status();
-    }
     constexpr uint32_t rpc = T >= 256 ? 1u : 256u / T;
     const size_t smem = (size_t)rpc * (PAD ? N + (N >> 5) : N) * 4;
     const size_t grid = (batch + rpc - 1) / rpc;
