@@ -2,7 +2,7 @@
 """bench.py -- the driver's benchmark contract for the batched 32-bit Montgomery path.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {b200,reference}]
-                    [--workload {step,c2,c3,c4,c5}]
+                    [--workload {step,c1,c2,c3,c4,c5,ntt}]
 
 One "step" (default workload) is one pass of the whole hot path of
 SURVEY.md §8(a) (rows A1-A11) over one batch of synthetic input, per rank:
@@ -24,7 +24,15 @@ sum_i(31 + popcount(exp_i)) ladder products.  Inputs are generated in HBM by
 the device generator (synth_fill) from the GLOBAL element index, so rank r of
 N processes slice r of an N-times larger job (weak scaling, no data-path
 collective).  The step's working set (~3.3 GiB) is far larger than the
-126 MB L2, so no L2 flush is needed between steps.
+126 MB L2, so no L2 flush is needed between steps (configs[0], 768 KiB, is
+timed step by step after an L2 flush instead).  The other workloads time one
+config each (c1..c5 = BASELINE configs[0..4]; ntt = SURVEY §8(f) NEXT #1).
+
+Besides `value`, the line carries `roofline` (the dominant kernel against the
+measured HBM copy rate, the nominal 8 TB/s and an in-run triad), `kernels`
+(every launch), `e2e` (the same step through the host-buffer executor
+mont_host_run, copies inside the timed region), `cpu_baseline` (the oracle on
+all host cores and on one), `clocks` and `parity`.
 
 --impl reference times the CPU oracle (oracle/, the slow plain-definition
 program) on a bounded sample of the same workload on the host cores; there
