@@ -790,6 +790,27 @@ def main():
         torch.cuda.synchronize()
         triad_gbs = 12 * n_t / (statistics.median(e0.elapsed_time(e1) for e0, e1 in ev) * 1e-3) / 1e9
         del ta, tb, tc
+    # the integer-multiply denominator measured in this run: the K8 microbenchmark's chain of the
+    # library's signed REDC (mb_imad kind 3: 8 independent chains per thread, 8 CTAs/SM)
+    redc_peak = None
+    if wl.kind in ("step", "c4", "ntt"):
+        import ctypes as _C
+        sms = torch.cuda.get_device_properties(0).multi_processor_count
+        sink = torch.empty(sms * 8 * 256, dtype=torch.uint32, device="cuda")
+        nthr = _C.c_ulonglong(0)
+        cfg = wl.m.Launch(ctas_per_sm=8)
+        st = torch.cuda.current_stream()
+        run = lambda: wl.m.lib().mb_imad(sink.data_ptr(), 3, 400, _C.byref(cfg), st.cuda_stream, _C.byref(nthr))
+        run()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(5)]
+        for e0, e1 in ev:
+            e0.record(st)
+            run()
+            e1.record(st)
+        torch.cuda.synchronize()
+        med = statistics.median(e0.elapsed_time(e1) for e0, e1 in ev) * 1e-3
+        redc_peak = nthr.value * 400 * 64 / med / 1e12  # REDCs per second, in T/s
+        del sink
     latency_us = None
     if wl.kind == "c1":  # configs[0] is launch-latency bound -- report one call's latency
         lat = []
@@ -836,6 +857,8 @@ def main():
                       # SURVEY §8(d)'s other denominator: 4 multiplies per REDC at the full IMAD rate
                       # (IMAD.WIDE/IMAD.HI measured half rate on B200, so this one is not reachable)
                       "frac_imad_div4": round(ach / (sms * 64 / 4 * clk / 1e12), 4)})
+            if redc_peak:
+                r.update({"redc_chain_peak_measured": round(redc_peak, 4), "frac_redc_measured": round(ach / redc_peak, 4)})
         r["traffic"] = ncu_traffic(name)
         rooflines.append(r)
     dom = max(range(len(per_ms)), key=lambda i: per_ms[i])
