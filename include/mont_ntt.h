@@ -47,7 +47,10 @@ mont_status_t mont_ntt(const mont_ctx_t *ctx, uint32_t *data, size_t batch, int 
  * product instead of REDC's two,
  * 4 / 5 = variants 0 / 3 with the XOR-swizzled shared layout (bit reversal in
  * the final gather; for measurement).  Variants 3-5 need log_n >= 5, else
- * MONT_EUNSUPPORTED.  All variants give identical outputs. */
+ * MONT_EUNSUPPORTED.  For P < 2^30 variants 0 and 3 keep values between stages
+ * in [0, 2P) (lazy butterflies, one correction fewer each; the environment
+ * variable MONT_NTT_NO_LAZY=1, read once, turns that off for measurement).
+ * All variants give identical outputs. */
 mont_status_t mont_ntt_ex(const mont_ctx_t *ctx, uint32_t *data, size_t batch, int log_n, const uint32_t *tw,
                           uint32_t scale, int variant, cudaStream_t stream);
 

@@ -18,6 +18,7 @@
 // plain twiddle with its precomputed quotient (Shoup).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/mont_ntt.h"
 #include "abi_util.h"
@@ -188,7 +189,12 @@ __host__ __device__ constexpr uint32_t brev_bits(uint32_t x) {
     return r;
 }
 
-template <int LOG_N, bool PQ = false, bool PAD = false>
+// LAZY (P < 2^30, so 4P < 2^32): values between stages live in [0, 2P) instead of [0, P)
+// (Harvey's lazy butterfly): the sum is folded to [0, 2P) with one min against 2P, the difference
+// a - d + 2P < 4P goes into the product unreduced, and the product's own final correction is
+// dropped (REDC and the precomputed-quotient product both return [0, 2P) before it) -- one ALU op
+// fewer per butterfly; outputs are canonicalised once at the end.
+template <int LOG_N, bool PQ = false, bool PAD = false, bool LAZY = false>
 __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
     k_ntt_dif(Ctx c, uint32_t *data, size_t batch, const uint32_t *__restrict__ tw, uint32_t scale, Tw2D t2) {
     constexpr uint32_t N = 1u << LOG_N, T = N >> 5;
@@ -229,17 +235,33 @@ __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
                 const int k1 = k0 | (1 << lb);
                 const uint32_t j = (uint32_t)(k0 & ((1 << lb) - 1));
                 const uint32_t a = v[k0], d = v[k1];
-                v[k0] = mod_add(a, d, c.p);
+                const uint32_t p2 = 2u * c.p;
+                if (LAZY) {
+                    const uint32_t sum = a + d;                  // [0, 4P)
+                    v[k0] = umin(sum, sum - p2);                 // [0, 2P)
+                } else {
+                    v[k0] = mod_add(a, d, c.p);
+                }
                 if (wlo == 0 && j == 0) {
                     // pos = 0 (tl is empty when wlo = 0): the twiddle is w^0 = 1, so the product is
                     // skipped (a compile-time decision; 30 of the last trip's 64 butterflies at 2^14)
-                    v[k1] = mod_sub(a, d, c.p);
+                    if (LAZY) {
+                        const uint32_t x = a - d + p2;           // (0, 4P)
+                        v[k1] = umin(x, x - p2);
+                    } else {
+                        v[k1] = mod_sub(a, d, c.p);
+                    }
                 } else if (PQ) {
                     const uint2 wq = __ldg(reinterpret_cast<const uint2 *>(tw) + ((1u << b) - 1u) + tl + (j << wlo));
-                    const uint32_t x = a - d + c.p;           // (0, 2P): any x < 2^32 is allowed
+                    const uint32_t x = a - d + (LAZY ? p2 : c.p);  // (0, 2P) or (0, 4P): any x < 2^32 is allowed
                     const uint32_t q = __umulhi(x, wq.y);     // floor(x w' / 2^32)
                     const uint32_t r = x * wq.x - q * c.p;    // x w - q P in [0, 2P), exact mod 2^32
-                    v[k1] = umin(r, r - c.p);
+                    v[k1] = LAZY ? r : umin(r, r - c.p);
+                } else if (LAZY) {
+                    // (a - d + 2P) w < 4P P < 2^32 P: REDC's precondition holds; keep t' + P in (0, 2P)
+                    const uint64_t T = mul_wide_u32(a - d + p2, __ldg(twb + (j << wlo)));
+                    const uint32_t m = (uint32_t)T * c.pinv;
+                    v[k1] = hi32(T) - hi32(mul_wide_u32(m, c.p)) + c.p;
                 } else {
                     const uint32_t w = __ldg(twb + (j << wlo));
                     // REDC needs only (a - d) w < 2^32 P, so a - d + P in (0, 2P) goes in unreduced:
@@ -269,6 +291,7 @@ __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
         for (int k = 0; k < 32; ++k) {
             const uint32_t idx = t + (uint32_t)k * T;
             uint32_t x = PAD ? s[bt + lay<PAD>((uint32_t)k * T)] : s[bt ^ swz(__brev((uint32_t)k * T) >> (32 - LOG_N))];
+            if (LAZY) x = umin(x, x - c.p);  // [0, 2P) -> [0, P)
             if (t2.lo) {
                 const uint64_t e = (rowg * idx) & t2.mask;
                 const uint32_t we = redc(__ldg(t2.hi + (e >> t2.shift)), __ldg(t2.lo + (e & t2.lomask)), c.p, c.pinv);
@@ -410,7 +433,7 @@ static mont_status_t launch_ntt_col(const Ctx &c, uint32_t *data, size_t ld, con
     return launch_status();
 }
 
-template <int LOG_N, bool PQ = false, bool PAD = false>
+template <int LOG_N, bool PQ = false, bool PAD = false, bool LAZY = false>
 static mont_status_t launch_ntt_dif(const Ctx &c, uint32_t *data, size_t batch, const uint32_t *tw, uint32_t scale,
                                     cudaStream_t stream, Tw2D t2) {
     constexpr uint32_t N = 1u << LOG_N, T = N >> 5;
@@ -419,10 +442,10 @@ static mont_status_t launch_ntt_dif(const Ctx &c, uint32_t *data, size_t batch, 
     const size_t grid = (batch + rpc - 1) / rpc;
     if (grid > 0x7fffffffu) return MONT_EUNSUPPORTED;
     if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(k_ntt_dif<LOG_N, PQ, PAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaFuncSetAttribute(k_ntt_dif<LOG_N, PQ, PAD, LAZY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess)
         return MONT_ECUDA;
-    k_ntt_dif<LOG_N, PQ, PAD><<<(unsigned)grid, rpc * T, smem, stream>>>(c, data, batch, tw, scale, t2);
+    k_ntt_dif<LOG_N, PQ, PAD, LAZY><<<(unsigned)grid, rpc * T, smem, stream>>>(c, data, batch, tw, scale, t2);
     return launch_status();
 }
 
@@ -506,8 +529,10 @@ static mont_status_t transpose(uint32_t *dst, const uint32_t *src, size_t R, siz
 
 #define MONT_NTT_CASE(L)                                                                           \
     case L:                                                                                        \
-        return kind == 0   ? launch_ntt_dif<L, false, true>(c, data, batch, tw, scale, s, t2)     \
-               : kind == 3 ? launch_ntt_dif<L, true, true>(c, data, batch, tw, scale, s, t2)      \
+        return kind == 0   ? (lazy ? launch_ntt_dif<L, false, true, true>(c, data, batch, tw, scale, s, t2)   \
+                                   : launch_ntt_dif<L, false, true>(c, data, batch, tw, scale, s, t2))      \
+               : kind == 3 ? (lazy ? launch_ntt_dif<L, true, true, true>(c, data, batch, tw, scale, s, t2)    \
+                                   : launch_ntt_dif<L, true, true>(c, data, batch, tw, scale, s, t2))       \
                : kind == 4 ? launch_ntt_dif<L, false, false>(c, data, batch, tw, scale, s, t2)    \
                : kind == 5 ? launch_ntt_dif<L, true, false>(c, data, batch, tw, scale, s, t2)     \
                            : launch_ntt_r32<L>(c, data, batch, tw, scale, s, t2);
@@ -516,6 +541,9 @@ static mont_status_t transpose(uint32_t *dst, const uint32_t *src, size_t R, siz
 // padded shared layout); 4 / 5 = 0 / 3 in the XOR-swizzled layout (kept for measurement)
 static mont_status_t ntt_rows(const Ctx &c, uint32_t *data, size_t batch, int log_n, const uint32_t *tw,
                               uint32_t scale, cudaStream_t s, Tw2D t2, int kind = 0) {
+    // lazy [0, 2P) butterflies when 4P < 2^32 (P < 2^30); MONT_NTT_NO_LAZY=1 turns them off
+    static const bool lazy_ok = !(getenv("MONT_NTT_NO_LAZY") && getenv("MONT_NTT_NO_LAZY")[0] == '1');
+    const bool lazy = lazy_ok && c.p < (1u << 30);
     switch (log_n) {
         MONT_NTT_CASE(5)
         MONT_NTT_CASE(6)

@@ -187,13 +187,14 @@ if args.what in ("pcie",):
     out(what="nvidia-smi topo", txt=subprocess.run(["nvidia-smi", "-q", "-d", "PCIE"], capture_output=True, text=True).stdout[-1500:])
 
 if args.what in ("ntt",):
-    P = 2013265921
+    P = int(os.environ.get("PROBE_P", "2013265921"))
+    G = {2013265921: 31, 469762049: 3, 998244353: 3}[P]
     ctx = m.ctx_init(P)
     import numpy as np
     for log_n in ((args.logn,) if args.logn else (10, 12, 13, 14, 15)):
         N = 1 << log_n
         batch = (1 << 26) // N
-        w = pow(31, (P - 1) // N, P)
+        w = pow(G, (P - 1) // N, P)
         tw = m.ntt_twiddles(ctx, w, log_n)
         d = torch.empty(batch * N, dtype=torch.uint32, device=dev)
         m.synth_fill(d, 42, 5, 0, P)
