@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
 template <int LOG_N, int C>
 constexpr uint32_t col_stride(bool pad) { return pad ? (1u << LOG_N) + (1u << (LOG_N - 5)) + 4u : (1u << LOG_N); }
 
-template <int LOG_N, int C, bool PQ, bool PAD = true>
+template <int LOG_N, int C, bool PQ, bool PAD = true, bool LAZY = false>
 __global__ void __launch_bounds__(C * (1 << LOG_N) / 32, C * (1 << LOG_N) / 32 <= 512 ? 2 : 1)
     k_ntt_col(Ctx c, uint32_t *data, size_t ld, const uint32_t *__restrict__ tw, Tw2D t2) {
     constexpr uint32_t N = 1u << LOG_N, T = N >> 5;
@@ -367,14 +367,29 @@ __global__ void __launch_bounds__(C * (1 << LOG_N) / 32, C * (1 << LOG_N) / 32 <
                 const int k1 = k0 | (1 << lb);
                 const uint32_t j = (uint32_t)(k0 & ((1 << lb) - 1));
                 const uint32_t a = v[k0], d = v[k1];
-                v[k0] = mod_add(a, d, c.p);
+                const uint32_t p2 = 2u * c.p;  // LAZY: values in [0, 2P), as in k_ntt_dif<.., LAZY>
+                if (LAZY) {
+                    const uint32_t sum = a + d;
+                    v[k0] = umin(sum, sum - p2);
+                } else {
+                    v[k0] = mod_add(a, d, c.p);
+                }
                 if (wlo == 0 && j == 0) {
-                    v[k1] = mod_sub(a, d, c.p);
+                    if (LAZY) {
+                        const uint32_t x = a - d + p2;
+                        v[k1] = umin(x, x - p2);
+                    } else {
+                        v[k1] = mod_sub(a, d, c.p);
+                    }
                 } else if (PQ) {  // precomputed-quotient product, as in k_ntt_dif<.., true>
                     const uint2 wq = __ldg(reinterpret_cast<const uint2 *>(tw) + ((1u << b) - 1u) + tl + (j << wlo));
-                    const uint32_t x = a - d + c.p;
+                    const uint32_t x = a - d + (LAZY ? p2 : c.p);
                     const uint32_t r = x * wq.x - __umulhi(x, wq.y) * c.p;
-                    v[k1] = umin(r, r - c.p);
+                    v[k1] = LAZY ? r : umin(r, r - c.p);
+                } else if (LAZY) {
+                    const uint64_t T = mul_wide_u32(a - d + p2, __ldg(twb + (j << wlo)));
+                    const uint32_t m = (uint32_t)T * c.pinv;
+                    v[k1] = hi32(T) - hi32(mul_wide_u32(m, c.p)) + c.p;
                 } else {
                     v[k1] = redc(a - d + c.p, __ldg(twb + (j << wlo)), c.p, c.pinv);
                 }
@@ -412,6 +427,7 @@ __global__ void __launch_bounds__(C * (1 << LOG_N) / 32, C * (1 << LOG_N) / 32 <
         const uint64_t de = (colg * T) & t2.mask;
 #pragma unroll
         for (int k = 0; k < 32; ++k, g += step, e = (e + de) & t2.mask) {
+            // (LAZY: x in [0, 2P); the REDC with the 2-D twiddle below still returns [0, P))
             const uint32_t x = PAD ? s[bt + lay<true>((uint32_t)k * T)] : s[bt ^ swz(__brev((uint32_t)k * T) >> (32 - LOG_N))];
             const uint32_t we = redc(__ldg(t2.hi + (e >> t2.shift)), __ldg(t2.lo + (e & t2.lomask)), c.p, c.pinv);
             st_stream1(g, redc(x, we, c.p, c.pinv));
@@ -419,7 +435,7 @@ __global__ void __launch_bounds__(C * (1 << LOG_N) / 32, C * (1 << LOG_N) / 32 <
     }
 }
 
-template <int LOG_N, int C, bool PQ>
+template <int LOG_N, int C, bool PQ, bool LAZY = false>
 static mont_status_t launch_ntt_col(const Ctx &c, uint32_t *data, size_t ld, const uint32_t *tw, Tw2D t2,
                                     cudaStream_t stream) {
     const size_t smem = (size_t)C * col_stride<LOG_N, C>(true) * 4;
@@ -427,9 +443,10 @@ static mont_status_t launch_ntt_col(const Ctx &c, uint32_t *data, size_t ld, con
     const size_t grid = ld / C;
     if (grid > 0x7fffffffu) return MONT_EUNSUPPORTED;
     if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(k_ntt_col<LOG_N, C, PQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        cudaFuncSetAttribute(k_ntt_col<LOG_N, C, PQ, true, LAZY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
         return MONT_ECUDA;
-    k_ntt_col<LOG_N, C, PQ><<<(unsigned)grid, C * ((1u << LOG_N) >> 5), smem, stream>>>(c, data, ld, tw, t2);
+    k_ntt_col<LOG_N, C, PQ, true, LAZY><<<(unsigned)grid, C * ((1u << LOG_N) >> 5), smem, stream>>>(c, data, ld, tw, t2);
     return launch_status();
 }
 
@@ -537,13 +554,17 @@ static mont_status_t transpose(uint32_t *dst, const uint32_t *src, size_t R, siz
                : kind == 5 ? launch_ntt_dif<L, true, false>(c, data, batch, tw, scale, s, t2)     \
                            : launch_ntt_r32<L>(c, data, batch, tw, scale, s, t2);
 
+// lazy [0, 2P) butterflies when 4P < 2^32 (P < 2^30); MONT_NTT_NO_LAZY=1 turns them off (measurement)
+static bool ntt_lazy(uint32_t p) {
+    static const bool ok = !(getenv("MONT_NTT_NO_LAZY") && getenv("MONT_NTT_NO_LAZY")[0] == '1');
+    return ok && p < (1u << 30);
+}
+
 // kind: 0 = DIF (REDC twiddles), 1 = DIT, 3 = DIF with precomputed-quotient twiddles (both in the
 // padded shared layout); 4 / 5 = 0 / 3 in the XOR-swizzled layout (kept for measurement)
 static mont_status_t ntt_rows(const Ctx &c, uint32_t *data, size_t batch, int log_n, const uint32_t *tw,
                               uint32_t scale, cudaStream_t s, Tw2D t2, int kind = 0) {
-    // lazy [0, 2P) butterflies when 4P < 2^32 (P < 2^30); MONT_NTT_NO_LAZY=1 turns them off
-    static const bool lazy_ok = !(getenv("MONT_NTT_NO_LAZY") && getenv("MONT_NTT_NO_LAZY")[0] == '1');
-    const bool lazy = lazy_ok && c.p < (1u << 30);
+    const bool lazy = ntt_lazy(c.p);
     switch (log_n) {
         MONT_NTT_CASE(5)
         MONT_NTT_CASE(6)
@@ -653,8 +674,11 @@ extern "C" mont_status_t mont_ntt_large(const mont_ctx_t *ctx, uint32_t *out, ui
         // output (k1, n2) times w^(n2 k1) -> [k1][n2]; then N1 row transforms of length N2 with
         // the output scale -> [k1][k2]; X[k1 + N1 k2] = [k1][k2]: one transpose to natural order
         // (both passes multiply by the twiddles with precomputed quotients: pair tables)
-        st = a == 11 ? launch_ntt_col<11, 8, true>(c, in, N2, tw1, t2, stream)
-                     : launch_ntt_col<12, 8, true>(c, in, N2, tw1, t2, stream);
+        const bool lazy = ntt_lazy(c.p);
+        st = a == 11 ? (lazy ? launch_ntt_col<11, 8, true, true>(c, in, N2, tw1, t2, stream)
+                             : launch_ntt_col<11, 8, true>(c, in, N2, tw1, t2, stream))
+                     : (lazy ? launch_ntt_col<12, 8, true, true>(c, in, N2, tw1, t2, stream)
+                             : launch_ntt_col<12, 8, true>(c, in, N2, tw1, t2, stream));
         if (st != MONT_OK) return st;
         if ((st = ntt_rows(c, in, N1, b, tw2, scale, stream, none, 3)) != MONT_OK) return st;
         return transpose(out, in, N1, N2, stream);

@@ -313,11 +313,12 @@ if args.what in ("hostrun",):
     out(what="raw 1.5GB h2d alone", ms=med * 1e3, gbs=24 * n / med / 1e9)
 
 if args.what in ("nttlarge",):
-    P = 2013265921
+    P = int(os.environ.get("PROBE_P", "2013265921"))
+    G = {2013265921: 31, 469762049: 3, 998244353: 3}[P]
     ctx = m.ctx_init(P)
-    for log_n in ((args.logn,) if args.logn else (20, 22, 23, 24, 25, 26, 27)):
+    for log_n in ((args.logn,) if args.logn else tuple(k for k in (20, 22, 23, 24, 25, 26, 27) if (P - 1) % (1 << k) == 0)):
         N = 1 << log_n
-        w = pow(31, (P - 1) // N, P)
+        w = pow(G, (P - 1) // N, P)
         plan = m.ntt_plan(ctx, w, log_n)
         x = torch.empty(N, dtype=torch.uint32, device=dev)
         m.synth_fill(x, 42, 5, 0, P)
