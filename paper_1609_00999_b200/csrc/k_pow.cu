@@ -6,9 +6,10 @@
 // one to_mont, ~46 Montgomery products held in registers, one from_mont.
 // The kernel is bound by the integer-multiply (FMAHeavy) pipe, not HBM
 // (12 B per ~48 REDCs).  B200 design choices:
-//   * signed lazy REDC (mont_core.cuh sredc): 3 FMAHeavy ops per product
-//     (IMAD.WIDE, IMAD, IMAD.WIDE), values stay in (-P, P) with no correction
-//     inside the chain;
+//   * signed lazy REDC (mont_core.cuh sredc): 3 FMAHeavy instructions per
+//     product (IMAD.WIDE, IMAD, IMAD.WIDE = 5 issue slots: high-word products
+//     are half rate on B200), values stay in (-P, P) with no correction inside
+//     the chain;
 //   * per-lane exponents would make a bitwise if() diverge inside a warp, so
 //     the ladder is a fixed 2-bit window (variant 0): every lane executes the
 //     same 2 + 15*3 = 47 products and picks its multiplier x^d (d in 0..3,
@@ -16,7 +17,12 @@
 //     (6 + 10*4 = 46 products, 8-way select); variant 1 the binary ladder with
 //     selects (64 products, reference point);
 //   * each thread runs the 4 independent ladders of one uint4 interleaved
-//     (instruction-level parallelism covers the ~20-cycle dependent latency).
+//     (instruction-level parallelism covers the ~20-cycle dependent latency);
+//     variant 10 runs 8 (two uint4), which saturates the pipe with fewer
+//     resident CTAs -- bench.py's two-lane step uses it at 2 CTAs/SM;
+//   * measured alternatives kept as variants: 3/4 = the window table in shared
+//     memory, 5-8 = some lanes as FP64 Barrett products on the FP64 pipe,
+//     9 = PAPER.md Alg. 3 (Fourier-prime REDC) products.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
