@@ -100,8 +100,8 @@ mont_status_t mont_mul_vec(const mont_ctx_t *ctx, uint32_t *c, const uint32_t *a
  * flat 128-bit stream and the table is read through the read-only (L1) path,
  * where it stays resident; for other len the table is staged per CTA into
  * shared memory by the bulk-copy (TMA) engine, cp.async.bulk + mbarrier
- * (mont_mul_twiddle_ex variant 0 forces that path; DESIGN.md §6 has both
- * measured).  Requires len >= 1 when batch > 0.  x and out are batch*len
+ * (mont_mul_twiddle_ex variant 4 forces that path for any len; DESIGN.md §6
+ * has both measured).  Requires len >= 1 when batch > 0.  x and out are batch*len
  * elements; out may alias x.  8 bytes of HBM traffic per element. */
 mont_status_t mont_mul_twiddle(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *x,
                                const uint32_t *tw, size_t batch, size_t len, cudaStream_t stream);

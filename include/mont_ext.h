@@ -19,7 +19,8 @@ extern "C" {
  *   threads   : threads per CTA (multiple of 32, <= 1024)
  *   ctas_per_sm: CTAs per SM for the persistent grid (grid = SMs * ctas_per_sm)
  *   unroll    : 128-bit chunks per thread per loop trip (1, 2, 4 or 8)
- *   variant   : kernel variant (kernel-specific; 0 = default).
+ *   variant   : kernel variant (kernel-specific; 0 = the library default, which
+ *               for every kernel but mont_mul_twiddle_ex is variant 0 itself).
  *                 mont_mul_vec_ex, mont_mul_vec_checksum_ex, to_mont_ex,
  *                 from_mont_ex, mb_triad, mb_copy : 0 = flat grid (one
  *                                   tile of threads*unroll uint4 per CTA),
@@ -35,9 +36,10 @@ extern "C" {
  *                                   warps stream at full bandwidth
  *                                   (variants 2 and 3: 16-byte co-aligned
  *                                   operands, else the 32-bit path)
- *                 mont_pow_vec_ex : 0 = 2-bit fixed window, table in
- *                                   registers; 1 = binary ladder with
- *                                   selects; 2 = 3-bit window, registers;
+ *                 mont_pow_vec_ex : 0 = library default: 11 when base, exp
+ *                                   and out share their address mod 16, else
+ *                                   17;  1 = binary ladder with selects;
+ *                                   2 = 3-bit window, registers;
  *                                   3 = 2-bit window, table in shared memory;
  *                                   4 = 3-bit window, shared memory;
  *                                   5/6/7/8 = 2-bit window with 3/2/1/0 of
@@ -45,19 +47,37 @@ extern "C" {
  *                                   rest as FP64 Barrett products on the
  *                                   FP64 pipe; 9 = 2-bit window with
  *                                   Fourier-prime REDC products (PAPER.md
- *                                   Alg. 3; P = c 2^n + 1, 2n >= 32,
- *                                   3P < 2^32, 16-byte aligned operands,
+ *                                   Alg. 3; P = c 2^n + 1, 2n >= 32, with
+ *                                   t held in 33 bits when 3P >= 2^32 --
+ *                                   DESIGN.md G8; 16-byte aligned operands,
  *                                   else MONT_EUNSUPPORTED / EINVAL_ARG);
- *                                   10 = variant 0 with 8 lanes (two uint4)
- *                                   per thread.
+ *                                   10 = variant 17 with 8 lanes (two uint4)
+ *                                   per thread; 11 = 2-bit window, 8 lanes
+ *                                   per thread, P a compile-time constant for
+ *                                   the config primes 469762049, 998244353,
+ *                                   2013265921 (run time otherwise);
+ *                                   12 = 11 with 2 of the 8 lanes as FP64
+ *                                   Barrett products; 13 = 11 with
+ *                                   precomputed-quotient (Shoup) window
+ *                                   multiplies; 14 = 13 + 2 FP64 lanes;
+ *                                   15 / 16 = 11 / 13 with P at run time;
+ *                                   (11-16 need 16-byte co-aligned operands,
+ *                                   else they run 17); 17 = 2-bit fixed
+ *                                   window, 4 lanes per thread, table in
+ *                                   registers (any alignment).
  *                                   ctas_per_sm = 0 selects a flat grid.
- *                 mont_mul_twiddle_ex : 0 = bulk-copy (TMA) staged table,
+ *                 mont_mul_twiddle_ex : 0 = library default: 2 for power-of-two
+ *                                   len, else 4;
  *                                   1 = table read through L1/L2 (no smem),
- *                                   2 = flat stream (power-of-two len; else 0),
+ *                                   2 = flat stream (power-of-two len; else 4),
  *                                   3 = whole table staged once per CTA
  *                                   by TMA + cluster-launch-control work
  *                                   stealing over 2-row items (4 len <=
- *                                   200 KiB; else 0)
+ *                                   200 KiB; else 4),
+ *                                   4 = table chunk staged per CTA by the
+ *                                   bulk-copy (TMA) engine, cp.async.bulk +
+ *                                   mbarrier (any len; 256 threads unless
+ *                                   threads is set)
  *   chunk     : mont_mul_twiddle_ex only: table columns staged per CTA
  *               (multiple of 4; 0 = min(len, 4096)).                       */
 typedef struct mont_launch {
@@ -119,6 +139,37 @@ mont_status_t mb_copy(uint32_t *out, const uint32_t *in, size_t n, const mont_la
                       cudaStream_t stream);
 mont_status_t mb_imad(uint32_t *sink, int kind, int iters, const mont_launch_t *cfg, cudaStream_t stream,
                       unsigned long long *threads_launched);
+
+/* mb_pipe: per-instruction issue-rate microbenchmark (csrc/k_pipes.cu).  Every thread runs 8
+ *   independent dependency chains in which each instruction consumes the previous result as a
+ *   register operand (nothing loop-invariant for ptxas to hoist), `iters` loop trips of
+ *   mb_pipe_ops_per_iter(kind) = 128 timed instructions.  kind: 0 IMAD R,R,R; 1 IMAD R,R,imm;
+ *   2 IMAD R,R,UR (kernel parameter); 3 IMAD.HI R,R,R; 4 IMAD.HI R,R,imm; 5 IMAD.WIDE R,R,R;
+ *   6 IMAD.WIDE + IMAD.HI 1:1; 7 IMAD.WIDE + IMAD 1:1; 8 add.u32 (ptxas: half IADD3 on the ALU,
+ *   half IMAD.IADD on FMAHeavy); 9 LOP3; 10 SEL; 11 VIMNMX; 12 SHF; 13 FFMA R,R,R;
+ *   14 FFMA R,R,imm; 15 DFMA; mixes 1:1 -- 16 IMAD.WIDE + FFMA, 17 IMAD.WIDE + IADD3,
+ *   18 IMAD.WIDE + DFMA, 19 IMAD.WIDE + IMAD imm, 20 IMAD + FFMA, 21 IMAD + IADD3,
+ *   22 IMAD.WIDE + LOP3, 23 IMAD + IMAD imm, 24 IMAD + DFMA, 25 IMAD.WIDE + DMUL,
+ *   26 IMAD.WIDE + DADD; modular products (counted as products, not instructions) --
+ *   27 the library's chain REDC (sredc), 28 the FP64 Barrett product (fmulmod), 29 REDC +
+ *   fmulmod 1:1, 30 REDC + fmulmod 3:1; 31 DMUL, 32 DADD, 33 IMAD + DMUL; warp-specialised
+ *   products, warps 4-7 of each CTA on fmulmod and 0-3 on REDC (one of each per SMSP) -- 34 equal
+ *   trip counts; 35, 36, 37: the FP64 warps run 2/3, 1/2, 1/3 of the trips, so their products are
+ *   2/5, 1/3, 1/4 of the total (the caller counts threads * (iters + fp_iters) / 2 * 128).
+ *   Warp-specialised instruction pairs (by hardware warp slot, %warpid, so both kinds share
+ *   every SMSP; equal trips): 38 IMAD.WIDE / DFMA, 39 IMAD.WIDE / DMUL, 40 REDC / DFMA,
+ *   41 IMAD.WIDE / fmulmod (counted as instructions; 40 and 41 count one REDC or fmulmod as
+ *   one).  42: no work; sink[t] = the %warpid of thread t's warp.  43-48: NI REDC + NF
+ *   fmulmod chains per thread interleaved instruction by instruction, (NI, NF) = (1,1), (3,1),
+ *   (6,2), (2,0), (0,2), (4,0); mb_pipe_ops_per_iter = 32 (NI + NF) products.
+ *   kind outside [0, 49) is MONT_EINVAL_ARG.
+ *   grid = SMs * ctas_per_sm (cfg may be NULL: 8), 256 threads; sink holds one word per
+ *   thread.  Executed instructions = threads * iters * 128.  If clk (a DEVICE pointer to 2
+ *   uint64) is not NULL, CTA 0 stores its elapsed SM cycles (clock64) and nanoseconds
+ *   (%globaltimer) there: their ratio is the SM clock the kernel actually ran at. */
+mont_status_t mb_pipe(uint32_t *sink, int kind, int iters, const mont_launch_t *cfg, cudaStream_t stream,
+                      unsigned long long *threads_launched, unsigned long long *clk);
+int mb_pipe_ops_per_iter(int kind);
 
 /* Number of SMs of the current device (cached per device), or -1. */
 int mont_sm_count(void);

@@ -243,12 +243,22 @@ def mod_sub(a: int, b: int, P: int) -> int:
 # NTT by definition -----------------------------------
 
 def dft(P: int, w: int, x) -> np.ndarray:
-    """X[k] = sum_j x[j] w^(jk) mod P for each row of x (O(N^2) per row)."""
+    """X[k] = sum_j x[j] w^(jk) mod P for each row of x (O(N^2) per row).  Rows run on a thread
+    pool (ctypes releases the GIL in the C call): slicing only, the arithmetic is oracle_dft's."""
+    from concurrent.futures import ThreadPoolExecutor
     x = _u32(x)
-    rows = x.reshape(-1, x.shape[-1])
+    rows = np.ascontiguousarray(x.reshape(-1, x.shape[-1]))
     out = np.empty_like(rows)
-    for r in range(rows.shape[0]):
-        lib().oracle_dft(P, w, np.ascontiguousarray(rows[r]), out[r], rows.shape[1])
+    L = lib()
+
+    def one(r):
+        L.oracle_dft(P, w, rows[r], out[r], rows.shape[1])
+
+    if rows.shape[0] == 1:
+        one(0)
+    else:
+        with ThreadPoolExecutor(max_workers=min(rows.shape[0], os.cpu_count() or 1)) as ex:
+            list(ex.map(one, range(rows.shape[0])))
     return out.reshape(x.shape)
 
 

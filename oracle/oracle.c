@@ -16,7 +16,7 @@
  *   inverse map         from_mont(x) = x*R^-1 mod P
  *   twiddle product     out[r][j] = x[r][j]*tw[j]*R^-1 mod P     (BASELINE configs[2])
  *   modular power       base^exp mod P, left-to-right square-and-multiply on
- *                       plain values over 31 exponent bits       (BASELINE configs[3])
+ *                       plain values over the 32 exponent bits   (BASELINE configs[3])
  *   checksum            (sum_i c[i]) mod P                       (BASELINE configs[4])
  *
  * R^-1 and P' come from the extended Euclidean algorithm, as PAPER.md:89 says
@@ -125,14 +125,15 @@ uint32_t oracle_from_mont1(const oracle_ctx_t *c, uint32_t x)
     return mulmod_naive(x % c->P, c->Rinv, c->P);
 }
 
-/* base^exp mod P on plain values: left-to-right square-and-multiply over the
- * 31 exponent bits 30..0, naive '%' (BASELINE configs[3]; DESIGN.md reading
- * G10: 0^0 = 1). */
+/* base^exp mod P on plain values: left-to-right square-and-multiply over all
+ * 32 exponent bits 31..0, naive '%' (BASELINE configs[3] draws 31-bit
+ * exponents; the product's contract, include/mont.h, takes any uint32
+ * exponent; reading G10: 0^0 = 1). */
 uint32_t oracle_pow1(uint32_t P, uint32_t base, uint32_t exp)
 {
     uint32_t acc = 1u % P;
     uint32_t x = base % P;
-    for (int bit = 30; bit >= 0; --bit) {
+    for (int bit = 31; bit >= 0; --bit) {
         acc = mulmod_naive(acc, acc, P);
         if ((exp >> bit) & 1u) acc = mulmod_naive(acc, x, P);
     }

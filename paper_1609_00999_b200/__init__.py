@@ -75,6 +75,8 @@ SIGNATURES = {
     "mb_triad": (C.c_int, [_P, _P, _P, _S, _LAUNCH, _P]),
     "mb_copy": (C.c_int, [_P, _P, _S, _LAUNCH, _P]),
     "mb_imad": (C.c_int, [_P, C.c_int, C.c_int, _LAUNCH, _P, C.POINTER(C.c_ulonglong)]),
+    "mb_pipe": (C.c_int, [_P, C.c_int, C.c_int, _LAUNCH, _P, C.POINTER(C.c_ulonglong), _P]),
+    "mb_pipe_ops_per_iter": (C.c_int, [C.c_int]),
     "mont_sm_count": (C.c_int, []),
     # include/mont_host.h
     "mont_host_min_workspace": (C.c_size_t, [C.c_int, C.c_size_t]),

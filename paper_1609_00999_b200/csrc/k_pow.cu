@@ -323,16 +323,17 @@ __global__ void __launch_bounds__(256) k_pow_barrett(BarrettDev c, uint32_t *out
 }
 
 // ---- Fourier-prime REDC ladder (variant 9): the same 2-bit window with every
-// product an Alg. 3 REDC (identical results to the Montgomery ladder)
-template <int L>
+// product an Alg. 3 REDC (identical results to the Montgomery ladder); WIDE = the 33-bit-t
+// form for 3P >= 2^32 (mont_core.cuh fredc33)
+template <int L, bool WIDE>
 __device__ __forceinline__ void pow_fourier(const PowParams &q, const FourierDev &f, const uint32_t (&base)[L],
                                             const uint32_t (&e)[L], uint32_t (&out)[L]) {
     uint32_t t1[L], t2[L], t3[L], acc[L];
 #pragma unroll
     for (int l = 0; l < L; ++l) {
         t1[l] = redc(base[l], q.r2, (uint32_t)q.p, (uint32_t)q.pinv);  // to_mont, any uint32 base
-        t2[l] = fredc(t1[l], t1[l], f);
-        t3[l] = fredc(t2[l], t1[l], f);
+        t2[l] = WIDE ? fredc33(t1[l], t1[l], f) : fredc(t1[l], t1[l], f);
+        t3[l] = WIDE ? fredc33(t2[l], t1[l], f) : fredc(t2[l], t1[l], f);
         const uint32_t d = e[l] >> 30;
         acc[l] = d == 0 ? q.r1 : d == 1 ? t1[l] : d == 2 ? t2[l] : t3[l];
     }
@@ -340,18 +341,19 @@ __device__ __forceinline__ void pow_fourier(const PowParams &q, const FourierDev
     for (int sh = 28; sh >= 0; sh -= 2) {
 #pragma unroll
         for (int l = 0; l < L; ++l) {
-            uint32_t a = fredc(acc[l], acc[l], f);
-            a = fredc(a, a, f);
+            uint32_t a = WIDE ? fredc33(acc[l], acc[l], f) : fredc(acc[l], acc[l], f);
+            a = WIDE ? fredc33(a, a, f) : fredc(a, a, f);
             const uint32_t d = (e[l] >> sh) & 3u;
             const uint32_t lo = (d & 1u) ? t1[l] : q.r1;
             const uint32_t hi = (d & 1u) ? t3[l] : t2[l];
-            acc[l] = fredc(a, (d & 2u) ? hi : lo, f);
+            acc[l] = WIDE ? fredc33(a, (d & 2u) ? hi : lo, f) : fredc(a, (d & 2u) ? hi : lo, f);
         }
     }
 #pragma unroll
     for (int l = 0; l < L; ++l) out[l] = redc1(acc[l], (uint32_t)q.p, (uint32_t)q.pinv);
 }
 
+template <bool WIDE>
 __global__ void __launch_bounds__(256) k_pow_fourier(PowParams q, FourierDev f, uint32_t *out, const uint32_t *base,
                                                       const uint32_t *exp, size_t n) {
     const size_t n4 = n / 4;
@@ -360,12 +362,12 @@ __global__ void __launch_bounds__(256) k_pow_fourier(PowParams q, FourierDev f, 
         const uint4 bv = ld_stream(reinterpret_cast<const uint4 *>(base) + i);
         const uint4 ev = ld_stream(reinterpret_cast<const uint4 *>(exp) + i);
         uint32_t b[4] = {bv.x, bv.y, bv.z, bv.w}, e[4] = {ev.x, ev.y, ev.z, ev.w}, o[4];
-        pow_fourier<4>(q, f, b, e, o);
+        pow_fourier<4, WIDE>(q, f, b, e, o);
         st_stream(reinterpret_cast<uint4 *>(out) + i, make_uint4(o[0], o[1], o[2], o[3]));
     } else if (i < n4 + (n & 3)) {
         const size_t j = 4 * n4 + (i - n4);
         uint32_t b[1] = {base[j]}, e[1] = {exp[j]}, o[1];
-        pow_fourier<1>(q, f, b, e, o);
+        pow_fourier<1, WIDE>(q, f, b, e, o);
         out[j] = o[0];
     }
 }
@@ -417,6 +419,9 @@ static const Launch kPowDefault{256, 0, 1, 0, 0};
 
 using namespace mont;
 
+mont_status_t mont_pow2_launch(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *base, const uint32_t *exp,
+                               size_t n, int variant, int ctas_per_sm, int sms, cudaStream_t stream);  // k_pow2.cu
+
 extern "C" mont_status_t mont_pow_vec_ex(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *base,
                                          const uint32_t *exp, size_t n, const mont_launch_t *cfg,
                                          cudaStream_t stream) {
@@ -424,11 +429,19 @@ extern "C" mont_status_t mont_pow_vec_ex(const mont_ctx_t *ctx, uint32_t *out, c
     if (n == 0) return MONT_OK;
     if (!out || !base || !exp || ((uintptr_t)out | (uintptr_t)base | (uintptr_t)exp) & 3u) return MONT_EINVAL_ARG;
     Launch L = resolve(cfg, kPowDefault);
-    if (L.threads != 256 || L.variant < 0 || L.variant > 10 || L.ctas_per_sm < 0) return MONT_EINVAL_ARG;
+    if (L.threads != 256 || L.variant < 0 || L.variant > 17 || L.ctas_per_sm < 0) return MONT_EINVAL_ARG;
     const int sms = sm_count();
     if (sms <= 0) return MONT_ECUDA;
     const PowParams q{(int32_t)ctx->p, (int32_t)(0u - ctx->pneg), ctx->r1, ctx->r2, (double)ctx->p, 1.0 / (double)ctx->p};
-    if (L.variant == 10 && same_mod16((uintptr_t)base, (uintptr_t)exp) && same_mod16((uintptr_t)base, (uintptr_t)out)) {
+    const bool co16 = same_mod16((uintptr_t)base, (uintptr_t)exp) && same_mod16((uintptr_t)base, (uintptr_t)out);
+    // variant 0 = the library default: variant 11 (8 lanes per thread, P specialised for the
+    // config primes; measured fastest) when the operands are 16-byte co-aligned,
+    // else the 4-lane 2-bit window (variant 17, round 1's default), which takes any alignment
+    if (L.variant == 0) L.variant = co16 ? 11 : 17;
+    if (L.variant >= 11 && L.variant <= 16 && co16)
+        return mont_pow2_launch(ctx, out, base, exp, n, L.variant, L.ctas_per_sm, sms, stream);
+    if (L.variant >= 11) L.variant = 0;  // 17, or misaligned operands: the 4-lane kernel
+    if (L.variant == 10 && co16) {
         const uint32_t head = head_elems((uintptr_t)base, n);
         const size_t n4 = (n - head) / 4;
         const uint32_t tail = (uint32_t)((n - head) % 4);
@@ -441,16 +454,19 @@ extern "C" mont_status_t mont_pow_vec_ex(const mont_ctx_t *ctx, uint32_t *out, c
         return launch_status();
     }
     if (L.variant == 10) L.variant = 0;  // misaligned operands: the 4-lane kernel handles them
-    if (L.variant == 9) {  // Fourier-prime REDC ladder: P = c 2^n + 1, 2n >= 32, 3P < 2^32
+    if (L.variant == 9) {  // Fourier-prime REDC ladder: P = c 2^n + 1, 2n >= 32
         uint32_t nn = 0, cc = ctx->p - 1u;
         while ((cc & 1u) == 0u) { cc >>= 1; ++nn; }
-        if (2 * nn < 32 || (uint64_t)ctx->p * 3u >= (1ull << 32)) return MONT_EUNSUPPORTED;
+        if (2 * nn < 32) return MONT_EUNSUPPORTED;
         if (((uintptr_t)out | (uintptr_t)base | (uintptr_t)exp) & 15u) return MONT_EINVAL_ARG;
         const FourierDev f{ctx->p, cc, nn, cc << (2 * nn - 32)};
         const size_t threads = n / 4 + (n & 3);
         const size_t grid = (threads + 255) / 256;
         if (grid > 0x7fffffff) return MONT_EUNSUPPORTED;
-        k_pow_fourier<<<(unsigned)grid, 256, 0, stream>>>(q, f, out, base, exp, n);
+        if ((uint64_t)ctx->p * 3u >= (1ull << 32))  // t + P would not fit 32 bits: 33-bit t
+            k_pow_fourier<true><<<(unsigned)grid, 256, 0, stream>>>(q, f, out, base, exp, n);
+        else
+            k_pow_fourier<false><<<(unsigned)grid, 256, 0, stream>>>(q, f, out, base, exp, n);
         return launch_status();
     }
     switch (L.variant) {

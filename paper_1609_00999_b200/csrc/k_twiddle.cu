@@ -200,9 +200,10 @@ __global__ void __launch_bounds__(256) k_twiddle_scalar(Ctx c, uint32_t *out, co
 // B200 sweeps: for power-of-two rows the flat stream with the
 // table through L1 (variant 2, 512 threads x 4 uint4) runs at the to_mont rate
 // (82 us for configs[2], 1.0x the measured copy peak); the bulk-copy staged
-// table (variant 0) peaks at 84-86 us with many small CTAs (64 per SM, a few
-// rows and a 4096-column chunk each) and is the path for other row lengths.
-static const Launch kTwDefault{512, 64, 4, 2, 4096};
+// table (variant 4) peaks at 84-86 us with many small CTAs (64 per SM, 256
+// threads, a few rows and a 4096-column chunk each) and is the path for other
+// row lengths.  Variant 0 = that choice (mont_ext.h).
+static const Launch kTwDefault{512, 64, 4, 0, 4096};
 
 template <int U, bool TMA>
 static mont_status_t launch_tw(const Ctx &c, uint32_t *out, const uint32_t *x, const uint32_t *tw, size_t batch,
@@ -245,7 +246,7 @@ extern "C" mont_status_t mont_mul_twiddle_ex(const mont_ctx_t *ctx, uint32_t *ou
     Launch L = resolve(cfg, kTwDefault);
     if (L.threads < 32 || L.threads > 512 || (L.threads & 31) || L.ctas_per_sm < 1 || L.chunk < 4 ||
         (L.chunk & 3) || !(L.unroll == 1 || L.unroll == 2 || L.unroll == 4 || L.unroll == 8) || L.variant < 0 ||
-        L.variant > 3)
+        L.variant > 4)
         return MONT_EINVAL_ARG;
     const int sms = sm_count();
     if (sms <= 0) return MONT_ECUDA;
@@ -260,7 +261,10 @@ extern "C" mont_status_t mont_mul_twiddle_ex(const mont_ctx_t *ctx, uint32_t *ou
         k_twiddle_scalar<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, stream>>>(c, out, x, tw, batch, len);
         return launch_status();
     }
-    if (L.variant == 3 && len * 4 <= 200 * 1024) {  // staged once per CTA + CLC work stealing
+    const bool pow2 = (len & (len - 1)) == 0;
+    int v = L.variant;
+    if (v == 0) v = pow2 ? 2 : 4;  // library default
+    if (v == 3 && len * 4 <= 200 * 1024) {  // staged once per CTA + CLC work stealing
         const uint32_t rows_per_item = 2u;
         const size_t items = (batch + rows_per_item - 1) / rows_per_item;
         const size_t smem = len * 4;
@@ -271,8 +275,8 @@ extern "C" mont_status_t mont_mul_twiddle_ex(const mont_ctx_t *ctx, uint32_t *ou
         k_twiddle_clc<<<(unsigned)items, 512, smem, stream>>>(c, out, x, tw, batch, len, rows_per_item);
         return launch_status();
     }
-    if (L.variant == 3) L.variant = 0;
-    if (L.variant == 2 && (len & (len - 1)) == 0) {  // flat stream, power-of-two rows
+    if (v == 3) v = 4;
+    if (v == 2 && pow2) {  // flat stream, power-of-two rows
         const size_t n4 = batch * len / 4;
         const size_t tile = (size_t)L.unroll * L.threads;
         const size_t grid = (n4 + tile - 1) / tile;
@@ -285,11 +289,9 @@ extern "C" mont_status_t mont_mul_twiddle_ex(const mont_ctx_t *ctx, uint32_t *ou
         }
         return launch_status();
     }
-    if (L.variant == 2) {  // not a power of two: the staged-table kernel with its own best shape
-        L.variant = 0;
-        if (!cfg || cfg->threads == 0) L.threads = 256;
-    }
-    if (L.variant == 0) {
+    if (v == 2) v = 4;  // not a power of two: the staged-table kernel
+    if (v == 4) {       // table chunk staged per CTA by cp.async.bulk (TMA engine) + mbarrier
+        if (!cfg || cfg->threads == 0) L.threads = 256;  // its own best shape
         switch (L.unroll) {
             case 1: return launch_tw<1, true>(c, out, x, tw, batch, len, L, sms, stream);
             case 2: return launch_tw<2, true>(c, out, x, tw, batch, len, L, sms, stream);
@@ -297,6 +299,7 @@ extern "C" mont_status_t mont_mul_twiddle_ex(const mont_ctx_t *ctx, uint32_t *ou
             default: return launch_tw<8, true>(c, out, x, tw, batch, len, L, sms, stream);
         }
     }
+    // v == 1: table read through L1/L2, no shared memory
     switch (L.unroll) {
         case 1: return launch_tw<1, false>(c, out, x, tw, batch, len, L, sms, stream);
         case 2: return launch_tw<2, false>(c, out, x, tw, batch, len, L, sms, stream);

@@ -213,6 +213,24 @@ __device__ __forceinline__ uint32_t fredc(uint32_t a, uint32_t b, const FourierD
     return umin(t, t - f.p);
 }
 
+// The same Alg. 3 product for any P = c 2^n + 1 < 2^31 with 2n >= 32, including 3P >= 2^32
+// (P0 = 15 2^27 + 1), where t = q1 - q2 + q3 in [-(P-1), 2(P-1)] spans more than
+// 2^32 values: t is held as a 33-bit quantity, the non-negative part s = q1 + q3 in [0, 2P)
+// (q1 = hi(ab) < P, q3 = c v 2^(2n-32) < c 2^n < P) and the sign of s - q2 (DESIGN.md reading
+// G8: the paper's 32-bit signed t with the mask step t + (t >> 31) & P is
+// wrong for P > 2^30).  s < q2: t = s - q2 in (-P, 0), canonical t + P; else t in [0, 2P),
+// one conditional subtract.
+__device__ __forceinline__ uint32_t fredc33(uint32_t a, uint32_t b, const FourierDev &f) {
+    const uint64_t T = mul_wide_u32(a, b);
+    const uint32_t q1 = hi32(T), r1 = (uint32_t)T;
+    const uint64_t u = mul_wide_u32(r1, f.c);
+    const uint32_t q2 = (uint32_t)(u >> (32 - f.n));
+    const uint32_t v = (uint32_t)u & ((1u << (32 - f.n)) - 1u);
+    const uint32_t s = q1 + v * f.c_sh;          // q1 + q3 in [0, 2P)
+    const uint32_t d = s - q2;                   // t mod 2^32
+    return s < q2 ? d + f.p : umin(d, d - f.p);
+}
+
 }  // namespace mont
 
 namespace mont {

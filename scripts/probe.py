@@ -69,6 +69,67 @@ if args.what in ("all", "imad"):
             out(what="imad", kind=names[kind], ctas_per_sm=ctas, ops=ops, sec=med,
                 gops=ops / med / 1e9, per_sm_per_clk_at_1965=ops / med / sms / 1.965e9)
 
+if args.what == "pipes":
+    # mb_pipe (csrc/k_pipes.cu): per-instruction rates from dependent chains nothing can hoist.
+    # Reports lanes/clk/SM at the SM clock nvidia-smi shows right after each kind (the kernel runs
+    # ~50-100 ms so the clock settles), and at the max clock.
+    import ctypes as C
+    import subprocess
+    names = {0: "IMAD R,R,R", 1: "IMAD R,R,imm", 2: "IMAD R,R,UR", 3: "IMAD.HI R,R,R", 4: "IMAD.HI R,R,imm",
+             5: "IMAD.WIDE R,R,R", 6: "IMAD.WIDE+IMAD.HI 1:1", 7: "IMAD.WIDE+IMAD 1:1",
+             8: "add.u32 (IADD3 / IMAD.IADD split)", 9: "LOP3", 10: "SEL", 11: "VIMNMX", 12: "SHF",
+             13: "FFMA R,R,R", 14: "FFMA R,R,imm", 15: "DFMA", 16: "IMAD.WIDE+FFMA 1:1",
+             17: "IMAD.WIDE+IADD3 1:1", 18: "IMAD.WIDE+DFMA 1:1", 19: "IMAD.WIDE+IMAD imm 1:1",
+             20: "IMAD+FFMA 1:1", 21: "IMAD+IADD3 1:1", 22: "IMAD.WIDE+LOP3 1:1", 23: "IMAD+IMAD imm 1:1",
+             24: "IMAD+DFMA 1:1", 25: "IMAD.WIDE+DMUL 1:1", 26: "IMAD.WIDE+DADD 1:1", 27: "sredc (products)",
+             28: "fmulmod (products)", 29: "sredc+fmulmod 1:1 (products)", 30: "sredc+fmulmod 3:1 (products)",
+             31: "DMUL", 32: "DADD", 33: "IMAD+DMUL 1:1", 34: "warp-specialised 1/2 fmulmod (products)",
+             35: "warp-specialised 2/5 fmulmod (products)", 36: "warp-specialised 1/3 fmulmod (products)",
+             37: "warp-specialised 1/4 fmulmod (products)", 38: "warps IMAD.WIDE | DFMA",
+             39: "warps IMAD.WIDE | DMUL", 40: "warps sredc | DFMA (ops)", 41: "warps IMAD.WIDE | fmulmod (ops)",
+             43: "in-warp 1 sredc : 1 fmulmod chains", 44: "in-warp 3:1", 45: "in-warp 6:2", 46: "2 sredc chains",
+             47: "2 fmulmod chains", 48: "4 sredc chains"}
+    sink = torch.empty(sms * 32 * 256, dtype=torch.uint32, device=dev)
+    clkbuf = torch.zeros(2, dtype=torch.int64, device=dev)
+
+    def smi_clock():
+        try:
+            o = subprocess.run(["nvidia-smi", "-i", "0", "--query-gpu=clocks.sm", "--format=csv,noheader,nounits"],
+                               capture_output=True, text=True, timeout=10).stdout.strip()
+            return float(o.split()[0])
+        except Exception:
+            return None
+
+    kinds = [int(k) for k in os.environ.get("PROBE_KINDS", "").split(",") if k] or list(range(42)) + list(range(43, 49))
+    if os.environ.get("PROBE_SLOTS"):
+        nthr = C.c_ulonglong(0)
+        lib().mb_pipe(sink.data_ptr(), 42, 1, C.byref(m.Launch(ctas_per_sm=8)), s.cuda_stream, C.byref(nthr), None)
+        torch.cuda.synchronize()
+        sl = sink[:nthr.value].view(-1, 256)[:, ::32].cpu().numpy().tolist()
+        out(what="warp_slots", first_ctas=sl[:6], note="per CTA: %warpid of warps 0..7")
+    for kind in kinds:
+        for ctas in (4, 8):
+            iters = int(os.environ.get("PROBE_ITERS", "3000"))
+            nthr = C.c_ulonglong(0)
+            cfg = m.Launch(ctas_per_sm=ctas)
+
+            def f():
+                st = lib().mb_pipe(sink.data_ptr(), kind, iters, C.byref(cfg), s.cuda_stream, C.byref(nthr),
+                                   clkbuf.data_ptr())
+                assert st == 0
+
+            med, best = timeit(f, reps=7)
+            cyc, ns = (int(v) for v in clkbuf.tolist())
+            mhz = cyc / ns * 1e3 if ns else None   # CTA 0's clock64 / globaltimer over its lifetime
+            ops = nthr.value * iters * lib().mb_pipe_ops_per_iter(kind)
+            if kind in (35, 36, 37):  # the FP64 half of the warps runs fewer trips
+                fi = {35: iters * 2 // 3, 36: iters // 2, 37: iters // 3}[kind]
+                ops = nthr.value * (iters + fi) // 2 * lib().mb_pipe_ops_per_iter(kind)
+            out(what="pipe", kind=kind, name=names[kind], ctas_per_sm=ctas, ops=ops, sec=med,
+                gops=ops / med / 1e9, sm_mhz_in_kernel=mhz, smi_mhz_after=smi_clock(),
+                lanes_per_sm_clk=(ops / med / sms / (mhz * 1e6)) if mhz else None,
+                lanes_per_sm_clk_at_1965=ops / med / sms / 1.965e9)
+
 if args.what in ("all", "hbm"):
     import ctypes as C
     n = 1 << 26
@@ -125,7 +186,7 @@ if args.what in ("all", "tw"):
     x = x.view(batch, L)
     o = torch.empty_like(x)
     tw = m.twiddle_table(ctx, 1657000625, L)
-    for variant in (0, 1):
+    for variant in (4, 1):  # 4 = bulk-copy staged table chunk per CTA, 1 = table through L1/L2
         for ctas in (3, 8, 16, 32, 64):
             for unroll in (1, 2, 4):
                 for chunk in (2048, 4096, 16384):
@@ -153,12 +214,21 @@ if args.what in ("all", "pow"):
     pc = e.cpu().numpy()
     import numpy as np
     useful = int(31 * n + np.unpackbits(pc.view(np.uint8)).sum())
-    for variant in (0, 10, 2, 5, 6, 7, 8, 9):
-        for ctas in (0,):
-            cfg = m.Launch(variant=variant, ctas_per_sm=ctas)
-            med, best = timeit(lambda: m.pow_vec(ctx, base, e, out=o, cfg=cfg), reps=10)
-            out(what="pow", variant=variant, ctas=ctas, us=med * 1e6, useful_mulmods=useful,
-                tmulmod=useful / med / 1e12)
+    variants = [int(v) for v in os.environ.get("PROBE_POW_VARIANTS", "0,10,2,5,6,7,8,9").split(",")]
+    ctas_list = [int(v) for v in os.environ.get("PROBE_POW_CTAS", "0").split(",")]
+    primes = [int(v) for v in os.environ.get("PROBE_POW_PRIMES", str(P)).split(",")]
+    for Pp in primes:
+        ctx = m.ctx_init(Pp)
+        if Pp != P:
+            m.synth_fill(base, 42, 3, 0, Pp, mode=1)
+        ref = m.pow_vec(ctx, base, e, cfg=m.Launch(variant=0))
+        for variant in variants:
+            for ctas in ctas_list:
+                cfg = m.Launch(variant=variant, ctas_per_sm=ctas)
+                med, best = timeit(lambda: m.pow_vec(ctx, base, e, out=o, cfg=cfg), reps=10)
+                same = bool((o.view(torch.int32) == ref.view(torch.int32)).all())
+                out(what="pow", P=Pp, variant=variant, ctas=ctas, us=med * 1e6, us_best=best * 1e6,
+                    useful_mulmods=useful, tmulmod=useful / med / 1e12, equal_to_variant0=same)
 
 if args.what in ("pcie",):
     n = 1 << 26   # 256 MiB
@@ -341,9 +411,13 @@ if args.what in ("tw2",):
     cfg = m.Launch(variant=3)
     med, _ = timeit(lambda: m.mul_twiddle(ctx, x, tw, out=o, cfg=cfg))
     out(what="twiddle TMA-staged once + CLC work stealing (variant 3)", us=med * 1e6, gbs=8 * batch * L / med / 1e9)
-    cfg = m.Launch(variant=0, threads=256)
-    med, _ = timeit(lambda: m.mul_twiddle(ctx, x, tw, out=o, cfg=cfg))
-    out(what="twiddle TMA-staged per CTA (variant 0)", us=med * 1e6, gbs=8 * batch * L / med / 1e9)
+    for threads, ctas, unroll, chunk in [(256, 64, 4, 4096), (256, 32, 4, 4096), (256, 64, 2, 4096),
+                                         (512, 32, 4, 4096), (256, 16, 4, 16384), (512, 8, 4, 16384),
+                                         (256, 64, 4, 2048), (128, 64, 4, 4096)]:
+        cfg = m.Launch(variant=4, threads=threads, ctas_per_sm=ctas, unroll=unroll, chunk=chunk)
+        med, _ = timeit(lambda: m.mul_twiddle(ctx, x, tw, out=o, cfg=cfg))
+        out(what="twiddle TMA-staged per CTA (variant 4)", threads=threads, ctas=ctas, unroll=unroll, chunk=chunk,
+            us=med * 1e6, gbs=8 * batch * L / med / 1e9)
     for threads in (256, 512):
         for unroll in (1, 2, 4):
             cfg = m.Launch(threads=threads, unroll=unroll, variant=2)

@@ -86,14 +86,22 @@ def test_c2_fullsize_every_element(m, P):
 
 
 def test_c3_c4_fullsize_every_element(m):
-    """configs[2] and configs[3] at full size, every element against the oracle."""
+    """configs[2] and configs[3] at full size, every element against the oracle: the twiddle
+    multiply in the default path (flat stream, table through L1) AND in the bulk-copy (TMA)
+    staged-table path (mont_mul_twiddle_ex variant 4) -- north_star's "twiddle tables staged in
+    shared memory via TMA" at the configs[2] shape."""
     batch, L = 4096, 1 << 14
     hx = synth.c3_x(P0, batch=batch, length=L)
     w = oracle.root_of_unity(P0, synth.G11_GENERATOR, L)
     tw_ref = oracle.twiddle_table(P0, w, L)
     ctx = m.ctx_init(P0)
-    out = m.mul_twiddle(ctx, torch.from_numpy(hx).cuda(), m.twiddle_table(ctx, w, L))
-    assert np.array_equal(out.cpu().numpy(), oracle.twiddle(P0, hx, tw_ref))
+    ref = oracle.twiddle(P0, hx, tw_ref)
+    tx, ttw = torch.from_numpy(hx).cuda(), m.twiddle_table(ctx, w, L)
+    out = m.mul_twiddle(ctx, tx, ttw)
+    assert np.array_equal(out.cpu().numpy(), ref)
+    for v in (4, 3, 1):
+        out = m.mul_twiddle(ctx, tx, ttw, cfg=m.Launch(variant=v))
+        assert np.array_equal(out.cpu().numpy(), ref), v
     hb, he = synth.c4_inputs(P1, 0, 1 << 24)
     outp = m.pow_vec(m.ctx_init(P1), torch.from_numpy(hb).cuda(), torch.from_numpy(he).cuda())
     assert np.array_equal(outp.cpu().numpy(), oracle.power(P1, hb, he))
@@ -147,16 +155,17 @@ def test_c4_fullsize(m):
     assert np.array_equal(out.cpu().numpy()[idx], oracle.power(P1, hb, he))
 
 
-def test_c4_fullsize_lane_launch(m):
-    """configs[3] in the launch bench.py's two-lane step times (variant 10, 8 ladders per thread,
-    persistent grid of 2 CTAs per SM): sampled outputs against the oracle, and every element equal
-    to the default launch's."""
+@pytest.mark.parametrize("variant", [10, 11])
+def test_c4_fullsize_lane_launch(m, variant):
+    """configs[3] in the launches bench.py's two-lane step can time (variants 10 / 11, 8 ladders
+    per thread, persistent grid of 2 CTAs per SM): sampled outputs against the oracle, and every
+    element equal to the 4-lane kernel's (variant 17, a different kernel)."""
     n = 1 << 24
     ctx = m.ctx_init(P1)
     base = gen(n, 3, P1, 1, m=m)
     e = gen(n, 4, P1, 2, m=m)
-    out = m.pow_vec(ctx, base, e, cfg=m.Launch(ctas_per_sm=2, variant=10))
-    ref = m.pow_vec(ctx, base, e)
+    out = m.pow_vec(ctx, base, e, cfg=m.Launch(ctas_per_sm=2, variant=variant))
+    ref = m.pow_vec(ctx, base, e, cfg=m.Launch(variant=17))
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
     idx = sample_idx(n, 20_000)

@@ -70,13 +70,14 @@ def test_pow_any_modulus(m, P):
     n = 2053
     rng = np.random.default_rng(P + 1)
     base = rng.integers(0, P, n, dtype=np.uint64).astype(np.uint32)
-    exp = rng.integers(0, 1 << 31, n, dtype=np.uint64).astype(np.uint32)   # the oracle's 31-bit exponents
-    base[:3], exp[:3] = [0, P - 1, 1], [0, 0x7FFFFFFF, 0x7FFFFFFF]
+    exp = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)   # full 32-bit exponents
+    base[:3], exp[:3] = [0, P - 1, 1], [0, 0xFFFFFFFF, 0x7FFFFFFF]
     ctx = m.ctx_init(P)
     ref = oracle.power(P, base, exp)
     assert np.array_equal(host(m.pow_vec(ctx, dev(base), dev(exp))), ref)
-    lane = m.Launch(ctas_per_sm=2, variant=10)
-    assert np.array_equal(host(m.pow_vec(ctx, dev(base), dev(exp), cfg=lane)), ref)
+    for v in (10, 11, 13, 17):
+        lane = m.Launch(ctas_per_sm=2, variant=v)
+        assert np.array_equal(host(m.pow_vec(ctx, dev(base), dev(exp), cfg=lane)), ref), v
 
 
 @pytest.mark.parametrize("P", MODULI[::5])

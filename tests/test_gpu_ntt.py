@@ -7,7 +7,9 @@ import oracle
 import synth
 
 pytestmark = pytest.mark.gpu
-GEN = {2013265921: 31, 469762049: 3, 998244353: 3}
+# 1073479681 = 4095 * 2^18 + 1 sits just under 2^30, the tight end of the lazy [0, 2P) butterflies'
+# bound 4P < 2^32 (smallest primitive root 11); rows up to 2^15 and six-step transforms up to 2^18
+GEN = {2013265921: 31, 469762049: 3, 998244353: 3, 1073479681: 11}
 
 
 @pytest.fixture(scope="module")
@@ -50,6 +52,60 @@ def test_ntt_vs_dft(m, P, log_n, variant):
     assert np.array_equal(X, oracle.dft(P, w, x))
     m.ntt(ctx, d, twi, scale=ninv_m, variant=variant)
     assert np.array_equal(d.cpu().numpy(), x)
+
+
+@pytest.mark.parametrize("P", list(GEN))
+@pytest.mark.parametrize("log_n", [13, 14, 15])
+def test_ntt_full_rows_vs_dft(m, P, log_n):
+    """The 2^13..2^15 row kernels (their own instantiations, incl. the 2^14 rows the bench times) on
+    4 full rows per size and prime against the oracle's O(N^2) definition-DFT, in the default
+    (REDC twiddles) and the precomputed-quotient (variant 3) forms, plus the inverse round trip."""
+    N = 1 << log_n
+    rows = 4
+    ctx, w, winv, tw, twi, ninv_m = tables(m, P, N)
+    x = synth.uniform(42, 23, P, 0, rows * N).reshape(rows, N)
+    x[0, :3] = [P - 1, 0, P - 1]
+    x[1, -2:] = [P - 1, P - 1]
+    ref = oracle.dft(P, w, x)
+    for variant, (t, ti) in ((None, (tw, twi)), (3, pq_tables(m, ctx, w, winv, log_n))):
+        d = torch.from_numpy(x).cuda()
+        m.ntt(ctx, d, t, variant=variant)
+        assert np.array_equal(d.cpu().numpy(), ref), variant
+        m.ntt(ctx, d, ti, scale=ninv_m, variant=variant)
+        assert np.array_equal(d.cpu().numpy(), x), variant
+
+
+def test_ntt_non_lazy_path(tmp_path):
+    """MONT_NTT_NO_LAZY=1 (read once per process) forces the canonical butterflies for P < 2^30:
+    run in a subprocess, rows and a large transform against the oracle."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    code = """
+import numpy as np, torch, sys
+sys.path.insert(0, %r)
+import oracle, synth, paper_1609_00999_b200 as m
+ok = True
+for P, g in ((998244353, 3), (1073479681, 11), (469762049, 3)):
+    ctx = m.ctx_init(P)
+    for log_n in (5, 12, 14):
+        N = 1 << log_n
+        w = oracle.root_of_unity(P, g, N)
+        x = synth.uniform(42, 24, P, 0, 3 * N).reshape(3, N)
+        d = torch.from_numpy(x).cuda()
+        m.ntt(ctx, d, m.ntt_twiddles(ctx, w, log_n))
+        ok &= np.array_equal(d.cpu().numpy(), oracle.dft(P, w, x))
+    N = 1 << 16
+    w = oracle.root_of_unity(P, g, N)
+    x = synth.uniform(42, 25, P, 0, N)
+    X = m.ntt_large(ctx, torch.from_numpy(x).cuda(), m.ntt_plan(ctx, w, 16)).cpu().numpy()
+    ok &= all(int(X[k]) == oracle.dft_at(P, w, x, k) for k in (0, 1, 777, N - 1))
+sys.exit(0 if ok else 1)
+""" % str(root)
+    env = dict(__import__("os").environ, MONT_NTT_NO_LAZY="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
 
 
 @pytest.mark.parametrize("log_n", [13, 14, 15])

@@ -190,9 +190,11 @@ def test_to_mont_alignment_in_place(m, off_in, off_out):
 
 # --------------------------------------------------------------------- pow
 
-@pytest.mark.parametrize("P", PRIMES + (17, 257, 2147483647, 3))
-@pytest.mark.parametrize("variant", list(range(9)) + [10])
+@pytest.mark.parametrize("P", PRIMES + (17, 257, 2147483647, 3, 536870909, 536870923))
+@pytest.mark.parametrize("variant", list(range(9)) + list(range(10, 18)))
 def test_pow_parity(m, P, variant):
+    """Every ladder variant vs the oracle; 536870909 / 536870923 straddle 2^29, where variants
+    13, 14, 16 switch from lazy [0, 2P) Shoup outputs to one canonicalising subtract."""
     n = 20_003
     base = synth.uniform(42, synth.STREAM_BASE, P, 0, n, low=1) if P > 3 else \
         np.random.default_rng(0).integers(0, 3, n).astype(np.uint32)
@@ -204,22 +206,27 @@ def test_pow_parity(m, P, variant):
     assert np.array_equal(host(out), oracle.power(P, base, exp))
 
 
-def test_pow_full_32bit_exponents_and_big_bases(m):
-    """Header contract: any uint32 base (reduced mod P) and full 32-bit exponents."""
-    P = 998244353
+@pytest.mark.parametrize("P", [998244353, 469762049, 2013265921, 2147483647, 17])
+def test_pow_full_32bit_exponents_and_big_bases(m, P):
+    """Header contract: any uint32 base (reduced mod P) and full 32-bit exponents, every variant
+    (incl. Alg. 3 = 9 for the Fourier primes) against the oracle, whose ladder covers bits 31..0
+    (pinned by Python's pow and Fermat in tests/test_oracle.py)."""
     rng = np.random.default_rng(14)
     n = 9_999
     base = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
     exp = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
-    exp[:3] = [0xFFFFFFFF, 1 << 31, 0]
-    ref = np.array([pow(int(b), int(e), P) for b, e in zip(base, exp)], dtype=np.uint32)
-    for variant in range(9):
+    exp[:4] = [0xFFFFFFFF, 1 << 31, 0, (1 << 31) + 1]
+    base[:4] = [P - 1, 0xFFFFFFFF, 0, P]
+    ref = oracle.power(P, base, exp)
+    assert int(ref[0]) == pow(P - 1, 0xFFFFFFFF, P) and int(ref[1]) == pow(0xFFFFFFFF, 1 << 31, P)
+    variants = list(range(9)) + list(range(10, 18)) + ([9] if P in (998244353, 469762049, 2013265921) else [])
+    for variant in variants:
         out = m.pow_vec(m.ctx_init(P), dev(base), dev(exp), cfg=m.Launch(variant=variant))
         assert np.array_equal(host(out), ref), variant
 
 
 @pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6, 7, 8, 9, 12, 1000, 1 << 16 | 3, (1 << 16) + 4])
-@pytest.mark.parametrize("variant", [0, 5, 6, 10])
+@pytest.mark.parametrize("variant", [0, 5, 6, 10, 11, 12, 13, 14, 17])
 def test_pow_ragged_and_misaligned(m, n, variant):
     P = 469762049
     base, exp = synth.c4_inputs(P, 5, n)
@@ -248,7 +255,7 @@ def test_twiddle_table_parity(m, L):
 
 @pytest.mark.parametrize("batch,L", [(1, 4), (3, 8), (5, 1000), (17, 1024), (7, 16384), (3, 16388), (2, 40000),
                                      (1000, 64), (33, 4100), (513, 4), (4096, 2048)])
-@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
 def test_twiddle_parity(m, batch, L, variant):
     P = 2013265921
     x = synth.c3_x(P, batch=batch, length=L)
@@ -274,7 +281,8 @@ def test_twiddle_launch_configs(m, chunk, ctas, unroll, threads):
     batch, L = 37, 8192
     x = synth.c3_x(P, batch=batch, length=L)
     tw = synth.uniform(42, 11, P, 0, L)
-    cfg = m.Launch(threads=threads, ctas_per_sm=ctas, unroll=unroll, chunk=chunk)
+    # variant 4 (bulk-copy staged table): the one whose shape chunk / ctas_per_sm set
+    cfg = m.Launch(threads=threads, ctas_per_sm=ctas, unroll=unroll, chunk=chunk, variant=4)
     out = m.mul_twiddle(m.ctx_init(P), dev(x), dev(tw), cfg=cfg)
     assert np.array_equal(host(out), oracle.twiddle(P, x, tw))
 
@@ -414,18 +422,37 @@ def test_guards_ntt(m, log_n, batch):
 
 # ------------------------------------------ NEXT #2: Fourier-prime REDC ladder (variant 9)
 
-@pytest.mark.parametrize("P", [469762049, 998244353, 65537, 786433])
+@pytest.mark.parametrize("P", [469762049, 998244353, 65537, 786433, 2013265921, 1811939329, 1711276033, 2113929217])
 @pytest.mark.parametrize("n", [1, 4, 5, 20003])
 def test_pow_fourier_variant(m, P, n):
-    # 469762049 = 7*2^26+1, 998244353 = 119*2^23+1, 65537 = 2^16+1, 786433 = 3*2^18+1
+    # 469762049 = 7*2^26+1, 998244353 = 119*2^23+1, 65537 = 2^16+1, 786433 = 3*2^18+1; with 3P >= 2^32
+    # (33-bit t, reading G8): 2013265921 = 15*2^27+1, 1811939329 = 27*2^26+1, 1711276033 = 51*2^25+1,
+    # 2113929217 = 63*2^25+1
     base = synth.uniform(42, 3, P, 0, n, low=1)
     e = synth.exponents(42, 4, 0, n)
+    base[:min(n, 3)] = [P - 1, 1, P - 2][:min(n, 3)]
     out = m.pow_vec(m.ctx_init(P), dev(base), dev(e), cfg=m.Launch(variant=9))
     assert np.array_equal(host(out), oracle.power(P, base, e))
 
 
+def test_pow_fourier_33bit_t_both_signs(m):
+    """P0 = 15*2^27+1 (3P > 2^32): all pairs of a set of residues that drive t = q1 - q2 + q3 to
+    both ends of [-(P-1), 2(P-1)], through a ladder whose every product is Alg. 3:
+    x^e with e = 2 is one squaring; x^3 one squaring and one multiply."""
+    P = 2013265921
+    vals = np.array([0, 1, 2, P - 1, P - 2, (P - 1) // 2, (P + 1) // 2, 1 << 30, (1 << 31) - 1 - P % 7,
+                     268435454, 1172168163, 943718400, 1 << 27, (1 << 27) + 1, 15, 16], dtype=np.uint64) % P
+    base = np.repeat(vals, 4).astype(np.uint32)
+    exp = np.tile(np.array([2, 3, 0xFFFFFFFF, 0x80000001], dtype=np.uint32), len(vals))
+    rng = np.random.default_rng(33)
+    base = np.concatenate([base, rng.integers(0, P, 40000, dtype=np.uint64).astype(np.uint32)])
+    exp = np.concatenate([exp, rng.integers(0, 1 << 32, 40000, dtype=np.uint64).astype(np.uint32)])
+    out = m.pow_vec(m.ctx_init(P), dev(base), dev(exp), cfg=m.Launch(variant=9))
+    assert np.array_equal(host(out), oracle.power(P, base, exp))
+
+
 def test_pow_fourier_unsupported(m):
-    for P in (2013265921, 1000003, 12289):   # 3P >= 2^32 / not a Fourier prime / 2n < 32
+    for P in (1000003, 12289):   # not a Fourier prime / 2n < 32
         with pytest.raises(m.MontError) as ei:
             m.pow_vec(m.ctx_init(P), dev(np.ones(8, np.uint32)), dev(np.ones(8, np.uint32)), cfg=m.Launch(variant=9))
         assert ei.value.status == 4
@@ -433,8 +460,9 @@ def test_pow_fourier_unsupported(m):
 
 @pytest.mark.parametrize("ctas", [0, 1, 3, 5])
 @pytest.mark.parametrize("n", [4, 8, 12, 4100, 1 << 20])
-def test_pow_variant10_grids(m, ctas, n):
+@pytest.mark.parametrize("variant", [10, 11, 13])
+def test_pow_variant10_grids(m, ctas, n, variant):
     P = 469762049
     base, e = synth.c4_inputs(P, 0, n)
-    out = m.pow_vec(m.ctx_init(P), dev(base), dev(e), cfg=m.Launch(variant=10, ctas_per_sm=ctas))
+    out = m.pow_vec(m.ctx_init(P), dev(base), dev(e), cfg=m.Launch(variant=variant, ctas_per_sm=ctas))
     assert np.array_equal(host(out), oracle.power(P, base, e))

@@ -168,6 +168,30 @@ def test_pow_vs_python_pow(P):
     assert out[0] == 1 % P and out[1] == 0            # 0^0 = 1, 0^e = 0 (G10)
 
 
+@pytest.mark.parametrize("P", CONFIG_PRIMES + (17, 257, 2147483647))
+def test_pow_full_32bit_exponents(P):
+    """The product's contract (include/mont.h) takes any uint32 exponent: bits 31..0.  Pinned by
+    Python's built-in pow (a library routine), by Fermat with exponents >= 2^31 (e = k(P-1) for
+    k >= 2), and by the reduction a^e = a^(e mod (P-1)) for e in [2^31, 2^32) -- an independent
+    path that never sets bit 31."""
+    rng = np.random.default_rng(41)
+    base = rng.integers(0, P, 20_000, dtype=np.uint64).astype(np.uint32)
+    exp = rng.integers(1 << 31, 1 << 32, 20_000, dtype=np.uint64).astype(np.uint32)
+    base[:3] = [0, 1, P - 1]
+    exp[:3] = [0xFFFFFFFF, 0x80000000, 0x80000001]
+    out = oracle.power(P, base, exp)
+    ref = np.array([pow(int(x), int(e), P) for x, e in zip(base, exp)], dtype=np.uint32)
+    assert np.array_equal(out, ref)
+    a = base[base != 0]
+    e = exp[base != 0]
+    assert np.array_equal(oracle.power(P, a, e), oracle.power(P, a, e % np.uint32(P - 1)))
+    k = np.uint64((1 << 31) // (P - 1) + 1)
+    fermat = np.full(a.shape, min(int(k) * (P - 1), 0xFFFFFFFF // (P - 1) * (P - 1)), dtype=np.uint32)
+    assert int(fermat[0]) >= 1 << 31
+    assert np.all(oracle.power(P, a, fermat) == 1)                     # Fermat: a^(k(P-1)) = 1
+    assert oracle.pow1(P, 0, 0x80000000) == 0 and oracle.pow1(P, 5 % P, 0x80000000) == pow(5, 1 << 31, P)
+
+
 @pytest.mark.parametrize("P", CONFIG_PRIMES)
 def test_pow_fermat_and_laws(P):
     rng = np.random.default_rng(5)

@@ -21,9 +21,14 @@ MUTANTS = {
                       "return (uint32_t)((((uint64_t)x % c->P) << (c->l - 1)) % c->P);"),
     "from_mont uses P'": ("return mulmod_naive(x % c->P, c->Rinv, c->P);",
                           "return mulmod_naive(x % c->P, c->Pprime % c->P, c->P);"),
-    "pow misses bit 30": ("for (int bit = 30; bit >= 0; --bit) {\n        acc = mulmod_naive(acc, acc, P);\n"
+    "pow drops bit 31": ("for (int bit = 31; bit >= 0; --bit) {\n        acc = mulmod_naive(acc, acc, P);\n"
+                         "        if ((exp >> bit) & 1u) acc = mulmod_naive(acc, x, P);",
+                         "for (int bit = 30; bit >= 0; --bit) {\n        acc = mulmod_naive(acc, acc, P);\n"
+                         "        if ((exp >> bit) & 1u) acc = mulmod_naive(acc, x, P);"),
+    "pow misses bit 30": ("for (int bit = 31; bit >= 0; --bit) {\n        acc = mulmod_naive(acc, acc, P);\n"
                           "        if ((exp >> bit) & 1u) acc = mulmod_naive(acc, x, P);",
-                          "for (int bit = 29; bit >= 0; --bit) {\n        acc = mulmod_naive(acc, acc, P);\n"
+                          "for (int bit = 31; bit >= 0; --bit) {\n        if (bit == 30) continue;\n"
+                          "        acc = mulmod_naive(acc, acc, P);\n"
                           "        if ((exp >> bit) & 1u) acc = mulmod_naive(acc, x, P);"),
     "pow multiply before square": ("        acc = mulmod_naive(acc, acc, P);\n        if ((exp >> bit) & 1u) acc = mulmod_naive(acc, x, P);\n    }\n    return acc;\n}\n\n/* -",
                                    "        if ((exp >> bit) & 1u) acc = mulmod_naive(acc, x, P);\n        acc = mulmod_naive(acc, acc, P);\n    }\n    return acc;\n}\n\n/* -"),

