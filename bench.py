@@ -82,8 +82,35 @@ def parse():
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="issue the two-lane step launch by launch instead of replaying it as one CUDA graph")
     ap.add_argument("--pow-ctas", type=int, default=2, help="CTAs per SM of the persistent pow grid (0 = flat)")
-    ap.add_argument("--pow-variant", type=int, default=10, help="mont_pow_vec_ex variant used in the lane schedule")
+    ap.add_argument("--pow-variant", type=int, default=11, help="mont_pow_vec_ex variant used in the lane schedule")
+    ap.add_argument("--no-subruns", action="store_true", help="skip the configs[4] / configs[0] sub-objects")
     return ap.parse_args()
+
+
+def launch_ranks(args):
+    """`--gpus N` launches N ranks itself when no launcher did (one process per GPU under
+    torch.distributed.run, rendezvous on 127.0.0.1); under a launcher, --gpus must equal
+    WORLD_SIZE.  Returns the exit code of the child launcher, or None to run in this process."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is not None:
+        if int(ws) != args.gpus:
+            print(json.dumps({"error": f"--gpus {args.gpus} disagrees with WORLD_SIZE={ws}"}), flush=True)
+            return 2
+        return None
+    if args.gpus <= 1:
+        return None
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py"), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def dist_timeout():
+    import datetime
+    return datetime.timedelta(seconds=int(os.environ.get("MONT_DIST_TIMEOUT_S", "900")))
 
 
 def peaks():
@@ -327,13 +354,14 @@ def _popcount_sum(t):
 
 # ----------------------------------------------------------- verification
 
-def verify(wl: Workload) -> dict:
+def verify(wl: Workload, run: bool = True) -> dict:
     """Independent correctness checks of this rank's outputs before any timing is
-    reported (a benchmark that computes wrong answers must fail).
-    Uses torch int64 arithmetic and Python's built-in pow -- never the product
-    kernels' own helpers and never the oracle."""
+    reported (a benchmark that computes wrong answers must fail), and again
+    (run=False) on the buffers the timed CUDA graph wrote.  Uses torch int64 arithmetic and
+    Python's built-in pow -- never the product kernels' own helpers and never the oracle."""
     torch = wl.torch
-    wl.step()
+    if run:
+        wl.step()
     torch.cuda.synchronize()
     checks = {}
 
@@ -391,6 +419,145 @@ def verify(wl: Workload) -> dict:
         checks["ntt_sampled_dft"] = ok
         wl.ntt_x.copy_(wl.ntt_x0)
     return checks
+
+
+# ------------------------------------------------ configs[4] and configs[0] sub-runs
+
+GOLDEN = ROOT / "tests" / "golden"
+
+
+def run_c5(m, torch, rank: int, world: int, reps: int = 5) -> dict:
+    """configs[4] inside every line: n = 2^31 uint32 pairs in total, rank r owns the contiguous
+    global-index slice [r n / W, (r+1) n / W) (generated on its GPU from the global index), the
+    fused mul_vec + checksum kernel per rank, box time = MAX over ranks of each rank's median
+    (CUDA events, barrier + synchronize around every rep), then ONE all-reduce SUM of the
+    checksum partials.  The box checksum must equal the oracle's (tests/golden/c5_checksum.json,
+    written by scripts/golden_c5.py from oracle/ only) for every W."""
+    from paper_1609_00999_b200 import shard
+    lo, hi = shard.slice_bounds(N_C5, world, rank)
+    n = hi - lo
+    ctx = m.ctx_init(P0)
+    u32 = dict(dtype=torch.uint32, device=torch.device("cuda", torch.cuda.current_device()))
+    a, b, c = torch.empty(n, **u32), torch.empty(n, **u32), torch.empty(n, **u32)
+    m.synth_fill(a, SEED, 1, lo, P0, 0, False)
+    m.synth_fill(b, SEED, 2, lo, P0, 0, False)
+    acc = torch.zeros(1, dtype=torch.int64, device=a.device)
+    fn = lambda: m.mul_vec_checksum(ctx, a, b, out=c, acc=acc)
+    for _ in range(2):
+        fn()
+    st = torch.cuda.current_stream()
+    ts = []
+    for _ in range(reps):
+        shard.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        fn()
+        e1.record(st)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    local = statistics.median(ts)
+    box_ms = shard.max_over_ranks(local)
+    fastest = -shard.max_over_ranks(-local)
+    acc.zero_()
+    fn()
+    torch.cuda.synchronize()
+    part = int(acc.item())
+    box = shard.combine_checksums(part, P0)
+    ok = True   # Montgomery identity c 2^32 = a b (mod P), 0 <= c < P, on every element
+    for s0 in range(0, n, 1 << 25):
+        aa, bb, cc = (t[s0:s0 + (1 << 25)].view(torch.int32).to(torch.int64) & 0xFFFFFFFF for t in (a, b, c))
+        ok &= bool(((cc << 32) % P0 == (aa * bb) % P0).all()) and bool((cc < P0).all())
+        del aa, bb, cc
+    ok_all = shard.max_over_ranks(0.0 if ok else 1.0) == 0.0
+    want = None
+    gp = GOLDEN / "c5_checksum.json"
+    if gp.exists():
+        g = json.loads(gp.read_text())
+        want = g["box_checksum_mod_P"]
+        rank_want = g["rank_checksums_mod_P"].get(str(world))
+        rank_ok = rank_want is None or rank_want[rank] == part % P0
+        ok_all &= shard.max_over_ranks(0.0 if rank_ok else 1.0) == 0.0
+    del a, b, c
+    torch.cuda.empty_cache()
+    return {"config": "configs[4]: n = 2^31 uint32 pairs, P = 2013265921, contiguous global-index slices, "
+                      "fused mul_vec + checksum, one NCCL all-reduce SUM of the partials after timing",
+            "n_total": N_C5, "n_rank": n, "ranks": world, "reps": reps,
+            "ms_box": round(box_ms, 4), "ms_fastest_rank": round(fastest, 4),
+            "rank_skew": round((box_ms - fastest) / box_ms, 4) if box_ms else None,
+            "gmulmod_s_box": round(N_C5 / (box_ms * 1e-3) / 1e9, 2),
+            "gbs_aggregate": round(12 * N_C5 / (box_ms * 1e-3) / 1e9, 1),
+            "box_checksum": box, "checksum_oracle": want,
+            "checksum_ok": (want is None or box == want) and ok_all, "identity_all_elements": ok_all,
+            "scaling": "strong (fixed total n)"}
+
+
+def run_c1(m, torch) -> dict:
+    """configs[0] inside every line (single GPU, launch-latency bound): one
+    mont_mul_vec_checksum call on n = 65536 with the G12 edge values.  Reports the latency of one
+    call (host call to completion, and between CUDA events after an L2 flush) and the throughput
+    of the call replayed back to back from a CUDA graph."""
+    import numpy as np  # noqa: F401
+
+    import synth as _synth  # the shared input generator (no method arithmetic)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ha, hb = _synth.c1_inputs(P0)
+    a, b = torch.from_numpy(ha).to(dev), torch.from_numpy(hb).to(dev)
+    c = torch.empty_like(a)
+    acc = torch.zeros(1, dtype=torch.int64, device=dev)
+    ctx = m.ctx_init(P0)
+    fn = lambda: m.mul_vec_checksum(ctx, a, b, out=c, acc=acc)
+    for _ in range(5):
+        fn()
+    torch.cuda.synchronize()
+    flush = torch.empty(128 << 20, dtype=torch.int32, device=dev)
+    host, devt = [], []
+    for k in range(50):
+        flush.fill_(k)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record()
+        fn()
+        e1.record()
+        e1.synchronize()
+        host.append((time.perf_counter() - t0) * 1e6)
+        devt.append(e0.elapsed_time(e1) * 1e3)
+    del flush
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    reps = 200
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(reps):
+            fn()
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        g.replay()
+    e1.record()
+    e1.synchronize()
+    per_call_us = e0.elapsed_time(e1) * 1e3 / (5 * reps)
+    acc.zero_()
+    fn()
+    torch.cuda.synchronize()
+    checksum = int(acc.item()) % P0
+    ka = GOLDEN / "survey_known_answers.json"
+    want = json.loads(ka.read_text())["c1"]["checksum_mod_P"] if ka.exists() else None
+    hc = c.cpu()
+    return {"config": "configs[0]: mont_mul_vec (fused checksum) n = 65536, P = 2013265921, G12 edge values",
+            "latency_us": {"host_call_to_completion": round(statistics.median(host), 2),
+                           "device_events_after_l2_flush": round(statistics.median(devt), 2)},
+            "graph_replay_us_per_call": round(per_call_us, 3),
+            "graph_replay_gmulmod_s": round(65536 / (per_call_us * 1e-6) / 1e9, 2),
+            "checksum": checksum, "checksum_survey_known_answer": want,
+            "checksum_ok": want is None or checksum == want,
+            "identity_ok": bool((((hc.view(torch.int32).to(torch.int64) & 0xFFFFFFFF) << 32) % P0 ==
+                                 ((a.cpu().view(torch.int32).to(torch.int64) & 0xFFFFFFFF) *
+                                  (b.cpu().view(torch.int32).to(torch.int64) & 0xFFFFFFFF)) % P0).all())}
 
 
 # ----------------------------------------------------------- device timing
@@ -690,6 +857,9 @@ def ncu_traffic(name: str):
 
 def main():
     args = parse()
+    rc = launch_ranks(args)
+    if rc is not None:
+        sys.exit(rc)
     global POW_CTAS, POW_VARIANT
     POW_CTAS = 0 if args.serial else args.pow_ctas
     POW_VARIANT = args.pow_variant
@@ -707,12 +877,16 @@ def main():
     # (the kernels of different ranks never wait on each other; only CPU-side gloo collectives)
     backend = os.environ.get("MONT_DIST_BACKEND", "nccl")
     dev_index = 0 if os.environ.get("MONT_SHARE_GPU") == "1" else local_rank
+    if os.environ.get("MONT_SHARE_GPU") != "1" and torch.cuda.device_count() < world:
+        if rank == 0:
+            print(json.dumps({"error": f"{world} ranks but {torch.cuda.device_count()} visible GPUs"}), flush=True)
+        sys.exit(2)
     torch.cuda.set_device(dev_index)
     if world > 1:
         if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index), timeout=dist_timeout())
         else:
-            dist.init_process_group(backend)
+            dist.init_process_group(backend, timeout=dist_timeout())
     wl = Workload(args.workload, rank, world)
     checks = verify(wl)
     ok = all(checks.values())
@@ -756,6 +930,13 @@ def main():
     torch.cuda.synchronize()
     shard.barrier()
     clocks = sampler.stop()
+    # the timed graph's own outputs, checked again (no re-run): what was timed is what was verified
+    post = verify(wl, run=False) if graph is not None else {}
+    post_ok = shard.max_over_ranks(0.0 if all(post.values()) else 1.0) == 0.0
+    if not post_ok:
+        if rank == 0:
+            print(json.dumps({"error": "parity check of the timed graph's outputs failed", "checks": post}), flush=True)
+        sys.exit(1)
     total_ms = shard.max_over_ranks(total_ms)
     serial_ms = shard.max_over_ranks(serial_ms)
     ms_per_step = total_ms / args.steps
@@ -828,6 +1009,13 @@ def main():
     if not args.no_e2e and world >= 1:
         e2e_ms = time_e2e(wl, max(1, args.e2e_steps))
         e2e_ms = None if e2e_ms is None else shard.max_over_ranks(e2e_ms)
+    # configs[4] (sharded n = 2^31, strong scaling) and configs[0] (latency) ride along in the
+    # default line, after the step's own timing: the driver runs only the default workload
+    c5 = c1 = None
+    if wl.kind == "step" and not args.no_subruns:   # 24 GiB / W more on top of the step's 3.3 GiB
+        c5 = run_c5(wl.m, torch, rank, world)
+        if rank == 0:
+            c1 = run_c1(wl.m, torch)
     if rank != 0:
         if dist.is_initialized():
             dist.destroy_process_group()
@@ -871,6 +1059,8 @@ def main():
     dom_r = max((r for r in rooflines if r["kernel"].split("[")[0] == dom_kind), key=lambda r: r["ms"])
     roof = {k: dom_r[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")}
     roof["kernel"] = dom_r["kernel"]
+    roof["traffic_source"] = ("cited, not measured in this run: dram__bytes_read.sum + dram__bytes_write.sum per "
+                              "launch from the committed ncu --set full capture, profiles/ncu_summary.json")
     roof["peak_kind"] = peak_kind if dom_r["bound"] == "hbm" else "derived (DESIGN.md §6)"
     if triad_gbs is not None and dom_r["bound"] == "hbm":
         roof["triad_gbs"] = round(triad_gbs, 1)
@@ -910,6 +1100,14 @@ def main():
     }
     if latency_us is not None:
         line["latency_us"] = latency_us
+    if c5 is not None:
+        line["c5"] = c5
+        line["parity"]["c5_checksum_ok"] = c5["checksum_ok"]
+    if c1 is not None:
+        line["c1"] = c1
+        line["parity"]["c1_checksum_ok"] = c1["checksum_ok"]
+    if post:
+        line["parity"]["timed_graph_outputs"] = post
     if e2e_ms is not None:
         line["e2e"] = {"value": round(mulmods_job / (e2e_ms * 1e-3) / 1e9, 3), "unit": "Gmulmod/s",
                        "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": wl.e2e_h2d,

@@ -35,6 +35,10 @@ def test_b200_arm_contract():
     assert all(d["parity"]["checks"].values())
     assert d["roofline"]["bound"] in ("hbm", "alu") and 0 < d["roofline"]["frac"] < 1.5
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    # configs[4] and configs[0] ride along: box checksum = the oracle's (tests/golden/c5_checksum.json)
+    assert d["c5"]["checksum_ok"] and d["c5"]["identity_all_elements"] and d["c5"]["n_total"] == 1 << 31
+    assert d["c1"]["checksum_ok"] and d["c1"]["latency_us"]["host_call_to_completion"] > 0
+    assert all(d["parity"]["timed_graph_outputs"].values())
     import oracle
     import synth
     want = []
@@ -42,3 +46,38 @@ def test_b200_arm_contract():
         a, b = synth.c2_inputs(P, 0, 1 << 26)
         want.append(oracle.checksum(P, oracle.mont_mul(P, a, b)))
     assert d["parity"]["box_checksums"] == want
+
+
+def test_gpus_flag_spawns_ranks():
+    """`bench.py --gpus 2` with no launcher starts 2 ranks itself (torch.distributed.run on
+    127.0.0.1); exactly one JSON line comes back, from rank 0, with n_gpus = 2 (CPU: the
+    reference arm, which needs no GPU)."""
+    d = run(["--impl", "reference", "--workload", "c1", "--steps", "1", "--warmup", "0", "--gpus", "2"])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2
+
+
+def test_gpus_flag_must_match_launcher():
+    import os
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--workload", "c1", "--gpus", "1"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 2 and "disagrees with WORLD_SIZE" in r.stdout
+
+
+@pytest.mark.gpu
+def test_b200_arm_two_ranks_on_one_gpu():
+    """`--gpus 2` launches two ranks itself; on the single gpurun GPU they share it in the
+    orchestration dry-run mode (gloo collectives on the CPU, kernels of different ranks never wait
+    on each other).  Two ranks report n_gpus 2, slice configs[4] in halves, and the box checksum
+    is still the oracle's."""
+    import os
+    env = dict(os.environ, MONT_SHARE_GPU="1", MONT_DIST_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3", "--soak", "0",
+                        "--no-cpu-baseline", "--no-e2e"], cwd=ROOT, capture_output=True, text=True, timeout=900,
+                       env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["c5"]["ranks"] == 2 and d["c5"]["n_rank"] == 1 << 30
+    assert d["c5"]["checksum_ok"] and all(d["parity"]["checks"].values())
