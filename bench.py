@@ -65,6 +65,10 @@ G11_GENERATOR = 31
 POW_CTAS = 0   # set from --pow-ctas
 POW_VARIANT = 0  # set from --pow-variant
 LANE_ORDER = tuple(os.environ.get("MONT_LANE_ORDER", "imad,hbm").split(","))
+# the lane whose stream gets the higher priority in the two-lane step (graph kernel nodes inherit
+# it): the persistent pow grid is placed first, one CTA per SM, and the HBM-bound launches fill
+# the rest of every SM (scripts/step_sweep.py, profiles/r02_step_sweep*.jsonl)
+LANE_PRIO = os.environ.get("MONT_LANE_PRIO", "imad")
 
 
 def parse():
@@ -81,8 +85,8 @@ def parse():
     ap.add_argument("--serial", action="store_true", help="report the serial (one-stream) step instead")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="issue the two-lane step launch by launch instead of replaying it as one CUDA graph")
-    ap.add_argument("--pow-ctas", type=int, default=2, help="CTAs per SM of the persistent pow grid (0 = flat)")
-    ap.add_argument("--pow-variant", type=int, default=11, help="mont_pow_vec_ex variant used in the lane schedule")
+    ap.add_argument("--pow-ctas", type=int, default=1, help="CTAs per SM of the persistent pow grid (0 = flat)")
+    ap.add_argument("--pow-variant", type=int, default=10, help="mont_pow_vec_ex variant used in the lane schedule")
     ap.add_argument("--no-subruns", action="store_true", help="skip the configs[4] / configs[0] sub-objects")
     return ap.parse_args()
 
@@ -198,6 +202,15 @@ class Workload:
         self.inputs, self.outputs = [], []                     # tensors copied in / out by e2e
         self.acc = torch.zeros(len(PRIMES), dtype=torch.int64, device=dev)
         self.config = {}
+        # launch configurations of the HBM-bound launches in the two-lane step: mul_vec+checksum
+        # 256 threads x 2 uint4, to/from 256 x 4 (the shapes that leave the co-running pow grid
+        # most room, profiles/r02_step_sweep4.jsonl); the twiddle multiply keeps the library
+        # default.  The serial pass uses the library defaults.
+        self.hbm_cfg_lane = {"mul": m.Launch(threads=256, unroll=2), "conv": m.Launch(threads=256, unroll=4)}
+        if os.environ.get("MONT_HBM_DEFAULTS") == "1":
+            self.hbm_cfg_lane = {}
+        self.hbm_cfg = {}    # the serial step: library defaults (each kernel's best standalone shape)
+        self.lane_events = None
         L = self.launches
         if kind in ("step", "c2"):
             off = rank * N_C2
@@ -214,7 +227,8 @@ class Workload:
                 # A7 + A11 fused: c = REDC(a, b) and the checksum partial in one pass
                 L.append((f"mont_mul_vec_checksum[P={P}]",
                           (lambda ctx=self.ctx[P], a=a, b=b, c=c, si=si:
-                           m.mul_vec_checksum(ctx, a, b, out=c, acc=self.acc[si:si + 1])),
+                           m.mul_vec_checksum(ctx, a, b, out=c, acc=self.acc[si:si + 1],
+                                              cfg=self.hbm_cfg.get("mul"))),
                           12 * N_C2, N_C2, "hbm"))
             self.config.update({"c2_n": N_C2, "c2_primes": list(PRIMES)})
         if kind == "step":
@@ -223,9 +237,11 @@ class Workload:
             back = torch.empty(N_C2, **u32)
             self.outputs.append(back)
             self.abar, self.back = abar, back
-            L.append(("to_mont", lambda a0=a0, abar=abar: m.to_mont(self.ctx[P0], a0, out=abar), 8 * N_C2, N_C2, "hbm"))
-            L.append(("from_mont", lambda abar=abar, back=back: m.from_mont(self.ctx[P0], abar, out=back), 8 * N_C2, N_C2,
-                      "hbm"))
+            L.append(("to_mont", lambda a0=a0, abar=abar: m.to_mont(self.ctx[P0], a0, out=abar,
+                                                                     cfg=self.hbm_cfg.get("conv")), 8 * N_C2, N_C2, "hbm"))
+            L.append(("from_mont", lambda abar=abar, back=back: m.from_mont(self.ctx[P0], abar, out=back,
+                                                                            cfg=self.hbm_cfg.get("conv")),
+                      8 * N_C2, N_C2, "hbm"))
         if kind in ("step", "c3"):
             x = torch.empty(TW_BATCH * TW_LEN, **u32)
             m.synth_fill(x, SEED, 5, rank * TW_BATCH * TW_LEN, P0, 0, False)
@@ -236,7 +252,8 @@ class Workload:
             self.tw_x, self.tw, self.tw_out, self.w = x, tw, o, w
             self.inputs += [x]
             self.outputs.append(o)
-            L.append(("mont_mul_twiddle", lambda x=x, tw=tw, o=o: m.mul_twiddle(self.ctx[P0], x, tw, out=o),
+            L.append(("mont_mul_twiddle", lambda x=x, tw=tw, o=o: m.mul_twiddle(self.ctx[P0], x, tw, out=o,
+                                                                                 cfg=self.hbm_cfg.get("tw")),
                       8 * TW_BATCH * TW_LEN, TW_BATCH * TW_LEN, "hbm"))
             self.config.update({"c3_batch": TW_BATCH, "c3_len": TW_LEN})
         if kind in ("step", "c4"):
@@ -323,8 +340,9 @@ class Workload:
         # the persistent pow grid only pays when HBM-bound launches co-run with it
         both = {b for *_, b in self.launches} >= {"hbm", "imad"}
         self.pow_cfg = getattr(self, "pow_cfg_lane", None) if both else None
+        self.hbm_cfg = self.hbm_cfg_lane
         if not hasattr(self, "_lanes"):
-            self._lanes = {"hbm": torch.cuda.Stream(), "imad": torch.cuda.Stream()}
+            self._lanes = {ln: torch.cuda.Stream(priority=-1 if ln == LANE_PRIO else 0) for ln in ("hbm", "imad")}
         ev = torch.cuda.Event()
         ev.record(cur)
         for st in self._lanes.values():
@@ -332,12 +350,17 @@ class Workload:
         for lane in LANE_ORDER:
             st = self._lanes[lane]
             with torch.cuda.stream(st):
-                for _, fn, _, _, bound in self.launches:
+                for i, (_, fn, _, _, bound) in enumerate(self.launches):
                     if bound == lane:
+                        if self.lane_events is not None:   # external events: graph event-record nodes
+                            self.lane_events[i][0].record(st)
                         fn()
+                        if self.lane_events is not None:
+                            self.lane_events[i][1].record(st)
         for st in self._lanes.values():
             cur.wait_stream(st)
         self.pow_cfg = None
+        self.hbm_cfg = {}
 
     def h2d_bytes(self):
         return sum(t.numel() * 4 for t in self.inputs)
@@ -592,6 +615,51 @@ def capture_step_graph(wl: Workload):
         wl.step_concurrent()
     torch.cuda.synchronize()
     return g
+
+
+def imad_launch_clock_mhz(wl: Workload, K: int):
+    """The SM clock the IMAD-bound launch (pow) runs at in the serial step: K more serial steps, each
+    with mb_sm_clock (one warp timing ~20 us of clock64 against %globaltimer) right after the pow
+    launch on the same stream -- the power-managed clock moves on a millisecond scale, so this is
+    the clock pow just ran at.  Median MHz over the K steps (not a timed pass)."""
+    import ctypes as _C  # noqa: F401
+    torch, m = wl.torch, wl.m
+    s = torch.cuda.current_stream()
+    buf = torch.zeros(K, 2, dtype=torch.int64, device=wl.dev)
+    got = False
+    for k in range(K):
+        for name, fn, _, _, bound in wl.launches:
+            fn()
+            if bound == "imad":
+                m.lib().mb_sm_clock(buf[k].data_ptr(), 40000, s.cuda_stream)
+                got = True
+    torch.cuda.synchronize()
+    if not got:
+        return None
+    v = [c / ns * 1e3 for c, ns in buf.tolist() if ns > 0]
+    return statistics.median(v) if v else None
+
+
+def in_step_kernel_times(wl: Workload, K: int):
+    """Each launch's duration INSIDE the two-lane step, co-running as timed: a second capture of
+    the same step with external CUDA events (graph event-record nodes) on each launch's own lane
+    stream around it, replayed K times; median per launch over the replays (a synchronize between
+    replays to read the events, outside any timed region)."""
+    torch = wl.torch
+    wl.lane_events = [(torch.cuda.Event(enable_timing=True, external=True),
+                       torch.cuda.Event(enable_timing=True, external=True)) for _ in wl.launches]
+    try:
+        g = capture_step_graph(wl)
+        per = [[] for _ in wl.launches]
+        for _ in range(max(3, K)):
+            g.replay()
+            torch.cuda.synchronize()
+            for i, (e0, e1) in enumerate(wl.lane_events):
+                per[i].append(e0.elapsed_time(e1))
+        del g
+        return [statistics.median(v) for v in per]
+    finally:
+        wl.lane_events = None
 
 
 def time_steps_graph(wl: Workload, g, K: int):
@@ -906,8 +974,10 @@ def main():
         torch.cuda.synchronize()
     shard.barrier()
     torch.cuda.synchronize()
-    # per-kernel durations: a serial pass (each launch bracketed by events)
+    # per-kernel durations: a serial pass (each launch bracketed by events), then the clock the
+    # IMAD-bound launch ran at in that state (its roofline is clock-normalised)
     serial_ms, per_ms = time_steps(wl, args.steps)
+    imad_mhz = imad_launch_clock_mhz(wl, max(3, args.steps))
     for _ in range(3):
         wl.step_concurrent()
     torch.cuda.synchronize()
@@ -932,6 +1002,7 @@ def main():
     clocks = sampler.stop()
     # the timed graph's own outputs, checked again (no re-run): what was timed is what was verified
     post = verify(wl, run=False) if graph is not None else {}
+    in_step_ms = in_step_kernel_times(wl, args.steps) if graph is not None else None
     post_ok = shard.max_over_ranks(0.0 if all(post.values()) else 1.0) == 0.0
     if not post_ok:
         if rank == 0:
@@ -1023,40 +1094,57 @@ def main():
     mulmods_job = wl.mulmods * world
     value = mulmods_job / (ms_per_step * 1e-3) / 1e9
     hbm_peak, peak_kind, sm_max = peaks()
-    rooflines = []
-    for (name, _, nbytes, mm, bound), t in zip(wl.launches, per_ms):
-        r = {"kernel": name, "ms": round(t, 4), "share": round(t / max(sum(per_ms), 1e-9), 4),
-             "gmulmod_s": round(mm / (t * 1e-3) / 1e9, 2) if mm else None}
-        if bound == "hbm":
-            gbs = nbytes / (t * 1e-3) / 1e9
-            r.update({"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",
-                      "frac": round(gbs / hbm_peak, 4), "bytes_per_launch": nbytes,
-                      "frac_nominal_8tbs": round(gbs / 8000.0, 4)})
-        else:
-            # integer-multiply (FMAHeavy) pipe: the measured REDC floor is 5 FMAHeavy issue
-            # slots per product -> 64/5 products per clk per SM.
-            sms = torch.cuda.get_device_properties(0).multi_processor_count
-            clk = (clocks.get("sm_mhz") or sm_max) * 1e6
-            peak = sms * 64 / 5 * clk / 1e12
-            ach = mm / (t * 1e-3) / 1e12
-            r.update({"bound": "alu", "achieved": round(ach, 4), "peak": round(peak, 4), "unit": "Tmulmod/s",
-                      "frac": round(ach / peak, 4),
-                      "peak_basis": f"{sms} SMs x 64 FMAHeavy lanes/clk / 5 issue slots per REDC x {clk/1e6:.0f} MHz",
-                      # SURVEY §8(d)'s other denominator: 4 multiplies per REDC at the full IMAD rate
-                      # (IMAD.WIDE/IMAD.HI measured half rate on B200, so this one is not reachable)
-                      "frac_imad_div4": round(ach / (sms * 64 / 4 * clk / 1e12), 4)})
-            if redc_peak:
-                r.update({"redc_chain_peak_measured": round(redc_peak, 4), "frac_redc_measured": round(ach / redc_peak, 4)})
-        r["traffic"] = ncu_traffic(name)
-        rooflines.append(r)
-    dom = max(range(len(per_ms)), key=lambda i: per_ms[i])
-    # dominant kernel = the kernel with the largest share of the step (summing same-kind launches)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+
+    def kernel_rows(times, imad_clk_mhz):
+        clk = (imad_clk_mhz or clocks.get("sm_mhz") or sm_max) * 1e6
+        rows = []
+        for (name, _, nbytes, mm, bound), t in zip(wl.launches, times):
+            r = {"kernel": name, "ms": round(t, 4), "share": round(t / max(sum(times), 1e-9), 4),
+                 "gmulmod_s": round(mm / (t * 1e-3) / 1e9, 2) if mm else None, "lane": bound}
+            if bound == "hbm":
+                gbs = nbytes / (t * 1e-3) / 1e9
+                r.update({"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                          "frac": round(gbs / hbm_peak, 4), "bytes_per_launch": nbytes,
+                          "frac_nominal_8tbs": round(gbs / 8000.0, 4)})
+            else:
+                # integer-multiply (FMAHeavy) pipe: the measured REDC floor is 5 FMAHeavy issue
+                # slots per product (profiles/r02_pipes.jsonl) -> 64/5 per clk per SM
+                peak = sms * 64 / 5 * clk / 1e12
+                ach = mm / (t * 1e-3) / 1e12
+                r.update({"bound": "alu", "achieved": round(ach, 4), "peak": round(peak, 4), "unit": "Tmulmod/s",
+                          "frac": round(ach / peak, 4),
+                          "peak_basis": f"{sms} SMs x 64 FMAHeavy lanes/clk / 5 issue slots per REDC x "
+                                        f"{clk/1e6:.0f} MHz" + (" (SM clock measured right after the launch, "
+                                                                "mb_sm_clock)" if imad_clk_mhz else
+                                                                " (median nvidia-smi clock of the timed region)"),
+                          # SURVEY §8(d)'s other denominator: 4 multiplies per REDC at the full IMAD rate
+                          # (IMAD.WIDE measured half rate on B200, so this one is not reachable)
+                          "frac_imad_div4": round(ach / (sms * 64 / 4 * clk / 1e12), 4)})
+                if redc_peak:
+                    r.update({"redc_chain_peak_measured": round(redc_peak, 4),
+                              "frac_redc_measured": round(ach / redc_peak, 4)})
+            r["traffic"] = ncu_traffic(name)
+            rows.append(r)
+        return rows
+
+    rooflines = kernel_rows(per_ms, imad_mhz)   # standalone, serial pass, library-default shapes
+    in_step = kernel_rows(in_step_ms, None) if in_step_ms else None
+    # dominant kernel: in the timed step, the longest lane (the critical path) and within it the
+    # kernel kind with the largest share; without a lane schedule, the serial pass
+    src = in_step if in_step else rooflines
+    lanes = {}
+    for r in src:
+        lanes[r["lane"]] = lanes.get(r["lane"], 0.0) + r["ms"]
+    crit = max(lanes, key=lanes.get) if in_step else None
     kinds = {}
-    for r in rooflines:
-        k = r["kernel"].split("[")[0]
-        kinds[k] = kinds.get(k, 0.0) + r["ms"]
+    for r in src:
+        if crit is None or r["lane"] == crit:
+            k = r["kernel"].split("[")[0]
+            kinds[k] = kinds.get(k, 0.0) + r["ms"]
     dom_kind = max(kinds, key=kinds.get)
-    dom_r = max((r for r in rooflines if r["kernel"].split("[")[0] == dom_kind), key=lambda r: r["ms"])
+    dom_r = max((r for r in src if r["kernel"].split("[")[0] == dom_kind and (crit is None or r["lane"] == crit)),
+                key=lambda r: r["ms"])
     roof = {k: dom_r[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")}
     roof["kernel"] = dom_r["kernel"]
     roof["traffic_source"] = ("cited, not measured in this run: dram__bytes_read.sum + dram__bytes_write.sum per "
@@ -1065,9 +1153,16 @@ def main():
     if triad_gbs is not None and dom_r["bound"] == "hbm":
         roof["triad_gbs"] = round(triad_gbs, 1)
         roof["frac_triad"] = round(dom_r["achieved"] / triad_gbs, 4)
-    roof["duration"] = ("median over the K timed steps of a serial pass with CUDA events around each launch "
-                        "(the HBM kernels in the launch configurations of the graph-replayed step; pow in its "
-                        "standalone flat grid)")
+    standalone = next(r for r in rooflines if r["kernel"] == dom_r["kernel"])
+    roof["frac_standalone"] = standalone["frac"]
+    if in_step:
+        roof["duration"] = ("inside the timed two-lane step: median over K replays of the step graph of the "
+                            "interval between external CUDA events captured around the launch on its own lane "
+                            "stream (co-running with the other lane exactly as timed)")
+        roof["lanes_ms_in_step"] = {k: round(v, 4) for k, v in lanes.items()}
+        roof["critical_lane"] = crit
+    else:
+        roof["duration"] = "median over the K timed steps of a serial pass with CUDA events around each launch"
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "Gmulmod/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
@@ -1090,14 +1185,20 @@ def main():
         "gpu_launches": len(wl.launches) * args.steps,
         "schedule": ("each step alone between CUDA events after an L2 flush" if wl.kind == "c1" else
                      "serial, one stream" if args.serial else
-                     "two lanes: HBM-bound launches on one stream, the IMAD-bound pow on another" +
+                     "two lanes: the HBM-bound launches in order on one stream (mul_vec+checksum 256 threads x 2 "
+                     "uint4, to/from_mont 256 x 4, twiddle default), the IMAD-bound pow on another, higher-priority "
+                     f"stream as a persistent grid of {POW_CTAS} CTA(s) per SM (mont_pow_vec_ex variant {POW_VARIANT})" +
                      (", replayed as one CUDA graph" if args.graph else "")),
         "ms_per_step_serial": round(serial_ms / args.steps, 5),
         "roofline": roof,
         "kernels": rooflines,
+        "kernels_note": ("'kernels': each launch alone (serial pass, library-default launch shapes); "
+                         "'kernels_in_step': the same launches inside the timed two-lane step"),
         "clocks": {k: clocks.get(k) for k in ("sm_mhz", "sm_max_mhz", "reasons", "samples", "samples_under_load")},
         "parity": {"checks": checks, "box_checksums": box_checksums},
     }
+    if in_step:
+        line["kernels_in_step"] = in_step
     if latency_us is not None:
         line["latency_us"] = latency_us
     if c5 is not None:

@@ -78,8 +78,12 @@ extern "C" {
  *                                   bulk-copy (TMA) engine, cp.async.bulk +
  *                                   mbarrier (any len; 256 threads unless
  *                                   threads is set)
- *   chunk     : mont_mul_twiddle_ex only: table columns staged per CTA
- *               (multiple of 4; 0 = min(len, 4096)).                       */
+ *   chunk     : mont_mul_twiddle_ex: table columns staged per CTA
+ *               (multiple of 4; 0 = min(len, 4096)).  mont_pow_vec_ex
+ *               variants 11-16: bytes of dynamic shared memory reserved
+ *               (never touched) per CTA, an occupancy cap that keeps a
+ *               flat pow grid to a few CTAs per SM while other kernels
+ *               co-run (0 = none, at most 227 KiB).                        */
 typedef struct mont_launch {
     int threads;
     int ctas_per_sm;
@@ -170,6 +174,12 @@ mont_status_t mb_imad(uint32_t *sink, int kind, int iters, const mont_launch_t *
 mont_status_t mb_pipe(uint32_t *sink, int kind, int iters, const mont_launch_t *cfg, cudaStream_t stream,
                       unsigned long long *threads_launched, unsigned long long *clk);
 int mb_pipe_ops_per_iter(int kind);
+
+/* mb_sm_clock: one warp spins `cycles` SM clocks (clock64) and stores out[0] = cycles elapsed,
+ * out[1] = nanoseconds elapsed (%globaltimer); out is a DEVICE pointer to 2 uint64.  Their ratio
+ * is the SM clock of the moment -- launched right after a kernel on the same stream, the clock
+ * that kernel ran at (the power-managed clock changes on a millisecond scale). */
+mont_status_t mb_sm_clock(unsigned long long *out, long long cycles, cudaStream_t stream);
 
 /* Number of SMs of the current device (cached per device), or -1. */
 int mont_sm_count(void);

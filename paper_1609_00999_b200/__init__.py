@@ -77,6 +77,7 @@ SIGNATURES = {
     "mb_imad": (C.c_int, [_P, C.c_int, C.c_int, _LAUNCH, _P, C.POINTER(C.c_ulonglong)]),
     "mb_pipe": (C.c_int, [_P, C.c_int, C.c_int, _LAUNCH, _P, C.POINTER(C.c_ulonglong), _P]),
     "mb_pipe_ops_per_iter": (C.c_int, [C.c_int]),
+    "mb_sm_clock": (C.c_int, [_P, C.c_longlong, _P]),
     "mont_sm_count": (C.c_int, []),
     # include/mont_host.h
     "mont_host_min_workspace": (C.c_size_t, [C.c_int, C.c_size_t]),

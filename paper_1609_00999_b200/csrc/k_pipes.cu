@@ -245,9 +245,30 @@ __global__ void __launch_bounds__(256) k_mix(uint32_t *sink, int iters, double P
     }
 }
 
+// one warp spins `cycles` SM clocks and stores (cycles elapsed, ns elapsed): the SM clock at that
+// moment, for clock-normalising a neighbouring launch (bench.py's pow roofline)
+__global__ void k_sm_clock(unsigned long long *out, long long cycles) {
+    long long g0, g1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+    const long long c0 = clock64();
+    long long c1 = c0;
+    while (c1 - c0 < cycles) c1 = clock64();
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+    if (threadIdx.x == 0) {
+        out[0] = (unsigned long long)(c1 - c0);
+        out[1] = (unsigned long long)(g1 - g0);
+    }
+}
+
 }  // namespace mont
 
 using namespace mont;
+
+extern "C" mont_status_t mb_sm_clock(unsigned long long *out, long long cycles, cudaStream_t stream) {
+    if (!out || cycles < 1) return MONT_EINVAL_ARG;
+    k_sm_clock<<<1, 32, 0, stream>>>(out, cycles);
+    return launch_status();
+}
 
 static const int kMixNI[6] = {1, 3, 6, 2, 0, 4};
 static const int kMixNF[6] = {1, 1, 2, 0, 2, 0};

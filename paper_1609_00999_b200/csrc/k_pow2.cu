@@ -186,21 +186,24 @@ __global__ void __launch_bounds__(256) k_pow2(Pow2Params q, uint32_t *out, const
 
 template <uint32_t PC, int NF, bool SH, bool BIGP>
 static void launch_pow2(const Pow2Params &q, uint32_t *out, const uint32_t *base, const uint32_t *exp, uint32_t head,
-                        size_t n4, uint32_t tail, unsigned grid, cudaStream_t s) {
-    k_pow2<PC, NF, SH, BIGP><<<grid, 256, 0, s>>>(q, out, base, exp, head, n4, tail);
+                        size_t n4, uint32_t tail, unsigned grid, size_t smem, cudaStream_t s) {
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_pow2<PC, NF, SH, BIGP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_pow2<PC, NF, SH, BIGP><<<grid, 256, smem, s>>>(q, out, base, exp, head, n4, tail);
 }
 
 template <int NF, bool SH, bool BIGP>
 static void dispatch_p(uint32_t p, bool specialise, const Pow2Params &q, uint32_t *out, const uint32_t *base,
-                       const uint32_t *exp, uint32_t head, size_t n4, uint32_t tail, unsigned grid, cudaStream_t s) {
+                       const uint32_t *exp, uint32_t head, size_t n4, uint32_t tail, unsigned grid, size_t smem,
+                       cudaStream_t s) {
     if (specialise && p == 469762049u && !BIGP)
-        launch_pow2<469762049u, NF, SH, false>(q, out, base, exp, head, n4, tail, grid, s);
+        launch_pow2<469762049u, NF, SH, false>(q, out, base, exp, head, n4, tail, grid, smem, s);
     else if (specialise && p == 998244353u && BIGP)
-        launch_pow2<998244353u, NF, SH, true>(q, out, base, exp, head, n4, tail, grid, s);
+        launch_pow2<998244353u, NF, SH, true>(q, out, base, exp, head, n4, tail, grid, smem, s);
     else if (specialise && p == 2013265921u && BIGP)
-        launch_pow2<2013265921u, NF, SH, true>(q, out, base, exp, head, n4, tail, grid, s);
+        launch_pow2<2013265921u, NF, SH, true>(q, out, base, exp, head, n4, tail, grid, smem, s);
     else
-        launch_pow2<0u, NF, SH, BIGP>(q, out, base, exp, head, n4, tail, grid, s);
+        launch_pow2<0u, NF, SH, BIGP>(q, out, base, exp, head, n4, tail, grid, smem, s);
 }
 
 }  // namespace mont
@@ -211,8 +214,13 @@ using namespace mont;
 //   11: REDC multiplies, P specialised for the config primes   12: 11 + 2 of 8 lanes on FP64
 //   13: Shoup multiplies, specialised                          14: 13 + 2 FP64 lanes
 //   15: 11 with P at run time (no specialisation)              16: 13 with P at run time
+// reserve_smem: dynamic shared memory requested per CTA and never touched -- an occupancy cap
+// (e.g. 100 KiB: at most 2 pow CTAs per SM), so that a flat pow grid co-running with the
+// HBM-bound launches keeps taking only a few CTA slots per SM while the block scheduler still
+// balances it dynamically (bench.py's two-lane step)
 mont_status_t mont_pow2_launch(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *base, const uint32_t *exp,
-                               size_t n, int variant, int ctas_per_sm, int sms, cudaStream_t stream) {
+                               size_t n, int variant, int ctas_per_sm, int sms, size_t reserve_smem,
+                               cudaStream_t stream) {
     const uint32_t p = ctx->p;
     const Pow2Params q{(int32_t)p, (int32_t)(0u - ctx->pneg), ctx->r1, ctx->r2, ctx->pneg, 0u, (double)p,
                        1.0 / (double)p};
@@ -230,8 +238,8 @@ mont_status_t mont_pow2_launch(const mont_ctx_t *ctx, uint32_t *out, const uint3
     const unsigned g = (unsigned)grid;
 #define P2(NF, SH)                                                                                \
     do {                                                                                          \
-        if (bigp) dispatch_p<NF, SH, true>(p, spec, q, out, base, exp, head, n4, tail, g, stream);  \
-        else dispatch_p<NF, SH, false>(p, spec, q, out, base, exp, head, n4, tail, g, stream);      \
+        if (bigp) dispatch_p<NF, SH, true>(p, spec, q, out, base, exp, head, n4, tail, g, reserve_smem, stream);  \
+        else dispatch_p<NF, SH, false>(p, spec, q, out, base, exp, head, n4, tail, g, reserve_smem, stream);      \
     } while (0)
     switch (v) {
         case 11: P2(0, false); break;

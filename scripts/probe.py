@@ -230,6 +230,44 @@ if args.what in ("all", "pow"):
                 out(what="pow", P=Pp, variant=variant, ctas=ctas, us=med * 1e6, us_best=best * 1e6,
                     useful_mulmods=useful, tmulmod=useful / med / 1e12, equal_to_variant0=same)
 
+if args.what == "powctx":
+    # pow (default launch) timed: back to back; after a 512 MiB L2 flush; after the twiddle kernel;
+    # each followed by mb_sm_clock for the clock it ran at
+    import numpy as np
+    P = 469762049
+    ctx = m.ctx_init(P)
+    n = 1 << 24
+    base = torch.empty(n, dtype=torch.uint32, device=dev)
+    e = torch.empty(n, dtype=torch.uint32, device=dev)
+    o = torch.empty(n, dtype=torch.uint32, device=dev)
+    m.synth_fill(base, 42, 3, 0, P, mode=1)
+    m.synth_fill(e, 42, 4, 0, P, mode=2)
+    useful = int(31 * n + np.unpackbits(e.cpu().numpy().view(np.uint8)).sum())
+    flush = torch.empty(128 << 20, dtype=torch.int32, device=dev)
+    clk = torch.zeros(2, dtype=torch.int64, device=dev)
+    for ctxname in ("back_to_back", "after_flush", "after_flush_sync"):
+        for variant in (11, 10, 17):
+            cfg = m.Launch(variant=variant)
+            ts, mhz = [], []
+            for k in range(20):
+                if ctxname != "back_to_back":
+                    flush.fill_(k)
+                if ctxname == "after_flush_sync":
+                    torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                m.pow_vec(ctx, base, e, out=o, cfg=cfg)
+                e1.record()
+                lib().mb_sm_clock(clk.data_ptr(), 40000, s.cuda_stream)
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1) * 1e3)
+                c, ns = clk.tolist()
+                mhz.append(c / ns * 1e3)
+            tm, cm = sorted(ts)[len(ts) // 2], sorted(mhz)[len(mhz) // 2]
+            floor_us = n / 32 * 478 / (sms * 4) / (cm * 1e6) * 1e6   # 478 FMAHeavy cycles per warp-ladder
+            out(what="powctx", ctx=ctxname, variant=variant, us=tm, mhz_after=cm, floor_us_at_that_clock=floor_us,
+                frac_floor=floor_us / tm, tmulmod=useful / tm / 1e6)
+
 if args.what in ("pcie",):
     n = 1 << 26   # 256 MiB
     hs = [torch.empty(n, dtype=torch.uint32, pin_memory=True) for _ in range(2)]

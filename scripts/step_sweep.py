@@ -1,0 +1,79 @@
+"""Sweep of the two-lane step's launch shapes (bench.py's graph-replayed step): the pow lane's
+variant / CTAs per SM and the HBM lane's launch configurations.  One JSON object per shape;
+outputs are re-verified after each timing (bench.verify on the graph's buffers).  Not part of the
+product; picks bench.py's defaults.
+
+    python scripts/step_sweep.py [--shapes NAME,...]
+"""
+import itertools
+import json
+import os
+import statistics
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+
+
+def main():
+    torch.cuda.set_device(0)
+    bench.POW_CTAS, bench.POW_VARIANT = 2, 11
+    wl = bench.Workload("step", 0, 1)
+    m = wl.m
+    assert all(bench.verify(wl).values())
+    L = m.Launch
+    # (variant, ctas_per_sm, reserved smem bytes): ctas 0 = flat grid
+    pows = [(10, 1, 0), (15, 1, 0), (11, 1, 0), (17, 2, 0), (10, 2, 0)]
+    prios = ["imad"]
+    if os.environ.get("SWEEP_WIDE"):
+        pows = [(11, 0, 0), (11, 0, 200 * 1024), (11, 0, 110 * 1024), (11, 0, 72 * 1024), (11, 0, 54 * 1024),
+                (11, 1, 0), (11, 2, 0), (10, 2, 0)]
+        prios = [None, "hbm", "imad"]
+    hbms = {
+        "default": {},   # mul+checksum 512 x 2, to/from 512 x 2, twiddle flat 512 x 4
+        "u2": {"mul": L(threads=256, unroll=2), "conv": L(threads=512, unroll=2), "tw": None},
+        "m256u1": {"mul": L(threads=256, unroll=1)},
+        "m256u4": {"mul": L(threads=256, unroll=4)},
+        "m1024u1": {"mul": L(threads=1024, unroll=1)},
+        "c256u2": {"conv": L(threads=256, unroll=2)},
+        "c256u4": {"conv": L(threads=256, unroll=4)},
+        "t256u4": {"tw": L(threads=256, unroll=4, variant=2)},
+        "t512u2": {"tw": L(threads=512, unroll=2, variant=2)},
+        "t256u8": {"tw": L(threads=256, unroll=8, variant=2)},
+        "all256u4": {"mul": L(threads=256, unroll=4), "conv": L(threads=256, unroll=4),
+                     "tw": L(threads=256, unroll=4, variant=2)},
+        "u2c4": {"mul": L(threads=256, unroll=2), "conv": L(threads=256, unroll=4)},
+    }
+    only = os.environ.get("SWEEP_HBM")
+    rebuilds = int(os.environ.get("SWEEP_REBUILDS", "2"))
+    for (pv, pc, sm), (hname, hcfg), prio in itertools.product(pows, hbms.items(), prios):
+        if only and hname not in only.split(","):
+            continue
+        wl.pow_cfg_lane = L(ctas_per_sm=pc, variant=pv, chunk=sm)
+        wl.hbm_cfg_lane = {k: v for k, v in hcfg.items() if v is not None}
+        # lane streams: torch priority -1 = high, 0 = low (graph kernel nodes inherit it)
+        wl._lanes = {"hbm": torch.cuda.Stream(priority=-1 if prio == "hbm" else 0),
+                     "imad": torch.cuda.Stream(priority=-1 if prio == "imad" else 0)}
+        for rb in range(rebuilds):
+            try:
+                g = bench.capture_step_graph(wl)
+            except Exception as ex:  # noqa: BLE001
+                print(json.dumps({"pow": [pv, pc, sm], "hbm": hname, "error": str(ex)}), flush=True)
+                break
+            for _ in range(3):
+                g.replay()
+            torch.cuda.synchronize()
+            ts = [bench.time_steps_graph(wl, g, 20) / 20 for _ in range(3)]
+            ok = all(bench.verify(wl, run=False).values())
+            print(json.dumps({"pow": [pv, pc, sm], "hbm": hname, "prio": prio, "rebuild": rb,
+                              "ms_per_step": round(statistics.median(ts), 4), "ms_best": round(min(ts), 4),
+                              "outputs_ok": ok}), flush=True)
+            del g
+
+
+if __name__ == "__main__":
+    main()

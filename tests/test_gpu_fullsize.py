@@ -155,16 +155,17 @@ def test_c4_fullsize(m):
     assert np.array_equal(out.cpu().numpy()[idx], oracle.power(P1, hb, he))
 
 
-@pytest.mark.parametrize("variant", [10, 11])
-def test_c4_fullsize_lane_launch(m, variant):
+@pytest.mark.parametrize("variant,ctas", [(10, 1), (10, 2), (11, 1), (11, 2)])
+def test_c4_fullsize_lane_launch(m, variant, ctas):
     """configs[3] in the launches bench.py's two-lane step can time (variants 10 / 11, 8 ladders
-    per thread, persistent grid of 2 CTAs per SM): sampled outputs against the oracle, and every
-    element equal to the 4-lane kernel's (variant 17, a different kernel)."""
+    per thread, persistent grid of 1 or 2 CTAs per SM; the bench default is variant 10 at 1):
+    sampled outputs against the oracle, and every element equal to the 4-lane kernel's
+    (variant 17, a different kernel)."""
     n = 1 << 24
     ctx = m.ctx_init(P1)
     base = gen(n, 3, P1, 1, m=m)
     e = gen(n, 4, P1, 2, m=m)
-    out = m.pow_vec(ctx, base, e, cfg=m.Launch(ctas_per_sm=2, variant=variant))
+    out = m.pow_vec(ctx, base, e, cfg=m.Launch(ctas_per_sm=ctas, variant=variant))
     ref = m.pow_vec(ctx, base, e, cfg=m.Launch(variant=17))
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
@@ -233,3 +234,26 @@ def test_c5_fullsize(m):
     for s in range(0, n, 1 << 28):
         tot += int(i64(c[s:s + (1 << 28)]).sum().item())
     assert int(acc.item()) == tot
+
+
+def test_bench_hbm_launch_shapes_fullsize(m):
+    """The HBM-bound launches in the shapes bench.py times (mul_vec+checksum 256 threads x 2 uint4,
+    to/from_mont 256 x 4): every element of configs[1] at P0 identical to the default launch's and
+    satisfying the Montgomery identity; the to/from round trip; the checksum."""
+    n = 1 << 26
+    ctx = m.ctx_init(P0)
+    a = gen(n, 1, P0, 0, True, m=m)
+    b = gen(n, 2, P0, 0, True, m=m)
+    c, acc = m.mul_vec_checksum(ctx, a, b, cfg=m.Launch(threads=256, unroll=2))
+    c0, acc0 = m.mul_vec_checksum(ctx, a, b)
+    torch.cuda.synchronize()
+    assert torch.equal(c, c0) and int(acc.item()) == int(acc0.item())
+    assert identity_all(P0, a, b, c)
+    t = m.to_mont(ctx, a, cfg=m.Launch(threads=256, unroll=4))
+    assert torch.equal(t, m.to_mont(ctx, a))
+    back = m.from_mont(ctx, t, cfg=m.Launch(threads=256, unroll=4))
+    assert torch.equal(back, a)
+    idx = sample_idx(n)
+    ha, hb = synth.c2_inputs_at(P0, idx.astype(np.uint64))
+    assert np.array_equal(c.cpu().numpy()[idx], oracle.mont_mul(P0, ha, hb))
+    assert np.array_equal(t.cpu().numpy()[idx], oracle.to_mont(P0, ha))
