@@ -3,9 +3,10 @@
 // PAPER.md Alg. 2 (REDC, :95-99) with the GPU refinement of the §3.2 dataflow
 // (:121-139): the paper gathers high and low 32-bit halves of 2-way 64-bit
 // products with shuffles because SSE has no high-half multiply; sm_100a has
-// one (mul.hi.u32 -> IMAD.HI), so the three integer multiplications
-// become four single-issue FMAHeavy-pipe instructions and no
-// gather exists:
+// one (mul.hi.u32 -> IMAD.HI) and a 32x32->64 multiply (mul.wide.u32 ->
+// IMAD.WIDE), so the three integer multiplications become three
+// FMAHeavy-pipe instructions (two of them half rate, below) and no gather
+// exists.  The textbook add form reads:
 //
 //   T  = a*b                 mul.lo + mul.hi       (A3, "needs twice the width", :123)
 //   m  = lo(T) * P' mod 2^32 mul.lo                (A4, the "short product", :93, :129)
@@ -35,11 +36,10 @@ struct Ctx {  // device view of mont_ctx_t (by value in kernel params); pinv = -
 
 __device__ __forceinline__ uint32_t umin(uint32_t x, uint32_t y) { return x < y ? x : y; }
 
-// canonical REDC(a*b): a*b < 2^32 * P required; returns [0, P).
-// "wide" form: T = a*b (IMAD.WIDE), m = lo(T) P' (IMAD), then
-// (T + m P) >> 32 is ONE IMAD.WIDE with the 64-bit T as addend -- the carry of
-// the paper's "2-way addition" is done inside the multiplier.
-// T + mP < 2 R P < 2^64, so nothing overflows.  3 FMAHeavy ops + 1 ALU op.
+// 32 x 32 -> 64 products (IMAD.WIDE): both halves of the paper's "2l-bit" product
+// in one register pair.  (A 64-bit addend is not fused: ptxas splits mad.wide with a
+// register-pair addend into IMAD.WIDE + IADD3 + IADD3.X, so the carry form of Alg. 2 costs ALU
+// ops the subtract form below does not.)
 __device__ __forceinline__ uint64_t mul_wide_u32(uint32_t a, uint32_t b) {
     uint64_t r;
     asm("mul.wide.u32 %0, %1, %2;" : "=l"(r) : "r"(a), "r"(b));
@@ -53,13 +53,16 @@ __device__ __forceinline__ int64_t mul_wide_s32(int32_t a, int32_t b) {
 __device__ __forceinline__ uint32_t hi32(uint64_t x) { return (uint32_t)(x >> 32); }
 __device__ __forceinline__ int32_t hi32s(int64_t x) { return (int32_t)(x >> 32); }
 
-// Measured on B200 (scripts/probe.py): IMAD and IMAD.WIDE issue
-// at 64 lanes/clk/SM but IMAD.HI at only 32.  So the high halves are taken
-// from IMAD.WIDE results, never from mul.hi, and the REDC is written in the
-// "subtract" form, which needs no carry:
+// Measured on B200 with dependent chains nothing can hoist (mb_pipe, csrc/k_pipes.cu;
+// profiles/r02_pipes.jsonl): IMAD issues at 64 lanes/clk/SM (register, immediate
+// or uniform-register operand alike), IMAD.WIDE at 32 (half rate), IMAD.HI at 32 with an
+// immediate operand and ~26 with three register operands.  So the high halves are taken from
+// IMAD.WIDE results, never from mul.hi, and the REDC is written in the "subtract" form, which
+// needs no carry:
 //   T = a b (IMAD.WIDE);  m = lo(T) P^-1 mod 2^32 (IMAD);  M = m P (IMAD.WIDE)
 //   lo(M) = lo(T) exactly, so (T - M) / 2^32 = hi(T) - hi(M)  (IADD3), in (-P, P)
-// = 3 full-rate FMAHeavy ops + 1 ALU op.  It is Alg. 2 with m' = -m:
+// = 4 + 2 + 4 = 10 FMAHeavy cycles per warp on an SMSP ("5 issue slots" of the 64-lane IMAD
+// rate) + 1 ALU op.  It is Alg. 2 with m' = -m:
 // t' = (T - m'P)/R = (T + mP)/R - P, i.e. the paper's t shifted by -P, so the
 // final "if t >= P then t - P" becomes "if t' < 0 then t' + P".
 // pinv = P^-1 mod 2^32 = -P' (reading G2).
