@@ -35,6 +35,12 @@ METRICS = [
     ("launch__grid_size", "grid"),
     ("launch__block_size", "block"),
     ("sm__cycles_elapsed.avg.per_second", "SM clock"),
+    ("smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio", "stall: barrier / issue"),
+    ("smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio", "stall: not selected / issue"),
+    ("smsp__average_warps_issue_stalled_wait_per_issue_active.ratio", "stall: wait / issue"),
+    ("smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio", "stall: short scoreboard / issue"),
+    ("smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio", "stall: MIO throttle / issue"),
+    ("sm__inst_executed_pipe_fmaheavy.sum", "FMAHeavy warp instructions"),
     ("smsp__inst_executed.sum", "warp instructions"),
     ("lts__t_bytes.sum", "L2 bytes"),
 ]
@@ -44,6 +50,8 @@ KIND = {  # ncu kernel name prefix -> bench.py kernel label prefix
     "k_map1": "to_mont",
     "k_twiddle": "mont_mul_twiddle",
     "k_pow": "mont_pow_vec",
+    "k_pow2": "mont_pow_vec",
+    "k_pow8": "mont_pow_vec[lane launch, variant 10]",
     "k_sum": "mont_checksum",
     "k_ntt_r32": "mont_ntt",
     "k_ntt_dif": "mont_ntt",
