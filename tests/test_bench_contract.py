@@ -81,3 +81,13 @@ def test_b200_arm_two_ranks_on_one_gpu():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["c5"]["ranks"] == 2 and d["c5"]["n_rank"] == 1 << 30
     assert d["c5"]["checksum_ok"] and all(d["parity"]["checks"].values())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("workload", ["c1", "c2", "c3", "c4", "c5", "ntt"])
+def test_b200_arm_each_workload(workload):
+    """Every --workload prints one line whose parity checks (before timing and on the timed
+    graph's outputs) all hold."""
+    d = run(["--workload", workload, "--steps", "3", "--warmup", "3", "--soak", "0", "--no-cpu-baseline", "--no-e2e"])
+    assert d["value"] > 0 and all(d["parity"]["checks"].values())
+    assert all(d["parity"].get("timed_graph_outputs", {}).values())
