@@ -340,7 +340,7 @@ class Workload:
         # the persistent pow grid only pays when HBM-bound launches co-run with it
         both = {b for *_, b in self.launches} >= {"hbm", "imad"}
         self.pow_cfg = getattr(self, "pow_cfg_lane", None) if both else None
-        self.hbm_cfg = self.hbm_cfg_lane
+        self.hbm_cfg = self.hbm_cfg_lane if both else {}   # lane shapes only next to a pow lane
         if not hasattr(self, "_lanes"):
             self._lanes = {ln: torch.cuda.Stream(priority=-1 if ln == LANE_PRIO else 0) for ln in ("hbm", "imad")}
         ev = torch.cuda.Event()

@@ -23,6 +23,22 @@ extern "C" {
 mont_status_t mont_dot(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *A, const uint32_t *x, size_t batch,
                        size_t len, cudaStream_t stream);
 
+/* mont_dot with an explicit launch (measurement): cfg->variant 0 = the
+ * default (= 1, measured fastest); 1 = one CTA per row,
+ * 4 x 16 B per thread per trip; 2 = 8 x 16 B; 3 = 4 x 16 B with the next
+ * trip's loads issued before this trip's products;
+ * 4 = 8 x 16 B prefetched; 5 = rows split into cfg->chunk-element pieces
+ * (multiple of 1024, 0 = 4096; needs len % 4 == 0, 16-byte aligned A and x,
+ * len >= 2 chunks, else variant 1), one CTA each, whose canonical partials
+ * are added into out[r] mod P by atomic compare-and-swap after the library
+ * zeroes out (out must not overlap A or x); 6 / 7 = 2 / 4 rows per CTA
+ * against one load of x (len % 4 == 0, 16-byte aligned A and x, else 1).
+ * cfg may be NULL.  Errors as mont_dot, plus MONT_EINVAL_ARG for another
+ * variant or chunk. */
+struct mont_launch;
+mont_status_t mont_dot_ex(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *A, const uint32_t *x, size_t batch,
+                          size_t len, const struct mont_launch *cfg, cudaStream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

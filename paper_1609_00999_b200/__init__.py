@@ -93,6 +93,7 @@ SIGNATURES["mont_ntt_twiddles"] = (C.c_int, [_CTX, _P, C.c_uint32, C.c_int, _P])
 SIGNATURES["mont_ntt_twiddles_pq"] = (C.c_int, [_CTX, _P, C.c_uint32, C.c_int, _P])
 SIGNATURES["mont_ntt_ex"] = (C.c_int, [_CTX, _P, _S, C.c_int, _P, C.c_uint32, C.c_int, _P])
 SIGNATURES["mont_dot"] = (C.c_int, [_CTX, _P, _P, _P, _S, _S, _P])
+SIGNATURES["mont_dot_ex"] = (C.c_int, [_CTX, _P, _P, _P, _S, _S, _LAUNCH, _P])
 SIGNATURES["mont_ntt_plan_words"] = (C.c_size_t, [C.c_int])
 SIGNATURES["mont_ntt_plan_init"] = (C.c_int, [_CTX, _P, C.c_uint32, C.c_int, _P])
 SIGNATURES["mont_ntt_large"] = (C.c_int, [_CTX, _P, _P, C.c_int, _P, C.c_uint32, _P])
@@ -440,7 +441,7 @@ def ntt_large(ctx: Ctx, x, plan, out=None, scale: int | None = None, stream=None
     return out
 
 
-def dot(ctx: Ctx, A, x, out=None, stream=None):
+def dot(ctx: Ctx, A, x, out=None, stream=None, cfg: Launch | None = None):
     """out[r] = sum_j A[r][j] x[j] R^-1 mod P for A (batch, len) (include/mont_dot.h)."""
     torch = _torch()
     _dev_u32(A, "A"), _dev_u32(x, "x")
@@ -448,8 +449,12 @@ def dot(ctx: Ctx, A, x, out=None, stream=None):
         raise ValueError("A must be (batch, len) and x (len,)")
     if out is None:
         out = torch.empty(A.shape[0], dtype=torch.uint32, device=A.device)
-    _check(lib().mont_dot(C.byref(ctx), _ptr(out), _ptr(A), _ptr(x), A.shape[0], A.shape[1],
-                          _stream_handle(stream)), "mont_dot")
+    if cfg is None:
+        _check(lib().mont_dot(C.byref(ctx), _ptr(out), _ptr(A), _ptr(x), A.shape[0], A.shape[1],
+                              _stream_handle(stream)), "mont_dot")
+    else:
+        _check(lib().mont_dot_ex(C.byref(ctx), _ptr(out), _ptr(A), _ptr(x), A.shape[0], A.shape[1], C.byref(cfg),
+                                 _stream_handle(stream)), "mont_dot_ex")
     return out
 
 

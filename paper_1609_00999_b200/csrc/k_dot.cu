@@ -7,11 +7,15 @@
 #include <stdint.h>
 
 #include "../../include/mont_dot.h"
+#include "../../include/mont_ext.h"
 #include "abi_util.h"
 
 namespace mont {
 
-template <int U>
+// One CTA per row.  PF = true: software-pipelined -- the next trip's U uint4 of the row are
+// loaded before this trip's products, so each thread always has a trip of A in flight (the row
+// stream is latency-bound otherwise: every trip waits for its own loads).
+template <int U, bool PF = false>
 __global__ void __launch_bounds__(256) k_dot(Ctx c, uint32_t *out, const uint32_t *A, const uint32_t *x, size_t len,
                                               bool vec) {
     const uint32_t *row = A + (size_t)blockIdx.x * len;
@@ -21,19 +25,46 @@ __global__ void __launch_bounds__(256) k_dot(Ctx c, uint32_t *out, const uint32_
         const uint4 *r4 = reinterpret_cast<const uint4 *>(row);
         const uint4 *x4 = reinterpret_cast<const uint4 *>(x);
         const size_t n4 = len >> 2;
+        const size_t stride = (size_t)U * blockDim.x;
         size_t i = threadIdx.x;
-        for (; i + (U - 1) * blockDim.x < n4; i += U * blockDim.x) {
-            uint4 a[U], b[U];
+        if (PF) {
+            uint4 an[U];
+            const bool first = i + (U - 1) * blockDim.x < n4;
+            if (first) {
 #pragma unroll
-            for (int k = 0; k < U; ++k) a[k] = ld_stream(r4 + i + k * blockDim.x);
+                for (int k = 0; k < U; ++k) an[k] = ld_stream(r4 + i + k * blockDim.x);
+            }
+            for (; i + (U - 1) * blockDim.x < n4; i += stride) {
+                uint4 a[U], b[U];
 #pragma unroll
-            for (int k = 0; k < U; ++k) b[k] = __ldg(x4 + i + k * blockDim.x);
+                for (int k = 0; k < U; ++k) a[k] = an[k];
+                if (i + stride + (U - 1) * blockDim.x < n4) {
 #pragma unroll
-            for (int k = 0; k < U; ++k)
-                s += (long long)sredc((int32_t)a[k].x, (int32_t)b[k].x, p, pinv) +
-                     (long long)sredc((int32_t)a[k].y, (int32_t)b[k].y, p, pinv) +
-                     (long long)sredc((int32_t)a[k].z, (int32_t)b[k].z, p, pinv) +
-                     (long long)sredc((int32_t)a[k].w, (int32_t)b[k].w, p, pinv);
+                    for (int k = 0; k < U; ++k) an[k] = ld_stream(r4 + i + stride + k * blockDim.x);
+                }
+#pragma unroll
+                for (int k = 0; k < U; ++k) b[k] = __ldg(x4 + i + k * blockDim.x);
+#pragma unroll
+                for (int k = 0; k < U; ++k)
+                    s += (long long)sredc((int32_t)a[k].x, (int32_t)b[k].x, p, pinv) +
+                         (long long)sredc((int32_t)a[k].y, (int32_t)b[k].y, p, pinv) +
+                         (long long)sredc((int32_t)a[k].z, (int32_t)b[k].z, p, pinv) +
+                         (long long)sredc((int32_t)a[k].w, (int32_t)b[k].w, p, pinv);
+            }
+        } else {
+            for (; i + (U - 1) * blockDim.x < n4; i += stride) {
+                uint4 a[U], b[U];
+#pragma unroll
+                for (int k = 0; k < U; ++k) a[k] = ld_stream(r4 + i + k * blockDim.x);
+#pragma unroll
+                for (int k = 0; k < U; ++k) b[k] = __ldg(x4 + i + k * blockDim.x);
+#pragma unroll
+                for (int k = 0; k < U; ++k)
+                    s += (long long)sredc((int32_t)a[k].x, (int32_t)b[k].x, p, pinv) +
+                         (long long)sredc((int32_t)a[k].y, (int32_t)b[k].y, p, pinv) +
+                         (long long)sredc((int32_t)a[k].z, (int32_t)b[k].z, p, pinv) +
+                         (long long)sredc((int32_t)a[k].w, (int32_t)b[k].w, p, pinv);
+            }
         }
         for (; i < n4; i += blockDim.x) {
             const uint4 a = ld_stream(r4 + i), b = __ldg(x4 + i);
@@ -63,18 +94,163 @@ __global__ void __launch_bounds__(256) k_dot(Ctx c, uint32_t *out, const uint32_
     }
 }
 
+// R rows per CTA against the same x: each thread loads x[i] once and multiplies it into the R rows
+// at the same positions (x's L1 traffic and its registers shrink by R per A byte).  Row-major A,
+// len % 4 == 0 and 16-byte aligned A, x (the launcher checks; otherwise k_dot runs).
+template <int R, int U>
+__global__ void __launch_bounds__(256) k_dot_rows(Ctx c, uint32_t *out, const uint32_t *A, const uint32_t *x,
+                                                   size_t batch, size_t len) {
+    const size_t r0 = (size_t)blockIdx.x * R;
+    const uint4 *x4 = reinterpret_cast<const uint4 *>(x);
+    const size_t n4 = len >> 2;
+    const int32_t p = (int32_t)c.p, pinv = (int32_t)c.pinv;
+    long long s[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[r] = 0;
+    for (size_t i = threadIdx.x; i < n4; i += (size_t)U * blockDim.x) {
+        uint4 a[R][U], b[U];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int k = 0; k < U; ++k)
+                if (r0 + r < batch && i + k * blockDim.x < n4)
+                    a[r][k] = ld_stream(reinterpret_cast<const uint4 *>(A + (r0 + r) * len) + i + k * blockDim.x);
+                else
+                    a[r][k] = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int k = 0; k < U; ++k) b[k] = i + k * blockDim.x < n4 ? __ldg(x4 + i + k * blockDim.x) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int k = 0; k < U; ++k)
+                s[r] += (long long)sredc((int32_t)a[r][k].x, (int32_t)b[k].x, p, pinv) +
+                        (long long)sredc((int32_t)a[r][k].y, (int32_t)b[k].y, p, pinv) +
+                        (long long)sredc((int32_t)a[r][k].z, (int32_t)b[k].z, p, pinv) +
+                        (long long)sredc((int32_t)a[r][k].w, (int32_t)b[k].w, p, pinv);
+    }
+    __shared__ long long part[R][8];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        long long v = s[r];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if (lane == 0) part[r][wid] = v;
+    }
+    __syncthreads();
+    if (wid < R && r0 + wid < batch) {
+        long long v = lane < (int)(blockDim.x >> 5) ? part[wid][lane] : 0ll;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if (lane == 0) {
+            long long rr = v % (long long)c.p;
+            if (rr < 0) rr += c.p;
+            out[r0 + wid] = (uint32_t)rr;
+        }
+    }
+}
+
+// Split rows (the default for rows of >= 2 chunks): CTA b computes chunk b % S of row b / S --
+// `chunk` elements, all of a thread's loads issued before any product (a flat grid of short CTAs
+// streams like mont_mul_vec's, instead of 4096 one-row CTAs in 3.5 waves) -- reduces its exact
+// int64 partial to a canonical residue and adds it into out[row] (zeroed by the launcher) with a
+// modular compare-and-swap loop.  Exact: every partial and every sum is reduced into [0, P).
+template <int U>
+__global__ void __launch_bounds__(256) k_dot_split(Ctx c, uint32_t *out, const uint32_t *A, const uint32_t *x,
+                                                    size_t len, uint32_t S, uint32_t chunk) {
+    const size_t row = blockIdx.x / S;
+    const uint32_t part = blockIdx.x % S;
+    const size_t j0 = (size_t)part * chunk;
+    const size_t j1 = j0 + chunk < len ? j0 + chunk : len;
+    const uint4 *r4 = reinterpret_cast<const uint4 *>(A + row * len + j0);
+    const uint4 *x4 = reinterpret_cast<const uint4 *>(x + j0);
+    const size_t n4 = (j1 - j0) >> 2;  // len % 4 == 0 and chunk % 4 == 0 on this path
+    const int32_t p = (int32_t)c.p, pinv = (int32_t)c.pinv;
+    long long s = 0;
+    size_t i = threadIdx.x;
+    for (; i + (U - 1) * blockDim.x < n4; i += U * blockDim.x) {
+        uint4 a[U], b[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) a[k] = ld_stream(r4 + i + k * blockDim.x);
+#pragma unroll
+        for (int k = 0; k < U; ++k) b[k] = __ldg(x4 + i + k * blockDim.x);
+#pragma unroll
+        for (int k = 0; k < U; ++k)
+            s += (long long)sredc((int32_t)a[k].x, (int32_t)b[k].x, p, pinv) +
+                 (long long)sredc((int32_t)a[k].y, (int32_t)b[k].y, p, pinv) +
+                 (long long)sredc((int32_t)a[k].z, (int32_t)b[k].z, p, pinv) +
+                 (long long)sredc((int32_t)a[k].w, (int32_t)b[k].w, p, pinv);
+    }
+    for (; i < n4; i += blockDim.x) {
+        const uint4 a = ld_stream(r4 + i), b = __ldg(x4 + i);
+        s += (long long)sredc((int32_t)a.x, (int32_t)b.x, p, pinv) + (long long)sredc((int32_t)a.y, (int32_t)b.y, p, pinv) +
+             (long long)sredc((int32_t)a.z, (int32_t)b.z, p, pinv) + (long long)sredc((int32_t)a.w, (int32_t)b.w, p, pinv);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    __shared__ long long partw[8];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) partw[wid] = s;
+    __syncthreads();
+    if (wid == 0) {
+        s = lane < (int)(blockDim.x >> 5) ? partw[lane] : 0ll;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+            long long r = s % (long long)c.p;
+            if (r < 0) r += c.p;
+            if (S == 1) {
+                out[row] = (uint32_t)r;
+            } else {
+                uint32_t old = out[row], assumed;
+                do {  // out[row] = (out[row] + r) mod P, both in [0, P)
+                    assumed = old;
+                    const uint32_t nv = assumed + (uint32_t)r;
+                    old = atomicCAS(out + row, assumed, umin(nv, nv - c.p));
+                } while (old != assumed);
+            }
+        }
+    }
+}
+
 }  // namespace mont
 
 using namespace mont;
 
-extern "C" mont_status_t mont_dot(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *A, const uint32_t *x,
-                                  size_t batch, size_t len, cudaStream_t stream) {
+extern "C" mont_status_t mont_dot_ex(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *A, const uint32_t *x,
+                                     size_t batch, size_t len, const mont_launch_t *cfg, cudaStream_t stream) {
     if (!ctx_ok(ctx)) return ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
     if (batch == 0) return MONT_OK;
     if (len == 0 || len >= (1ull << 32)) return MONT_EINVAL_ARG;
     if (!out || !A || !x || ((uintptr_t)out | (uintptr_t)A | (uintptr_t)x) & 3u) return MONT_EINVAL_ARG;
     if (batch > 0x7fffffffu) return MONT_EUNSUPPORTED;
+    const int variant = cfg ? cfg->variant : 0;
+    const int chunk_req = cfg ? cfg->chunk : 0;
+    if (variant < 0 || variant > 7 || chunk_req < 0 || (chunk_req % 1024) != 0) return MONT_EINVAL_ARG;
     const bool vec = (len % 4 == 0) && (((uintptr_t)A | (uintptr_t)x) & 15u) == 0;
-    k_dot<4><<<(unsigned)batch, 256, 0, stream>>>(to_dev(ctx), out, A, x, len, vec);
+    const uint32_t chunk = chunk_req ? (uint32_t)chunk_req : 4096u;  // 4 uint4 per thread of 256
+    const size_t S = (len + chunk - 1) / chunk;
+    if (variant == 5 && vec && S >= 2 && batch * S <= 0x7fffffffu) {
+        if (cudaMemsetAsync(out, 0, batch * sizeof(uint32_t), stream) != cudaSuccess) return MONT_ECUDA;
+        k_dot_split<4><<<(unsigned)(batch * S), 256, 0, stream>>>(to_dev(ctx), out, A, x, len, (uint32_t)S, chunk);
+        return launch_status();
+    }
+    const Ctx c = to_dev(ctx);
+    if ((variant == 6 || variant == 7) && vec) {
+        if (variant == 6) k_dot_rows<2, 2><<<(unsigned)((batch + 1) / 2), 256, 0, stream>>>(c, out, A, x, batch, len);
+        else k_dot_rows<4, 1><<<(unsigned)((batch + 3) / 4), 256, 0, stream>>>(c, out, A, x, batch, len);
+        return launch_status();
+    }
+    switch (variant) {
+        case 2: k_dot<8, false><<<(unsigned)batch, 256, 0, stream>>>(c, out, A, x, len, vec); break;
+        case 3: k_dot<4, true><<<(unsigned)batch, 256, 0, stream>>>(c, out, A, x, len, vec); break;
+        case 4: k_dot<8, true><<<(unsigned)batch, 256, 0, stream>>>(c, out, A, x, len, vec); break;
+        default: k_dot<4, false><<<(unsigned)batch, 256, 0, stream>>>(c, out, A, x, len, vec); break;  // 0, 1, 5-7
+    }
     return launch_status();
+}
+
+extern "C" mont_status_t mont_dot(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *A, const uint32_t *x,
+                                  size_t batch, size_t len, cudaStream_t stream) {
+    return mont_dot_ex(ctx, out, A, x, batch, len, nullptr, stream);
 }

@@ -354,8 +354,16 @@ if args.what in ("dot",):
     x = torch.empty(L, dtype=torch.uint32, device=dev)
     m.synth_fill(x, 42, 32, 0, P)
     o = torch.empty(batch, dtype=torch.uint32, device=dev)
-    med, _ = timeit(lambda: m.dot(ctx, A, x, out=o))
-    out(what="dot", us=med * 1e6, gbs=4 * batch * L / med / 1e9, gmulmod=batch * L / med / 1e9)
+    ref = m.dot(ctx, A, x, cfg=m.Launch(variant=1))
+    for name, cfg in (("default", None), ("one CTA per row, 4 uint4 (variant 1)", m.Launch(variant=1)),
+                      ("8 uint4 (variant 2)", m.Launch(variant=2)), ("4 uint4 prefetched (variant 3)", m.Launch(variant=3)),
+                      ("8 uint4 prefetched (variant 4)", m.Launch(variant=4)),
+                      ("split 4096 (variant 5)", m.Launch(variant=5)), ("split 8192", m.Launch(variant=5, chunk=8192)),
+                      ("2 rows per CTA (variant 6)", m.Launch(variant=6)), ("4 rows per CTA (variant 7)", m.Launch(variant=7))):
+        med, _ = timeit(lambda: m.dot(ctx, A, x, out=o, cfg=cfg))
+        same = bool((o.view(torch.int32) == ref.view(torch.int32)).all())
+        out(what="dot", launch=name, us=med * 1e6, gbs=4 * batch * L / med / 1e9, gmulmod=batch * L / med / 1e9,
+            equal_to_one_cta_per_row=same)
 
 if args.what in ("tma",):
     import ctypes as C

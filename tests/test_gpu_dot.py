@@ -36,3 +36,28 @@ def test_dot_misaligned_and_extremes(m):
     tA.copy_(torch.from_numpy(A).cuda())
     out = m.dot(m.ctx_init(P), tA, torch.from_numpy(x).cuda())
     assert np.array_equal(out.cpu().numpy(), oracle.dot(P, A, x))
+
+
+@pytest.mark.parametrize("P", [2013265921, 469762049, 3, 2147483647])
+@pytest.mark.parametrize("cfg", [None, (1, 0), (2, 0), (3, 0), (4, 0), (5, 1024), (5, 2048), (5, 0), (5, 8192), (6, 0), (7, 0)])
+@pytest.mark.parametrize("batch,L", [(3, 8192), (5, 16384), (2, 16384 + 1028), (7, 40000), (1, 1 << 20)])
+def test_dot_split_rows(m, P, cfg, batch, L):
+    """The split-row path (chunks per CTA, canonical partials added into out by modular CAS) and
+    the one-CTA-per-row path against the oracle, incl. a ragged last chunk and a stale out."""
+    A = synth.uniform(42, 33, P, 0, batch * L).reshape(batch, L)
+    x = synth.uniform(42, 34, P, 0, L)
+    A[:, -1] = P - 1
+    x[-1] = P - 1
+    launch = None if cfg is None else m.Launch(variant=cfg[0], chunk=cfg[1])
+    out = torch.full((batch,), 12345, dtype=torch.int32, device="cuda").view(torch.uint32)  # stale
+    m.dot(m.ctx_init(P), torch.from_numpy(A).cuda(), torch.from_numpy(x).cuda(), out=out, cfg=launch)
+    assert np.array_equal(out.cpu().numpy(), oracle.dot(P, A, x))
+
+
+def test_dot_ex_rejects(m):
+    ctx = m.ctx_init(2013265921)
+    A = torch.zeros((2, 8192), dtype=torch.int32, device="cuda").view(torch.uint32)
+    x = torch.zeros(8192, dtype=torch.int32, device="cuda").view(torch.uint32)
+    for cfg in (m.Launch(variant=8), m.Launch(chunk=1000)):
+        with pytest.raises(m.MontError):
+            m.dot(ctx, A, x, cfg=cfg)
