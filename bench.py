@@ -69,6 +69,8 @@ LANE_ORDER = tuple(os.environ.get("MONT_LANE_ORDER", "imad,hbm").split(","))
 # it): the persistent pow grid is placed first, one CTA per SM, and the HBM-bound launches fill
 # the rest of every SM (scripts/step_sweep.py, profiles/r02_step_sweep*.jsonl)
 LANE_PRIO = os.environ.get("MONT_LANE_PRIO", "imad")
+# streams the HBM-bound launches are spread over inside the step (independent launches only)
+HBM_STREAMS = int(os.environ.get("MONT_HBM_STREAMS", "2"))
 
 
 def parse():
@@ -343,21 +345,37 @@ class Workload:
         self.hbm_cfg = self.hbm_cfg_lane if both else {}   # lane shapes only next to a pow lane
         if not hasattr(self, "_lanes"):
             self._lanes = {ln: torch.cuda.Stream(priority=-1 if ln == LANE_PRIO else 0) for ln in ("hbm", "imad")}
+        nh = max(1, HBM_STREAMS)
+        if len(getattr(self, "_hbm_extra", [])) != nh - 1:
+            self._hbm_extra = [torch.cuda.Stream(priority=-1 if LANE_PRIO == "hbm" else 0) for _ in range(nh - 1)]
+        hbm_streams = [self._lanes["hbm"]] + self._hbm_extra
+        # HBM launches that do not depend on each other go to different streams (graph branches), so
+        # one kernel's tail overlaps the next one's ramp; to_mont -> from_mont stay in order
+        groups = []
+        for name, *_rest in self.launches:
+            g = "conv" if name in ("to_mont", "from_mont") else name
+            if _rest[-1] == "hbm" and g not in groups:
+                groups.append(g)
         ev = torch.cuda.Event()
         ev.record(cur)
-        for st in self._lanes.values():
+        for st in list(self._lanes.values()) + self._hbm_extra:
             st.wait_event(ev)
         for lane in LANE_ORDER:
-            st = self._lanes[lane]
-            with torch.cuda.stream(st):
-                for i, (_, fn, _, _, bound) in enumerate(self.launches):
-                    if bound == lane:
-                        if self.lane_events is not None:   # external events: graph event-record nodes
-                            self.lane_events[i][0].record(st)
-                        fn()
-                        if self.lane_events is not None:
-                            self.lane_events[i][1].record(st)
-        for st in self._lanes.values():
+            for i, (name, fn, _, _, bound) in enumerate(self.launches):
+                if bound != lane:
+                    continue
+                if lane == "hbm":
+                    g = "conv" if name in ("to_mont", "from_mont") else name
+                    st = hbm_streams[groups.index(g) % nh]
+                else:
+                    st = self._lanes[lane]
+                with torch.cuda.stream(st):
+                    if self.lane_events is not None:   # external events: graph event-record nodes
+                        self.lane_events[i][0].record(st)
+                    fn()
+                    if self.lane_events is not None:
+                        self.lane_events[i][1].record(st)
+        for st in list(self._lanes.values()) + self._hbm_extra:
             cur.wait_stream(st)
         self.pow_cfg = None
         self.hbm_cfg = {}
