@@ -658,26 +658,40 @@ def imad_launch_clock_mhz(wl: Workload, K: int):
     return statistics.median(v) if v else None
 
 
-def in_step_kernel_times(wl: Workload, K: int):
-    """Each launch's duration INSIDE the two-lane step, co-running as timed: a second capture of
-    the same step with external CUDA events (graph event-record nodes) on each launch's own lane
-    stream around it, replayed K times; median per launch over the replays (a synchronize between
-    replays to read the events, outside any timed region)."""
+def in_step_kernel_times(wl: Workload, K: int, hbm_streams: int):
+    """Each launch's duration INSIDE the two-lane step: a second capture of the same step with
+    external CUDA events (graph event-record nodes) on each launch's own stream around it, replayed
+    K times; median per launch over the replays (a synchronize between replays to read the events,
+    outside any timed region).  With hbm_streams = 1 each HBM launch has the memory system to
+    itself (only the pow lane co-runs), so bytes / duration is that kernel's rate; with the timed
+    configuration's streams, the HBM lane's wall time (first HBM launch start to last end) gives
+    the lane's aggregate rate.  Returns (per-launch ms, {lane: wall ms})."""
+    global HBM_STREAMS
     torch = wl.torch
+    saved = HBM_STREAMS
+    HBM_STREAMS = hbm_streams
     wl.lane_events = [(torch.cuda.Event(enable_timing=True, external=True),
                        torch.cuda.Event(enable_timing=True, external=True)) for _ in wl.launches]
     try:
         g = capture_step_graph(wl)
         per = [[] for _ in wl.launches]
+        span = {}
         for _ in range(max(3, K)):
             g.replay()
             torch.cuda.synchronize()
             for i, (e0, e1) in enumerate(wl.lane_events):
                 per[i].append(e0.elapsed_time(e1))
+            for lane in {b for *_, b in wl.launches}:
+                idx = [i for i, (*_, b) in enumerate(wl.launches) if b == lane]
+                ref = wl.lane_events[idx[0]][0]
+                t0 = min(ref.elapsed_time(wl.lane_events[i][0]) for i in idx)
+                t1 = max(ref.elapsed_time(wl.lane_events[i][1]) for i in idx)
+                span.setdefault(lane, []).append(t1 - t0)
         del g
-        return [statistics.median(v) for v in per]
+        return [statistics.median(v) for v in per], {k: statistics.median(v) for k, v in span.items()}
     finally:
         wl.lane_events = None
+        HBM_STREAMS = saved
 
 
 def time_steps_graph(wl: Workload, g, K: int):
@@ -1025,7 +1039,10 @@ def main():
         graph.replay()
         torch.cuda.synchronize()
     post = verify(wl, run=False) if graph is not None else {}
-    in_step_ms = in_step_kernel_times(wl, args.steps) if graph is not None else None
+    # per-kernel in-step durations: HBM launches one after another (each alone on the memory
+    # system, co-running with pow); lane wall times: the timed configuration
+    in_step_ms, _ = in_step_kernel_times(wl, args.steps, 1) if graph is not None else (None, None)
+    _, lane_wall = in_step_kernel_times(wl, args.steps, HBM_STREAMS) if graph is not None else (None, None)
     post_ok = shard.max_over_ranks(0.0 if all(post.values()) else 1.0) == 0.0
     if not post_ok:
         if rank == 0:
@@ -1179,11 +1196,20 @@ def main():
     standalone = next(r for r in rooflines if r["kernel"] == dom_r["kernel"])
     roof["frac_standalone"] = standalone["frac"]
     if in_step:
-        roof["duration"] = ("inside the timed two-lane step: median over K replays of the step graph of the "
-                            "interval between external CUDA events captured around the launch on its own lane "
-                            "stream (co-running with the other lane exactly as timed)")
+        roof["duration"] = ("inside the two-lane step: median over K replays of a capture of the step graph with "
+                            "external CUDA events around each launch on its own stream, co-running with the pow "
+                            "lane as timed, the HBM launches one after another (the timed graph spreads them over "
+                            f"{HBM_STREAMS} streams: see hbm_lane)")
         roof["lanes_ms_in_step"] = {k: round(v, 4) for k, v in lanes.items()}
         roof["critical_lane"] = crit
+        if lane_wall and "hbm" in lane_wall:
+            hb = sum(nb for _, _, nb, _, b in wl.launches if b == "hbm")
+            w = lane_wall["hbm"]
+            roof["hbm_lane"] = {"streams": HBM_STREAMS, "wall_ms": round(w, 4), "bytes": hb,
+                                "achieved_gbs": round(hb / (w * 1e-3) / 1e9, 1),
+                                "frac": round(hb / (w * 1e-3) / 1e9 / hbm_peak, 4),
+                                "what": "all HBM launches of the step as timed (first start to last end, external "
+                                        "graph events), algorithmic bytes / wall time"}
     else:
         roof["duration"] = "median over the K timed steps of a serial pass with CUDA events around each launch"
     line = {
