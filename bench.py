@@ -69,6 +69,9 @@ LANE_ORDER = tuple(os.environ.get("MONT_LANE_ORDER", "imad,hbm").split(","))
 # it): the persistent pow grid is placed first, one CTA per SM, and the HBM-bound launches fill
 # the rest of every SM (scripts/step_sweep.py, profiles/r02_step_sweep*.jsonl)
 LANE_PRIO = os.environ.get("MONT_LANE_PRIO", "imad")
+# the HBM lane of the step: "run" = one mont_run launch over all HBM jobs, "streams" = the
+# individual launches spread over HBM_STREAMS streams
+HBM_MODE = os.environ.get("MONT_HBM_MODE", "run")
 # streams the HBM-bound launches are spread over inside the step (independent launches only)
 HBM_STREAMS = int(os.environ.get("MONT_HBM_STREAMS", "2"))
 
@@ -326,6 +329,37 @@ class Workload:
     def mulmods(self):
         return sum(x[3] for x in self.launches)
 
+    @property
+    def step_launches(self):
+        """The launches of the two-lane step: the HBM-bound ones as ONE mont_run (include/
+        mont_run.h: one flat grid over all their tiles, to_mont -> from_mont fused) when
+        HBM_MODE == "run", else individually; the IMAD-bound ones as they are."""
+        hbm = [x for x in self.launches if x[4] == "hbm"]
+        if HBM_MODE != "run" or len(hbm) < 2:
+            return self.launches
+        if not hasattr(self, "_run_launch"):
+            m = self.m
+            jobs = []
+            for name, *_ in hbm:
+                if name.startswith("mont_mul_vec_checksum[P="):
+                    P = int(name.split("=")[1].rstrip("]"))
+                    a, b, c = self.c2[P]
+                    si = PRIMES.index(P)
+                    jobs.append(m.run_job("mul_vec", self.ctx[P], c, a, b, acc=self.acc[si:si + 1]))
+                elif name == "to_mont":
+                    jobs.append(m.run_job("to_mont", self.ctx[P0], self.abar, self.c2[P0][0]))
+                elif name == "from_mont":
+                    jobs.append(m.run_job("from_mont", self.ctx[P0], self.back, self.abar))
+                elif name == "mont_mul_twiddle":
+                    jobs.append(m.run_job("twiddle", self.ctx[P0], self.tw_out.view(-1), self.tw_x.view(-1), self.tw))
+                else:
+                    raise RuntimeError(f"no mont_run job for {name}")
+            self.run_jobs = jobs
+            self.run_bytes = m.run_bytes(jobs)
+            self._run_launch = ("mont_run[hbm lane: " + ", ".join(x[0] for x in hbm) + "]",
+                                lambda: m.run(self.run_jobs), self.run_bytes, sum(x[3] for x in hbm), "hbm")
+        return [self._run_launch] + [x for x in self.launches if x[4] != "hbm"]
+
     def step(self):
         """Serial step: every launch in order on the current stream."""
         for _, fn, *_ in self.launches:
@@ -340,7 +374,8 @@ class Workload:
         torch = self.torch
         cur = torch.cuda.current_stream()
         # the persistent pow grid only pays when HBM-bound launches co-run with it
-        both = {b for *_, b in self.launches} >= {"hbm", "imad"}
+        launches = self.step_launches
+        both = {b for *_, b in launches} >= {"hbm", "imad"}
         self.pow_cfg = getattr(self, "pow_cfg_lane", None) if both else None
         self.hbm_cfg = self.hbm_cfg_lane if both else {}   # lane shapes only next to a pow lane
         if not hasattr(self, "_lanes"):
@@ -352,7 +387,7 @@ class Workload:
         # HBM launches that do not depend on each other go to different streams (graph branches), so
         # one kernel's tail overlaps the next one's ramp; to_mont -> from_mont stay in order
         groups = []
-        for name, *_rest in self.launches:
+        for name, *_rest in launches:
             g = "conv" if name in ("to_mont", "from_mont") else name
             if _rest[-1] == "hbm" and g not in groups:
                 groups.append(g)
@@ -361,7 +396,7 @@ class Workload:
         for st in list(self._lanes.values()) + self._hbm_extra:
             st.wait_event(ev)
         for lane in LANE_ORDER:
-            for i, (name, fn, _, _, bound) in enumerate(self.launches):
+            for i, (name, fn, _, _, bound) in enumerate(launches):
                 if bound != lane:
                     continue
                 if lane == "hbm":
@@ -658,40 +693,41 @@ def imad_launch_clock_mhz(wl: Workload, K: int):
     return statistics.median(v) if v else None
 
 
-def in_step_kernel_times(wl: Workload, K: int, hbm_streams: int):
-    """Each launch's duration INSIDE the two-lane step: a second capture of the same step with
+def in_step_kernel_times(wl: Workload, K: int, hbm_mode: str, hbm_streams: int):
+    """Each launch's duration INSIDE the two-lane step: a second capture of the step graph with
     external CUDA events (graph event-record nodes) on each launch's own stream around it, replayed
     K times; median per launch over the replays (a synchronize between replays to read the events,
-    outside any timed region).  With hbm_streams = 1 each HBM launch has the memory system to
-    itself (only the pow lane co-runs), so bytes / duration is that kernel's rate; with the timed
-    configuration's streams, the HBM lane's wall time (first HBM launch start to last end) gives
-    the lane's aggregate rate.  Returns (per-launch ms, {lane: wall ms})."""
-    global HBM_STREAMS
+    outside any timed region).  hbm_mode / hbm_streams select how the HBM lane is issued: "streams"
+    with 1 stream gives each individual HBM kernel the memory system to itself (only the pow lane
+    co-runs); the timed configuration gives the lane as timed.  Returns (the step's launch list,
+    per-launch ms, {lane: wall ms from its first launch's start to its last launch's end})."""
+    global HBM_STREAMS, HBM_MODE
     torch = wl.torch
-    saved = HBM_STREAMS
-    HBM_STREAMS = hbm_streams
+    saved = HBM_STREAMS, HBM_MODE
+    HBM_STREAMS, HBM_MODE = hbm_streams, hbm_mode
+    launches = wl.step_launches
     wl.lane_events = [(torch.cuda.Event(enable_timing=True, external=True),
-                       torch.cuda.Event(enable_timing=True, external=True)) for _ in wl.launches]
+                       torch.cuda.Event(enable_timing=True, external=True)) for _ in launches]
     try:
         g = capture_step_graph(wl)
-        per = [[] for _ in wl.launches]
+        per = [[] for _ in launches]
         span = {}
         for _ in range(max(3, K)):
             g.replay()
             torch.cuda.synchronize()
             for i, (e0, e1) in enumerate(wl.lane_events):
                 per[i].append(e0.elapsed_time(e1))
-            for lane in {b for *_, b in wl.launches}:
-                idx = [i for i, (*_, b) in enumerate(wl.launches) if b == lane]
+            for lane in {b for *_, b in launches}:
+                idx = [i for i, (*_, b) in enumerate(launches) if b == lane]
                 ref = wl.lane_events[idx[0]][0]
                 t0 = min(ref.elapsed_time(wl.lane_events[i][0]) for i in idx)
                 t1 = max(ref.elapsed_time(wl.lane_events[i][1]) for i in idx)
                 span.setdefault(lane, []).append(t1 - t0)
         del g
-        return [statistics.median(v) for v in per], {k: statistics.median(v) for k, v in span.items()}
+        return launches, [statistics.median(v) for v in per], {k: statistics.median(v) for k, v in span.items()}
     finally:
         wl.lane_events = None
-        HBM_STREAMS = saved
+        HBM_STREAMS, HBM_MODE = saved
 
 
 def time_steps_graph(wl: Workload, g, K: int):
@@ -1041,8 +1077,23 @@ def main():
     post = verify(wl, run=False) if graph is not None else {}
     # per-kernel in-step durations: HBM launches one after another (each alone on the memory
     # system, co-running with pow); lane wall times: the timed configuration
-    in_step_ms, _ = in_step_kernel_times(wl, args.steps, 1) if graph is not None else (None, None)
-    _, lane_wall = in_step_kernel_times(wl, args.steps, HBM_STREAMS) if graph is not None else (None, None)
+    in_step_ms = timed_launches = timed_ms = lane_wall = None
+    if graph is not None:
+        _, in_step_ms, _ = in_step_kernel_times(wl, args.steps, "streams", 1)
+        timed_launches, timed_ms, lane_wall = in_step_kernel_times(wl, args.steps, HBM_MODE, HBM_STREAMS)
+    # the HBM lane's one mont_run launch alone (its standalone rate), when the step uses it
+    run_alone_ms = None
+    if graph is not None and HBM_MODE == "run" and hasattr(wl, "_run_launch"):
+        fn = wl._run_launch[1]
+        for _ in range(3):
+            fn()
+        evr = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+        for e0, e1 in evr:
+            e0.record()
+            fn()
+            e1.record()
+        torch.cuda.synchronize()
+        run_alone_ms = statistics.median(e0.elapsed_time(e1) for e0, e1 in evr)
     post_ok = shard.max_over_ranks(0.0 if all(post.values()) else 1.0) == 0.0
     if not post_ok:
         if rank == 0:
@@ -1136,10 +1187,10 @@ def main():
     hbm_peak, peak_kind, sm_max = peaks()
     sms = torch.cuda.get_device_properties(0).multi_processor_count
 
-    def kernel_rows(times, imad_clk_mhz):
+    def kernel_rows(times, imad_clk_mhz, launches=None):
         clk = (imad_clk_mhz or clocks.get("sm_mhz") or sm_max) * 1e6
         rows = []
-        for (name, _, nbytes, mm, bound), t in zip(wl.launches, times):
+        for (name, _, nbytes, mm, bound), t in zip(launches or wl.launches, times):
             r = {"kernel": name, "ms": round(t, 4), "share": round(t / max(sum(times), 1e-9), 4),
                  "gmulmod_s": round(mm / (t * 1e-3) / 1e9, 2) if mm else None, "lane": bound}
             if bound == "hbm":
@@ -1170,9 +1221,10 @@ def main():
 
     rooflines = kernel_rows(per_ms, imad_mhz)   # standalone, serial pass, library-default shapes
     in_step = kernel_rows(in_step_ms, None) if in_step_ms else None
-    # dominant kernel: in the timed step, the longest lane (the critical path) and within it the
-    # kernel kind with the largest share; without a lane schedule, the serial pass
-    src = in_step if in_step else rooflines
+    timed_rows = kernel_rows(timed_ms, None, timed_launches) if timed_ms else None
+    # dominant kernel: in the timed step (its own launches), the longest lane (the critical path)
+    # and within it the kernel kind with the largest share; without a lane schedule, the serial pass
+    src = timed_rows if timed_rows else rooflines
     lanes = {}
     for r in src:
         lanes[r["lane"]] = lanes.get(r["lane"], 0.0) + r["ms"]
@@ -1193,19 +1245,27 @@ def main():
     if triad_gbs is not None and dom_r["bound"] == "hbm":
         roof["triad_gbs"] = round(triad_gbs, 1)
         roof["frac_triad"] = round(dom_r["achieved"] / triad_gbs, 4)
-    standalone = next(r for r in rooflines if r["kernel"] == dom_r["kernel"])
-    roof["frac_standalone"] = standalone["frac"]
-    if in_step:
-        roof["duration"] = ("inside the two-lane step: median over K replays of a capture of the step graph with "
-                            "external CUDA events around each launch on its own stream, co-running with the pow "
-                            "lane as timed, the HBM launches one after another (the timed graph spreads them over "
-                            f"{HBM_STREAMS} streams: see hbm_lane)")
+    standalone = next((r for r in rooflines if r["kernel"] == dom_r["kernel"]), None)
+    if standalone is not None:
+        roof["frac_standalone"] = standalone["frac"]
+    elif run_alone_ms and dom_r["kernel"].startswith("mont_run"):
+        roof["frac_standalone"] = round(wl.run_bytes / (run_alone_ms * 1e-3) / 1e9 / hbm_peak, 4)
+        roof["ms_standalone"] = round(run_alone_ms, 4)
+    if dom_r["kernel"].startswith("mont_run"):
+        roof["bytes_per_launch"] = wl.run_bytes
+        roof["bytes_note"] = ("algorithmic bytes of the run by plan (mont_run_bytes): every job's reads and writes, "
+                              "the fused to_mont -> from_mont pair reading its input once (12 B per element)")
+    if timed_rows:
+        roof["duration"] = ("inside the timed two-lane step: median over K replays of a capture of the step graph "
+                            "with external CUDA events around each launch on its own stream, co-running with the "
+                            "pow lane as timed")
         roof["lanes_ms_in_step"] = {k: round(v, 4) for k, v in lanes.items()}
         roof["critical_lane"] = crit
         if lane_wall and "hbm" in lane_wall:
-            hb = sum(nb for _, _, nb, _, b in wl.launches if b == "hbm")
+            hb = sum(nb for _, _, nb, _, b in timed_launches if b == "hbm")
             w = lane_wall["hbm"]
-            roof["hbm_lane"] = {"streams": HBM_STREAMS, "wall_ms": round(w, 4), "bytes": hb,
+            roof["hbm_lane"] = {"mode": HBM_MODE, "streams": HBM_STREAMS if HBM_MODE != "run" else 1,
+                                "wall_ms": round(w, 4), "bytes": hb,
                                 "achieved_gbs": round(hb / (w * 1e-3) / 1e9, 1),
                                 "frac": round(hb / (w * 1e-3) / 1e9 / hbm_peak, 4),
                                 "what": "all HBM launches of the step as timed (first start to last end, external "
@@ -1231,23 +1291,30 @@ def main():
                            "c5": f"{12 * (N_C5 // world) / 2**30:.0f} GiB", "ntt": "256 MiB"}[wl.kind] +
                           " vs 126 MB L2)"),
                    "mulmods_per_step_per_rank": wl.mulmods, **wl.config},
-        "gpu_launches": len(wl.launches) * args.steps,
+        "gpu_launches": (len(wl.step_launches) if graph is not None else len(wl.launches)) * args.steps,
         "schedule": ("each step alone between CUDA events after an L2 flush" if wl.kind == "c1" else
                      "serial, one stream" if args.serial else
-                     "two lanes: the HBM-bound launches in order on one stream (mul_vec+checksum 256 threads x 2 "
-                     "uint4, to/from_mont 256 x 4, twiddle default), the IMAD-bound pow on another, higher-priority "
+                     ("two lanes: the HBM-bound operations as ONE mont_run launch (one flat grid over all their "
+                      "tiles, 256 threads x 2 uint4, to_mont -> from_mont fused)" if HBM_MODE == "run" else
+                      f"two lanes: the HBM-bound launches on {HBM_STREAMS} stream(s) (mul_vec+checksum 256 threads x 2 "
+                      "uint4, to/from_mont 256 x 4, twiddle default)") +
+                     ", the IMAD-bound pow on another, higher-priority "
                      f"stream as a persistent grid of {POW_CTAS} CTA(s) per SM (mont_pow_vec_ex variant {POW_VARIANT})" +
                      (", replayed as one CUDA graph" if args.graph else "")),
         "ms_per_step_serial": round(serial_ms / args.steps, 5),
         "roofline": roof,
         "kernels": rooflines,
         "kernels_note": ("'kernels': each launch alone (serial pass, library-default launch shapes); "
-                         "'kernels_in_step': the same launches inside the timed two-lane step"),
+                         "'kernels_in_step': the same individual launches inside the two-lane step (HBM ones one "
+                         "after another next to the pow lane); 'kernels_timed_step': the launches of the timed "
+                         "step itself (the HBM lane as one mont_run launch)"),
         "clocks": {k: clocks.get(k) for k in ("sm_mhz", "sm_max_mhz", "reasons", "samples", "samples_under_load")},
         "parity": {"checks": checks, "box_checksums": box_checksums},
     }
     if in_step:
         line["kernels_in_step"] = in_step
+    if timed_rows and timed_launches is not wl.launches:
+        line["kernels_timed_step"] = timed_rows
     if latency_us is not None:
         line["latency_us"] = latency_us
     if c5 is not None:

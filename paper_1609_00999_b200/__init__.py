@@ -122,6 +122,18 @@ class HostJob(C.Structure):
 
 
 SIGNATURES["mont_host_run"] = (C.c_int, [C.POINTER(HostJob), C.c_int, _P, _S, _P])
+
+RUN_OPS = {"mul_vec": 0, "to_mont": 1, "from_mont": 2, "twiddle": 3}
+
+
+class RunJob(C.Structure):
+    """mont_run_job_t (include/mont_run.h)."""
+    _fields_ = [("op", C.c_int), ("ctx", _CTX), ("out", C.c_void_p), ("in0", C.c_void_p), ("in1", C.c_void_p),
+                ("n", C.c_size_t), ("len", C.c_size_t), ("acc", C.c_void_p)]
+
+
+SIGNATURES["mont_run"] = (C.c_int, [C.POINTER(RunJob), C.c_int, _P])
+SIGNATURES["mont_run_bytes"] = (C.c_int, [C.POINTER(RunJob), C.c_int, C.POINTER(C.c_ulonglong)])
 SIGNATURES["mont_host_run_bytes"] = (C.c_int, [C.POINTER(HostJob), C.c_int, C.POINTER(C.c_ulonglong),
                                                C.POINTER(C.c_ulonglong)])
 
@@ -499,6 +511,35 @@ def host_job(op: str, ctx: Ctx, out, in0, in1=None, acc=None, depends_on: int = 
     j.depends_on = int(depends_on)
     j._keep = (ctx, out, in0, in1, acc)  # keep the referenced objects alive
     return j
+
+
+def run_job(op: str, ctx: Ctx, out, in0, in1=None, acc=None) -> RunJob:
+    """Describe one operation on DEVICE tensors for run() (include/mont_run.h); twiddle: in0 = x
+    (batch, len) or flat with in1 = the len-word table; mul_vec: acc = optional int64 tensor (1,)."""
+    j = RunJob()
+    j.op = RUN_OPS[op]
+    j.ctx = C.pointer(ctx)
+    j.out, j.in0 = _ptr(_dev_u32(out, "out")), _ptr(_dev_u32(in0, "in0"))
+    j.in1 = _ptr(_dev_u32(in1, "in1")) if in1 is not None else None
+    j.n = in0.numel()
+    j.len = in1.numel() if op == "twiddle" else 0
+    j.acc = _ptr(acc) if acc is not None else None
+    j._keep = (ctx, out, in0, in1, acc)
+    return j
+
+
+def run(jobs, stream=None):
+    """Run the jobs as one launch (mont_run): independent HBM-bound operations back to back in one
+    flat grid; a from_mont reading an earlier to_mont's output is fused into it."""
+    arr = (RunJob * len(jobs))(*jobs)
+    _check(lib().mont_run(arr, len(jobs), _stream_handle(stream)), "mont_run")
+
+
+def run_bytes(jobs) -> int:
+    arr = (RunJob * len(jobs))(*jobs)
+    b = C.c_ulonglong(0)
+    _check(lib().mont_run_bytes(arr, len(jobs), C.byref(b)), "mont_run_bytes")
+    return int(b.value)
 
 
 def host_run(jobs, ws, stream=None):

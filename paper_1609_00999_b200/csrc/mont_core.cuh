@@ -77,11 +77,14 @@ __device__ __forceinline__ uint32_t redc(uint32_t a, uint32_t b, uint32_t p, uin
     return umin(t, t + p);                 // t < 0 (wrapped) -> t + P
 }
 
-// REDC(x * 1) = x R^-1 mod P (A10): T = x, hi(T) = 0
+// REDC(x * 1) = x R^-1 mod P (A10): T = x, hi(T) = 0, so t = -hi(m P) and the canonical value
+// is P - hi(m P), or 0 when hi(m P) = 0.  Written as a select, not as min(t, t + P): for that
+// form NVVM emits neg / sub / min.u32, and ptxas 12.9 fused it in one kernel (k_run) into a
+// VIADDMNMX that added +hi instead of -hi (wrong results; tests/test_gpu_run.py caught it).
 __device__ __forceinline__ uint32_t redc1(uint32_t x, uint32_t p, uint32_t pinv) {
     const uint32_t m = x * pinv;
-    const uint32_t t = 0u - hi32(mul_wide_u32(m, p));
-    return umin(t, t + p);
+    const uint32_t h = hi32(mul_wide_u32(m, p));
+    return h ? p - h : 0u;
 }
 
 // signed lazy form for chains: |a|, |b| < P  ->  result in (-P, P),

@@ -27,9 +27,10 @@ def main():
     assert all(bench.verify(wl).values())
     L = m.Launch
     # (variant, ctas_per_sm, reserved smem bytes): ctas 0 = flat grid
-    pows = [(10, 1, 0), (11, 1, 0)]
+    pows = [(10, 1, 0), (11, 1, 0), (10, 2, 0)]
     prios = ["imad"]
     hstreams = [int(v) for v in os.environ.get("SWEEP_HBM_STREAMS", "1").split(",")]
+    modes = os.environ.get("SWEEP_HBM_MODES", "streams").split(",")
     if os.environ.get("SWEEP_WIDE"):
         pows = [(11, 0, 0), (11, 0, 200 * 1024), (11, 0, 110 * 1024), (11, 0, 72 * 1024), (11, 0, 54 * 1024),
                 (11, 1, 0), (11, 2, 0), (10, 2, 0)]
@@ -51,10 +52,12 @@ def main():
     }
     only = os.environ.get("SWEEP_HBM")
     rebuilds = int(os.environ.get("SWEEP_REBUILDS", "2"))
-    for (pv, pc, sm), (hname, hcfg), prio, hs in itertools.product(pows, hbms.items(), prios, hstreams):
+    for (pv, pc, sm), (hname, hcfg), prio, hs, mode in itertools.product(pows, hbms.items(), prios, hstreams, modes):
         if only and hname not in only.split(","):
             continue
-        bench.HBM_STREAMS = hs
+        if mode == "run" and (hs != 1 or hname != "default"):
+            continue   # the run has its own launch shape and one launch
+        bench.HBM_STREAMS, bench.HBM_MODE = hs, mode
         wl.pow_cfg_lane = L(ctas_per_sm=pc, variant=pv, chunk=sm)
         wl.hbm_cfg_lane = {k: v for k, v in hcfg.items() if v is not None}
         # lane streams: torch priority -1 = high, 0 = low (graph kernel nodes inherit it)
@@ -72,7 +75,8 @@ def main():
             torch.cuda.synchronize()
             ts = [bench.time_steps_graph(wl, g, 20) / 20 for _ in range(3)]
             ok = all(bench.verify(wl, run=False).values())
-            print(json.dumps({"pow": [pv, pc, sm], "hbm": hname, "prio": prio, "hbm_streams": hs, "rebuild": rb,
+            print(json.dumps({"pow": [pv, pc, sm], "hbm": hname, "prio": prio, "hbm_streams": hs, "mode": mode,
+                              "rebuild": rb,
                               "ms_per_step": round(statistics.median(ts), 4), "ms_best": round(min(ts), 4),
                               "outputs_ok": ok}), flush=True)
             del g

@@ -146,3 +146,55 @@ def test_host_run_bytes_fusion_plan():
     assert m.host_run_bytes([m.host_job("mul_vec", ctx, c, a, a)]) == (4 * n, 4 * n)
     with pytest.raises(m.MontError):
         m.host_run_bytes([m.host_job("from_mont", ctx, f, t, depends_on=0)])  # depends on itself
+
+
+def _run_job(op, ctx, out, in0, in1=0, n=0, length=0, acc=0):
+    j = m.RunJob()
+    j.op, j.ctx, j.out, j.in0, j.in1, j.n, j.len, j.acc = op, C.pointer(ctx), out, in0, in1 or None, n, length, acc or None
+    return j
+
+
+def test_run_plan_bytes_and_validation():
+    """mont_run's planner on the host (fake, never dereferenced device addresses): the fused
+    to_mont -> from_mont pair is counted once (12 B/element instead of 16), and every dependency
+    other than that pair is refused before any launch."""
+    lib = m.lib()
+    c0 = m.ctx_init(2013265921)
+    c1 = m.ctx_init(469762049)
+    MB = 1 << 20
+    A, B, Cc, D, E, F, T = (0x10000000 + k * 64 * MB for k in range(7))
+    n = 1 << 20
+    acc = 0x7f000000
+
+    def bytes_of(jobs):
+        arr = (m.RunJob * len(jobs))(*jobs)
+        b = C.c_ulonglong(0)
+        st = lib.mont_run_bytes(arr, len(jobs), C.byref(b))
+        return st, b.value
+
+    mul = _run_job(0, c0, Cc, A, B, n, acc=acc)
+    to = _run_job(1, c0, D, A, n=n)
+    frm = _run_job(2, c0, E, D, n=n)
+    tw = _run_job(3, c0, F, T, A, n=n, length=4096)
+    st, b = bytes_of([mul, to, frm, tw])
+    assert st == 0 and b == 12 * n + 12 * n + (8 * n + 4 * 4096)
+    assert bytes_of([mul])[1] == 12 * n and bytes_of([frm])[1] == 8 * n
+    # the chain with a different modulus is not a fused pair: a dependency -> refused
+    frm1 = _run_job(2, c1, E, D, n=n)
+    assert bytes_of([to, frm1])[0] == 2
+    # FROM before its producer, overlapping outputs, a job reading another's output, partial aliasing
+    assert bytes_of([frm, to])[0] == 2
+    assert bytes_of([mul, _run_job(1, c0, Cc, A, n=n)])[0] == 2
+    assert bytes_of([mul, _run_job(0, c0, D, Cc, B, n=n)])[0] == 2
+    assert bytes_of([_run_job(1, c0, A + 16, A, n=n)])[0] == 2
+    # in place is fine; n % 4, alignment, op, twiddle len, acc on a non-mul job, too many jobs
+    assert bytes_of([_run_job(1, c0, A, A, n=n)])[0] == 0
+    assert bytes_of([_run_job(1, c0, D, A, n=n + 2)])[0] == 2
+    assert bytes_of([_run_job(1, c0, D + 4, A, n=n)])[0] == 2
+    assert bytes_of([_run_job(7, c0, D, A, n=n)])[0] == 2
+    assert bytes_of([_run_job(3, c0, F, T, A, n=n, length=3000)])[0] == 2
+    assert bytes_of([_run_job(1, c0, D, A, n=n, acc=acc)])[0] == 2
+    assert bytes_of([to] * 17)[0] == 2
+    bad = m.Ctx()
+    assert bytes_of([_run_job(1, bad, D, A, n=n)])[0] == 1
+    assert bytes_of([])[0] == 0 and bytes_of([])[1] == 0
