@@ -268,6 +268,32 @@ if args.what == "powctx":
             out(what="powctx", ctx=ctxname, variant=variant, us=tm, mhz_after=cm, floor_us_at_that_clock=floor_us,
                 frac_floor=floor_us / tm, tmulmod=useful / tm / 1e6)
 
+if args.what == "run":
+    # the step's HBM lane alone: individual launches (library defaults / the lane's shapes) vs ONE
+    # mont_run launch (to_mont -> from_mont fused), CUDA events, no pow lane
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    import bench
+    wl = bench.Workload("step", 0, 1)
+    hbm = [x for x in wl.launches if x[4] == "hbm"]
+    nbytes = sum(x[2] for x in hbm)
+
+    def serial(cfgs):
+        wl.hbm_cfg = cfgs
+        for _, fn, *_ in hbm:
+            fn()
+        wl.hbm_cfg = {}
+
+    bench.HBM_MODE = "run"
+    run_l = wl.step_launches[0]
+    L = m.Launch
+    for name, fn in (("individual, library defaults", lambda: serial({})),
+                     ("individual, lane shapes 256x2 / 256x4",
+                      lambda: serial({"mul": L(threads=256, unroll=2), "conv": L(threads=256, unroll=4)})),
+                     ("one mont_run (to/from fused)", run_l[1])):
+        med, best = timeit(fn, reps=20)
+        out(what="run", how=name, us=med * 1e6, us_best=best * 1e6, bytes_individual=nbytes, bytes_run=wl.run_bytes,
+            gbs_algorithmic=(wl.run_bytes if "run" in name else nbytes) / med / 1e9)
+
 if args.what in ("pcie",):
     n = 1 << 26   # 256 MiB
     hs = [torch.empty(n, dtype=torch.uint32, pin_memory=True) for _ in range(2)]
