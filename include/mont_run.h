@@ -5,7 +5,7 @@
  * three mul_vec, the to_mont / from_mont pair, configs[2]'s twiddle multiply).  Issued one by
  * one, every launch pays its own ramp (CTAs reaching the SMs) and tail (the last partial wave)
  * with the memory system idle in between.  mont_run runs a list of such jobs as one flat grid:
- * the tiles of all jobs back to back, each CTA one 256-thread x 2 x 16 B tile of one job, so the
+ * the tiles of all jobs back to back, each CTA one 512-thread x 2 x 16 B tile of one job, so the
  * memory stream never drains between jobs.  A from_mont job whose input is exactly the output of
  * an earlier to_mont job (same n, same modulus) is fused into it: from_mont(x-bar) is computed
  * from the register that to_mont just produced (the conversions bracket a chain),
@@ -60,6 +60,13 @@ typedef struct mont_run_job {
  * pointer, n % 4 != 0, a bad op / len, or a dependency other than the fused pair;
  * MONT_EINVAL_P for a context that was not initialised; MONT_ECUDA for a failed launch. */
 mont_status_t mont_run(const mont_run_job_t *jobs, int njobs, cudaStream_t stream);
+
+/* mont_run with an explicit tile shape (measurement): cfg->threads 256 or 512 (0 = 512),
+ * cfg->unroll 1, 2 or 4 uint4 per thread per tile (0 = 2); other fields ignored; cfg may be
+ * NULL.  MONT_EINVAL_ARG for another shape. */
+struct mont_launch;
+mont_status_t mont_run_ex(const mont_run_job_t *jobs, int njobs, const struct mont_launch *cfg,
+                          cudaStream_t stream);
 
 /* Bytes of HBM traffic the run moves by plan (after fusion): the algorithmic bytes of the
  * launch (reads + writes of every job, a fused pair counted once), for the roofline. */

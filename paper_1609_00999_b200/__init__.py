@@ -133,6 +133,7 @@ class RunJob(C.Structure):
 
 
 SIGNATURES["mont_run"] = (C.c_int, [C.POINTER(RunJob), C.c_int, _P])
+SIGNATURES["mont_run_ex"] = (C.c_int, [C.POINTER(RunJob), C.c_int, _LAUNCH, _P])
 SIGNATURES["mont_run_bytes"] = (C.c_int, [C.POINTER(RunJob), C.c_int, C.POINTER(C.c_ulonglong)])
 SIGNATURES["mont_host_run_bytes"] = (C.c_int, [C.POINTER(HostJob), C.c_int, C.POINTER(C.c_ulonglong),
                                                C.POINTER(C.c_ulonglong)])
@@ -528,11 +529,14 @@ def run_job(op: str, ctx: Ctx, out, in0, in1=None, acc=None) -> RunJob:
     return j
 
 
-def run(jobs, stream=None):
+def run(jobs, stream=None, cfg: Launch | None = None):
     """Run the jobs as one launch (mont_run): independent HBM-bound operations back to back in one
     flat grid; a from_mont reading an earlier to_mont's output is fused into it."""
     arr = (RunJob * len(jobs))(*jobs)
-    _check(lib().mont_run(arr, len(jobs), _stream_handle(stream)), "mont_run")
+    if cfg is None:
+        _check(lib().mont_run(arr, len(jobs), _stream_handle(stream)), "mont_run")
+    else:
+        _check(lib().mont_run_ex(arr, len(jobs), C.byref(cfg), _stream_handle(stream)), "mont_run_ex")
 
 
 def run_bytes(jobs) -> int:

@@ -13,14 +13,15 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "../../include/mont_ext.h"
 #include "../../include/mont_run.h"
 #include "abi_util.h"
 
 namespace mont {
 
-constexpr int kRunU = 2;            // uint4 per thread per tile
-constexpr int kRunThreads = 256;
-constexpr size_t kRunTile = (size_t)kRunU * kRunThreads;  // uint4 per tile
+// tile = THREADS x U uint4 per operand; the default (512 x 2, as mont_mul_vec_checksum's) and
+// the alternatives are measured in profiles/r02_probe_run.jsonl
+constexpr int kRunThreadsMax = 512;
 
 struct RunJob {
     uint32_t op, fused;      // fused: TO job whose from_mont consumer writes out2
@@ -44,7 +45,9 @@ __device__ __forceinline__ unsigned long long run_warp_sum(unsigned long long v)
     return v;
 }
 
+template <int kRunThreads, int kRunU>
 __global__ void __launch_bounds__(kRunThreads) k_run(const __grid_constant__ RunParams P) {
+    constexpr size_t kRunTile = (size_t)kRunU * kRunThreads;  // uint4 per tile
     const size_t t = blockIdx.x;
     int j = 0;
 #pragma unroll 1
@@ -79,7 +82,7 @@ __global__ void __launch_bounds__(kRunThreads) k_run(const __grid_constant__ Run
             }
         }
         if (J.acc) {  // block-uniform branch: the CTA's sum, one 64-bit atomic
-            __shared__ unsigned long long part[kRunThreads / 32];
+            __shared__ unsigned long long part[kRunThreadsMax / 32];
             s = run_warp_sum(s);
             const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
             if (lane == 0) part[wid] = s;
@@ -142,7 +145,7 @@ static bool overlap(const Range &a, const Range &b) { return a.lo < b.hi && b.lo
 
 // validates the jobs and builds the plan; returns the total tile count through *tiles
 static mont_status_t run_plan(const mont_run_job_t *jobs, int njobs, RunParams &P, size_t *tiles,
-                              unsigned long long *bytes) {
+                              unsigned long long *bytes, size_t kRunTile) {
     if (njobs < 0 || njobs > MONT_RUN_MAX_JOBS || (njobs > 0 && !jobs)) return MONT_EINVAL_ARG;
     int fused_into[MONT_RUN_MAX_JOBS];
     for (int i = 0; i < njobs; ++i) fused_into[i] = -1;
@@ -235,20 +238,37 @@ static mont_status_t run_plan(const mont_run_job_t *jobs, int njobs, RunParams &
 
 using namespace mont;
 
-extern "C" mont_status_t mont_run(const mont_run_job_t *jobs, int njobs, cudaStream_t stream) {
+extern "C" mont_status_t mont_run_ex(const mont_run_job_t *jobs, int njobs, const mont_launch_t *cfg,
+                                     cudaStream_t stream) {
+    const int threads = cfg && cfg->threads ? cfg->threads : 512;
+    const int unroll = cfg && cfg->unroll ? cfg->unroll : 2;
+    if (!((threads == 256 || threads == 512) && (unroll == 1 || unroll == 2 || unroll == 4))) return MONT_EINVAL_ARG;
     RunParams P{};
     size_t tiles = 0;
-    const mont_status_t st = run_plan(jobs, njobs, P, &tiles, nullptr);
+    const mont_status_t st = run_plan(jobs, njobs, P, &tiles, nullptr, (size_t)threads * unroll);
     if (st != MONT_OK) return st;
     if (tiles == 0) return MONT_OK;
     if (tiles > 0x7fffffffu) return MONT_EUNSUPPORTED;
-    k_run<<<(unsigned)tiles, kRunThreads, 0, stream>>>(P);
+    const unsigned g = (unsigned)tiles;
+    if (threads == 512) {
+        if (unroll == 1) k_run<512, 1><<<g, 512, 0, stream>>>(P);
+        else if (unroll == 2) k_run<512, 2><<<g, 512, 0, stream>>>(P);
+        else k_run<512, 4><<<g, 512, 0, stream>>>(P);
+    } else {
+        if (unroll == 1) k_run<256, 1><<<g, 256, 0, stream>>>(P);
+        else if (unroll == 2) k_run<256, 2><<<g, 256, 0, stream>>>(P);
+        else k_run<256, 4><<<g, 256, 0, stream>>>(P);
+    }
     return launch_status();
+}
+
+extern "C" mont_status_t mont_run(const mont_run_job_t *jobs, int njobs, cudaStream_t stream) {
+    return mont_run_ex(jobs, njobs, nullptr, stream);
 }
 
 extern "C" mont_status_t mont_run_bytes(const mont_run_job_t *jobs, int njobs, unsigned long long *bytes) {
     if (!bytes) return MONT_EINVAL_ARG;
     RunParams P{};
     size_t tiles = 0;
-    return run_plan(jobs, njobs, P, &tiles, bytes);
+    return run_plan(jobs, njobs, P, &tiles, bytes, 1024);
 }

@@ -289,7 +289,11 @@ if args.what == "run":
     for name, fn in (("individual, library defaults", lambda: serial({})),
                      ("individual, lane shapes 256x2 / 256x4",
                       lambda: serial({"mul": L(threads=256, unroll=2), "conv": L(threads=256, unroll=4)})),
-                     ("one mont_run (to/from fused)", run_l[1])):
+                     ("one mont_run (to/from fused)", run_l[1]),
+                     ("mont_run 256 x 2", lambda: m.run(wl.run_jobs, cfg=L(threads=256, unroll=2))),
+                     ("mont_run 256 x 4", lambda: m.run(wl.run_jobs, cfg=L(threads=256, unroll=4))),
+                     ("mont_run 512 x 1", lambda: m.run(wl.run_jobs, cfg=L(threads=512, unroll=1))),
+                     ("mont_run 512 x 4", lambda: m.run(wl.run_jobs, cfg=L(threads=512, unroll=4)))):
         med, best = timeit(fn, reps=20)
         out(what="run", how=name, us=med * 1e6, us_best=best * 1e6, bytes_individual=nbytes, bytes_run=wl.run_bytes,
             gbs_algorithmic=(wl.run_bytes if "run" in name else nbytes) / med / 1e9)

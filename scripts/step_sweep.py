@@ -27,7 +27,8 @@ def main():
     assert all(bench.verify(wl).values())
     L = m.Launch
     # (variant, ctas_per_sm, reserved smem bytes): ctas 0 = flat grid
-    pows = [(10, 1, 0), (11, 1, 0), (10, 2, 0)]
+    pows = [(int(a), int(b), int(c)) for a, b, c in
+            (v.split(":") for v in os.environ.get("SWEEP_POWS", "10:1:0,11:1:0,10:2:0").split(","))]
     prios = ["imad"]
     hstreams = [int(v) for v in os.environ.get("SWEEP_HBM_STREAMS", "1").split(",")]
     modes = os.environ.get("SWEEP_HBM_MODES", "streams").split(",")
