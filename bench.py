@@ -69,11 +69,15 @@ LANE_ORDER = tuple(os.environ.get("MONT_LANE_ORDER", "imad,hbm").split(","))
 # it): the persistent pow grid is placed first, one CTA per SM, and the HBM-bound launches fill
 # the rest of every SM (scripts/step_sweep.py, profiles/r02_step_sweep*.jsonl)
 LANE_PRIO = os.environ.get("MONT_LANE_PRIO", "imad")
-# the HBM lane of the step: "run" = one mont_run launch over all HBM jobs, "streams" = the
-# individual launches spread over HBM_STREAMS streams
-HBM_MODE = os.environ.get("MONT_HBM_MODE", "run")
+# the HBM lane of the step: "streams" = the individual launches on HBM_STREAMS streams (default:
+# one), "run" = one mont_run launch over all HBM jobs (fastest alone, 546 vs 598 us, but slower
+# next to the pow lane: 0.64-0.65 vs 0.63 ms, profiles/r02_step_sweep.jsonl)
+HBM_MODE = os.environ.get("MONT_HBM_MODE", "streams")
+# tile shape of that mont_run launch inside the step (threads, uint4 per thread): 256-thread tiles
+# leave the co-running pow grid the room 512-thread ones take (profiles/r02_step_sweep.jsonl)
+RUN_SHAPE = tuple(int(v) for v in os.environ.get("MONT_RUN_SHAPE", "256,2").split(","))
 # streams the HBM-bound launches are spread over inside the step (independent launches only)
-HBM_STREAMS = int(os.environ.get("MONT_HBM_STREAMS", "2"))
+HBM_STREAMS = int(os.environ.get("MONT_HBM_STREAMS", "1"))
 
 
 def parse():
@@ -357,7 +361,8 @@ class Workload:
             self.run_jobs = jobs
             self.run_bytes = m.run_bytes(jobs)
             self._run_launch = ("mont_run[hbm lane: " + ", ".join(x[0] for x in hbm) + "]",
-                                lambda: m.run(self.run_jobs), self.run_bytes, sum(x[3] for x in hbm), "hbm")
+                                lambda: m.run(self.run_jobs, cfg=m.Launch(threads=RUN_SHAPE[0], unroll=RUN_SHAPE[1])),
+                                self.run_bytes, sum(x[3] for x in hbm), "hbm")
         return [self._run_launch] + [x for x in self.launches if x[4] != "hbm"]
 
     def step(self):
@@ -381,7 +386,7 @@ class Workload:
         if not hasattr(self, "_lanes"):
             self._lanes = {ln: torch.cuda.Stream(priority=-1 if ln == LANE_PRIO else 0) for ln in ("hbm", "imad")}
         nh = max(1, HBM_STREAMS)
-        if len(getattr(self, "_hbm_extra", [])) != nh - 1:
+        if not hasattr(self, "_hbm_extra") or len(self._hbm_extra) != nh - 1:
             self._hbm_extra = [torch.cuda.Stream(priority=-1 if LANE_PRIO == "hbm" else 0) for _ in range(nh - 1)]
         hbm_streams = [self._lanes["hbm"]] + self._hbm_extra
         # HBM launches that do not depend on each other go to different streams (graph branches), so

@@ -32,6 +32,7 @@ def main():
     prios = ["imad"]
     hstreams = [int(v) for v in os.environ.get("SWEEP_HBM_STREAMS", "1").split(",")]
     modes = os.environ.get("SWEEP_HBM_MODES", "streams").split(",")
+    shapes = [tuple(int(x) for x in v.split("x")) for v in os.environ.get("SWEEP_RUN_SHAPES", "256x2").split(",")]
     if os.environ.get("SWEEP_WIDE"):
         pows = [(11, 0, 0), (11, 0, 200 * 1024), (11, 0, 110 * 1024), (11, 0, 72 * 1024), (11, 0, 54 * 1024),
                 (11, 1, 0), (11, 2, 0), (10, 2, 0)]
@@ -53,12 +54,17 @@ def main():
     }
     only = os.environ.get("SWEEP_HBM")
     rebuilds = int(os.environ.get("SWEEP_REBUILDS", "2"))
-    for (pv, pc, sm), (hname, hcfg), prio, hs, mode in itertools.product(pows, hbms.items(), prios, hstreams, modes):
+    for (pv, pc, sm), (hname, hcfg), prio, hs, mode, shape in itertools.product(pows, hbms.items(), prios, hstreams,
+                                                                                   modes, shapes):
         if only and hname not in only.split(","):
             continue
         if mode == "run" and (hs != 1 or hname != "default"):
             continue   # the run has its own launch shape and one launch
-        bench.HBM_STREAMS, bench.HBM_MODE = hs, mode
+        if mode != "run" and shape != shapes[0]:
+            continue
+        bench.HBM_STREAMS, bench.HBM_MODE, bench.RUN_SHAPE = hs, mode, shape
+        if hasattr(wl, "_run_launch"):
+            del wl._run_launch
         wl.pow_cfg_lane = L(ctas_per_sm=pc, variant=pv, chunk=sm)
         wl.hbm_cfg_lane = {k: v for k, v in hcfg.items() if v is not None}
         # lane streams: torch priority -1 = high, 0 = low (graph kernel nodes inherit it)
@@ -77,6 +83,7 @@ def main():
             ts = [bench.time_steps_graph(wl, g, 20) / 20 for _ in range(3)]
             ok = all(bench.verify(wl, run=False).values())
             print(json.dumps({"pow": [pv, pc, sm], "hbm": hname, "prio": prio, "hbm_streams": hs, "mode": mode,
+                              "run_shape": list(shape) if mode == "run" else None,
                               "rebuild": rb,
                               "ms_per_step": round(statistics.median(ts), 4), "ms_best": round(min(ts), 4),
                               "outputs_ok": ok}), flush=True)
