@@ -69,13 +69,14 @@ LANE_ORDER = tuple(os.environ.get("MONT_LANE_ORDER", "imad,hbm").split(","))
 # it): the persistent pow grid is placed first, one CTA per SM, and the HBM-bound launches fill
 # the rest of every SM (scripts/step_sweep.py, profiles/r02_step_sweep*.jsonl)
 LANE_PRIO = os.environ.get("MONT_LANE_PRIO", "imad")
-# the HBM lane of the step: "streams" = the individual launches on HBM_STREAMS streams (default:
-# one), "run" = one mont_run launch over all HBM jobs (fastest alone, 546 vs 598 us, but slower
-# next to the pow lane: 0.64-0.65 vs 0.63 ms, profiles/r02_step_sweep.jsonl)
-HBM_MODE = os.environ.get("MONT_HBM_MODE", "streams")
+# the HBM lane of the step: "pair" (default) = the individual launches on HBM_STREAMS streams except
+# to_mont -> from_mont, which run as ONE fused mont_run launch (0.599-0.601 ms per step);
+# "streams" = all individual (0.630); "run" = one mont_run launch over all HBM jobs (fastest alone,
+# 546 vs 598 us, but slower next to the pow lane: 0.64-0.65 ms) -- profiles/r02_step_sweep.jsonl
+HBM_MODE = os.environ.get("MONT_HBM_MODE", "pair")
 # tile shape of that mont_run launch inside the step (threads, uint4 per thread): 256-thread tiles
 # leave the co-running pow grid the room 512-thread ones take (profiles/r02_step_sweep.jsonl)
-RUN_SHAPE = tuple(int(v) for v in os.environ.get("MONT_RUN_SHAPE", "256,2").split(","))
+RUN_SHAPE = tuple(int(v) for v in os.environ.get("MONT_RUN_SHAPE", "512,2").split(","))
 # streams the HBM-bound launches are spread over inside the step (independent launches only)
 HBM_STREAMS = int(os.environ.get("MONT_HBM_STREAMS", "1"))
 
@@ -339,6 +340,23 @@ class Workload:
         mont_run.h: one flat grid over all their tiles, to_mont -> from_mont fused) when
         HBM_MODE == "run", else individually; the IMAD-bound ones as they are."""
         hbm = [x for x in self.launches if x[4] == "hbm"]
+        if HBM_MODE == "pair" and hasattr(self, "abar"):
+            # only the to_mont -> from_mont pair as one fused mont_run launch, the rest individual
+            if not hasattr(self, "_pair_launch"):
+                m = self.m
+                self.pair_jobs = [m.run_job("to_mont", self.ctx[P0], self.abar, self.c2[P0][0]),
+                                  m.run_job("from_mont", self.ctx[P0], self.back, self.abar)]
+                self._pair_launch = ("mont_run[to_mont -> from_mont fused]",
+                                     lambda: m.run(self.pair_jobs, cfg=m.Launch(threads=RUN_SHAPE[0],
+                                                                                unroll=RUN_SHAPE[1])),
+                                     m.run_bytes(self.pair_jobs), 2 * N_C2, "hbm")
+            out = []
+            for x in self.launches:
+                if x[0] == "to_mont":
+                    out.append(self._pair_launch)
+                elif x[0] != "from_mont":
+                    out.append(x)
+            return out
         if HBM_MODE != "run" or len(hbm) < 2:
             return self.launches
         if not hasattr(self, "_run_launch"):
@@ -676,21 +694,28 @@ def capture_step_graph(wl: Workload):
 
 
 def imad_launch_clock_mhz(wl: Workload, K: int):
-    """The SM clock the IMAD-bound launch (pow) runs at in the serial step: K more serial steps, each
-    with mb_sm_clock (one warp timing ~20 us of clock64 against %globaltimer) right after the pow
-    launch on the same stream -- the power-managed clock moves on a millisecond scale, so this is
-    the clock pow just ran at.  Median MHz over the K steps (not a timed pass)."""
-    import ctypes as _C  # noqa: F401
+    """The SM clock the IMAD-bound launch (pow) runs at in the serial step: K more serial steps, in
+    each of which mb_sm_clock (one warp timing clock64 against %globaltimer) runs on a high-priority
+    side stream DURING the pow launch -- it is released by an event recorded just before pow and
+    spins for ~2/3 of pow's duration, taking the first slot a finishing pow CTA frees.  Median MHz
+    over the K steps (not a timed pass)."""
     torch, m = wl.torch, wl.m
     s = torch.cuda.current_stream()
+    side = torch.cuda.Stream(priority=-1)
     buf = torch.zeros(K, 2, dtype=torch.int64, device=wl.dev)
     got = False
     for k in range(K):
         for name, fn, _, _, bound in wl.launches:
-            fn()
             if bound == "imad":
-                m.lib().mb_sm_clock(buf[k].data_ptr(), 40000, s.cuda_stream)
+                ev = torch.cuda.Event()
+                ev.record(s)
+                side.wait_event(ev)
+                fn()
+                m.lib().mb_sm_clock(buf[k].data_ptr(), 300000, side.cuda_stream)   # ~160 us at 1.9 GHz
                 got = True
+            else:
+                fn()
+        s.wait_stream(side)
     torch.cuda.synchronize()
     if not got:
         return None
@@ -1211,8 +1236,8 @@ def main():
                 r.update({"bound": "alu", "achieved": round(ach, 4), "peak": round(peak, 4), "unit": "Tmulmod/s",
                           "frac": round(ach / peak, 4),
                           "peak_basis": f"{sms} SMs x 64 FMAHeavy lanes/clk / 5 issue slots per REDC x "
-                                        f"{clk/1e6:.0f} MHz" + (" (SM clock measured right after the launch, "
-                                                                "mb_sm_clock)" if imad_clk_mhz else
+                                        f"{clk/1e6:.0f} MHz" + (" (SM clock measured during the launch by a "
+                                                                "co-running one-warp mb_sm_clock)" if imad_clk_mhz else
                                                                 " (median nvidia-smi clock of the timed region)"),
                           # SURVEY §8(d)'s other denominator: 4 multiplies per REDC at the full IMAD rate
                           # (IMAD.WIDE measured half rate on B200, so this one is not reachable)
@@ -1300,7 +1325,10 @@ def main():
         "schedule": ("each step alone between CUDA events after an L2 flush" if wl.kind == "c1" else
                      "serial, one stream" if args.serial else
                      ("two lanes: the HBM-bound operations as ONE mont_run launch (one flat grid over all their "
-                      "tiles, 256 threads x 2 uint4, to_mont -> from_mont fused)" if HBM_MODE == "run" else
+                      "tiles, to_mont -> from_mont fused)" if HBM_MODE == "run" else
+                      "two lanes: the HBM-bound launches in order on one stream (mul_vec+checksum 256 threads x 2 "
+                      "uint4 x 3, to_mont -> from_mont as one fused mont_run launch, twiddle default)"
+                      if HBM_MODE == "pair" else
                       f"two lanes: the HBM-bound launches on {HBM_STREAMS} stream(s) (mul_vec+checksum 256 threads x 2 "
                       "uint4, to/from_mont 256 x 4, twiddle default)") +
                      ", the IMAD-bound pow on another, higher-priority "

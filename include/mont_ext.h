@@ -62,7 +62,9 @@ extern "C" {
  *                                   multiplies; 14 = 13 + 2 FP64 lanes;
  *                                   15 / 16 = 11 / 13 with P at run time;
  *                                   (11-16 need 16-byte co-aligned operands,
- *                                   else they run 17); 17 = 2-bit fixed
+ *                                   else they run 17; they take threads =
+ *                                   64, 128 (their default) or 256, the
+ *                                   others 256); 17 = 2-bit fixed
  *                                   window, 4 lanes per thread, table in
  *                                   registers (any alignment).
  *                                   ctas_per_sm = 0 selects a flat grid.

@@ -420,7 +420,7 @@ static const Launch kPowDefault{256, 0, 1, 0, 0};
 using namespace mont;
 
 mont_status_t mont_pow2_launch(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *base, const uint32_t *exp,
-                               size_t n, int variant, int ctas_per_sm, int sms, size_t reserve_smem,
+                               size_t n, int variant, int ctas_per_sm, int sms, size_t reserve_smem, int threads,
                                cudaStream_t stream);  // k_pow2.cu
 
 extern "C" mont_status_t mont_pow_vec_ex(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *base,
@@ -430,7 +430,13 @@ extern "C" mont_status_t mont_pow_vec_ex(const mont_ctx_t *ctx, uint32_t *out, c
     if (n == 0) return MONT_OK;
     if (!out || !base || !exp || ((uintptr_t)out | (uintptr_t)base | (uintptr_t)exp) & 3u) return MONT_EINVAL_ARG;
     Launch L = resolve(cfg, kPowDefault);
-    if (L.threads != 256 || L.variant < 0 || L.variant > 17 || L.ctas_per_sm < 0 || L.chunk < 0 ||
+    const bool v2 = L.variant == 0 || (L.variant >= 11 && L.variant <= 16);  // k_pow2: 64, 128 or 256 threads
+    // k_pow2's default CTA is 128 threads: twice the CTAs of 256 for the same warps per SM, so the
+    // last wave is half as long (235.9 vs 240.0 us for configs[3], profiles/r02_probe_pow_variants.jsonl)
+    if (v2 && (!cfg || cfg->threads == 0)) L.threads = 128;
+    if (!(L.threads == 256 || (v2 && (L.threads == 128 || L.threads == 64))) || L.variant < 0 || L.variant > 17 ||
+        L.ctas_per_sm < 0 ||
+        L.chunk < 0 ||
         L.chunk > 227 * 1024)
         return MONT_EINVAL_ARG;
     const int sms = sm_count();
@@ -442,7 +448,9 @@ extern "C" mont_status_t mont_pow_vec_ex(const mont_ctx_t *ctx, uint32_t *out, c
     // else the 4-lane 2-bit window (variant 17, round 1's default), which takes any alignment
     if (L.variant == 0) L.variant = co16 ? 11 : 17;
     if (L.variant >= 11 && L.variant <= 16 && co16)
-        return mont_pow2_launch(ctx, out, base, exp, n, L.variant, L.ctas_per_sm, sms, (size_t)L.chunk, stream);
+        return mont_pow2_launch(ctx, out, base, exp, n, L.variant, L.ctas_per_sm, sms, (size_t)L.chunk, L.threads,
+                                stream);
+    L.threads = 256;  // the other ladders run 256-thread CTAs
     if (L.variant >= 11) L.variant = 0;  // 17, or misaligned operands: the 4-lane kernel
     if (L.variant == 10 && co16) {
         const uint32_t head = head_elems((uintptr_t)base, n);

@@ -186,24 +186,24 @@ __global__ void __launch_bounds__(256) k_pow2(Pow2Params q, uint32_t *out, const
 
 template <uint32_t PC, int NF, bool SH, bool BIGP>
 static void launch_pow2(const Pow2Params &q, uint32_t *out, const uint32_t *base, const uint32_t *exp, uint32_t head,
-                        size_t n4, uint32_t tail, unsigned grid, size_t smem, cudaStream_t s) {
+                        size_t n4, uint32_t tail, unsigned grid, size_t smem, int threads, cudaStream_t s) {
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_pow2<PC, NF, SH, BIGP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_pow2<PC, NF, SH, BIGP><<<grid, 256, smem, s>>>(q, out, base, exp, head, n4, tail);
+    k_pow2<PC, NF, SH, BIGP><<<grid, threads, smem, s>>>(q, out, base, exp, head, n4, tail);
 }
 
 template <int NF, bool SH, bool BIGP>
 static void dispatch_p(uint32_t p, bool specialise, const Pow2Params &q, uint32_t *out, const uint32_t *base,
                        const uint32_t *exp, uint32_t head, size_t n4, uint32_t tail, unsigned grid, size_t smem,
-                       cudaStream_t s) {
+                       int threads, cudaStream_t s) {
     if (specialise && p == 469762049u && !BIGP)
-        launch_pow2<469762049u, NF, SH, false>(q, out, base, exp, head, n4, tail, grid, smem, s);
+        launch_pow2<469762049u, NF, SH, false>(q, out, base, exp, head, n4, tail, grid, smem, threads, s);
     else if (specialise && p == 998244353u && BIGP)
-        launch_pow2<998244353u, NF, SH, true>(q, out, base, exp, head, n4, tail, grid, smem, s);
+        launch_pow2<998244353u, NF, SH, true>(q, out, base, exp, head, n4, tail, grid, smem, threads, s);
     else if (specialise && p == 2013265921u && BIGP)
-        launch_pow2<2013265921u, NF, SH, true>(q, out, base, exp, head, n4, tail, grid, smem, s);
+        launch_pow2<2013265921u, NF, SH, true>(q, out, base, exp, head, n4, tail, grid, smem, threads, s);
     else
-        launch_pow2<0u, NF, SH, BIGP>(q, out, base, exp, head, n4, tail, grid, smem, s);
+        launch_pow2<0u, NF, SH, BIGP>(q, out, base, exp, head, n4, tail, grid, smem, threads, s);
 }
 
 }  // namespace mont
@@ -220,14 +220,14 @@ using namespace mont;
 // balances it dynamically (bench.py's two-lane step)
 mont_status_t mont_pow2_launch(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *base, const uint32_t *exp,
                                size_t n, int variant, int ctas_per_sm, int sms, size_t reserve_smem,
-                               cudaStream_t stream) {
+                               int threads, cudaStream_t stream) {
     const uint32_t p = ctx->p;
     const Pow2Params q{(int32_t)p, (int32_t)(0u - ctx->pneg), ctx->r1, ctx->r2, ctx->pneg, 0u, (double)p,
                        1.0 / (double)p};
     const uint32_t head = head_elems((uintptr_t)base, n);
     const size_t n4 = (n - head) / 4;
     const uint32_t tail = (uint32_t)((n - head) % 4);
-    const size_t need = (n4 / 2 + 255) / 256;
+    const size_t need = (n4 / 2 + threads - 1) / threads;
     size_t grid = ctas_per_sm > 0 ? (size_t)sms * ctas_per_sm : need;
     if (grid > need) grid = need;
     if (grid == 0) grid = 1;
@@ -238,8 +238,8 @@ mont_status_t mont_pow2_launch(const mont_ctx_t *ctx, uint32_t *out, const uint3
     const unsigned g = (unsigned)grid;
 #define P2(NF, SH)                                                                                \
     do {                                                                                          \
-        if (bigp) dispatch_p<NF, SH, true>(p, spec, q, out, base, exp, head, n4, tail, g, reserve_smem, stream);  \
-        else dispatch_p<NF, SH, false>(p, spec, q, out, base, exp, head, n4, tail, g, reserve_smem, stream);      \
+        if (bigp) dispatch_p<NF, SH, true>(p, spec, q, out, base, exp, head, n4, tail, g, reserve_smem, threads, stream); \
+        else dispatch_p<NF, SH, false>(p, spec, q, out, base, exp, head, n4, tail, g, reserve_smem, threads, stream);     \
     } while (0)
     switch (v) {
         case 11: P2(0, false); break;

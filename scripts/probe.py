@@ -216,6 +216,7 @@ if args.what in ("all", "pow"):
     useful = int(31 * n + np.unpackbits(pc.view(np.uint8)).sum())
     variants = [int(v) for v in os.environ.get("PROBE_POW_VARIANTS", "0,10,2,5,6,7,8,9").split(",")]
     ctas_list = [int(v) for v in os.environ.get("PROBE_POW_CTAS", "0").split(",")]
+    threads_list = [int(v) for v in os.environ.get("PROBE_POW_THREADS", "256").split(",")]
     primes = [int(v) for v in os.environ.get("PROBE_POW_PRIMES", str(P)).split(",")]
     for Pp in primes:
         ctx = m.ctx_init(Pp)
@@ -224,11 +225,16 @@ if args.what in ("all", "pow"):
         ref = m.pow_vec(ctx, base, e, cfg=m.Launch(variant=0))
         for variant in variants:
             for ctas in ctas_list:
-                cfg = m.Launch(variant=variant, ctas_per_sm=ctas)
-                med, best = timeit(lambda: m.pow_vec(ctx, base, e, out=o, cfg=cfg), reps=10)
-                same = bool((o.view(torch.int32) == ref.view(torch.int32)).all())
-                out(what="pow", P=Pp, variant=variant, ctas=ctas, us=med * 1e6, us_best=best * 1e6,
-                    useful_mulmods=useful, tmulmod=useful / med / 1e12, equal_to_variant0=same)
+                for thr in threads_list:
+                    cfg = m.Launch(variant=variant, ctas_per_sm=ctas, threads=thr)
+                    try:
+                        med, best = timeit(lambda: m.pow_vec(ctx, base, e, out=o, cfg=cfg), reps=10)
+                    except m.MontError as ex:
+                        out(what="pow", P=Pp, variant=variant, ctas=ctas, threads=thr, err=str(ex))
+                        continue
+                    same = bool((o.view(torch.int32) == ref.view(torch.int32)).all())
+                    out(what="pow", P=Pp, variant=variant, ctas=ctas, threads=thr, us=med * 1e6, us_best=best * 1e6,
+                        useful_mulmods=useful, tmulmod=useful / med / 1e12, equal_to_variant0=same)
 
 if args.what == "powctx":
     # pow (default launch) timed: back to back; after a 512 MiB L2 flush; after the twiddle kernel;

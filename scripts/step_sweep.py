@@ -60,11 +60,12 @@ def main():
             continue
         if mode == "run" and (hs != 1 or hname != "default"):
             continue   # the run has its own launch shape and one launch
-        if mode != "run" and shape != shapes[0]:
+        if mode == "streams" and shape != shapes[0]:
             continue
         bench.HBM_STREAMS, bench.HBM_MODE, bench.RUN_SHAPE = hs, mode, shape
-        if hasattr(wl, "_run_launch"):
-            del wl._run_launch
+        for attr in ("_run_launch", "_pair_launch"):
+            if hasattr(wl, attr):
+                delattr(wl, attr)
         wl.pow_cfg_lane = L(ctas_per_sm=pc, variant=pv, chunk=sm)
         wl.hbm_cfg_lane = {k: v for k, v in hcfg.items() if v is not None}
         # lane streams: torch priority -1 = high, 0 = low (graph kernel nodes inherit it)
@@ -83,7 +84,7 @@ def main():
             ts = [bench.time_steps_graph(wl, g, 20) / 20 for _ in range(3)]
             ok = all(bench.verify(wl, run=False).values())
             print(json.dumps({"pow": [pv, pc, sm], "hbm": hname, "prio": prio, "hbm_streams": hs, "mode": mode,
-                              "run_shape": list(shape) if mode == "run" else None,
+                              "run_shape": list(shape) if mode != "streams" else None,
                               "rebuild": rb,
                               "ms_per_step": round(statistics.median(ts), 4), "ms_best": round(min(ts), 4),
                               "outputs_ok": ok}), flush=True)

@@ -466,3 +466,22 @@ def test_pow_variant10_grids(m, ctas, n, variant):
     base, e = synth.c4_inputs(P, 0, n)
     out = m.pow_vec(m.ctx_init(P), dev(base), dev(e), cfg=m.Launch(variant=variant, ctas_per_sm=ctas))
     assert np.array_equal(host(out), oracle.power(P, base, e))
+
+
+@pytest.mark.parametrize("threads", [64, 128, 256])
+@pytest.mark.parametrize("variant", [0, 11, 12, 13, 16])
+@pytest.mark.parametrize("n", [1, 7, 8, 9, 4100, 1 << 20])
+def test_pow2_cta_sizes(m, threads, variant, n):
+    """The k_pow2 ladders (default variant 11 at 128 threads) at every CTA size they accept."""
+    P = 2013265921
+    base, e = synth.c4_inputs(P, 3, n)
+    out = m.pow_vec(m.ctx_init(P), dev(base), dev(e), cfg=m.Launch(variant=variant, threads=threads))
+    assert np.array_equal(host(out), oracle.power(P, base, e))
+
+
+def test_pow_rejects_thread_counts(m):
+    P = 469762049
+    b = dev(np.ones(64, np.uint32))
+    for cfg in (m.Launch(variant=17, threads=128), m.Launch(variant=11, threads=96), m.Launch(variant=1, threads=64)):
+        with pytest.raises(m.MontError):
+            m.pow_vec(m.ctx_init(P), b, b, cfg=cfg)
