@@ -27,8 +27,8 @@ def main():
     assert all(bench.verify(wl).values())
     L = m.Launch
     # (variant, ctas_per_sm, reserved smem bytes): ctas 0 = flat grid
-    pows = [(int(a), int(b), int(c)) for a, b, c in
-            (v.split(":") for v in os.environ.get("SWEEP_POWS", "10:1:0,11:1:0,10:2:0").split(","))]
+    pows = [tuple(int(x) for x in (v.split(":") + ["256"])[:4]) for v in
+            os.environ.get("SWEEP_POWS", "10:1:0,11:1:0,10:2:0").split(",")]   # variant:ctas:smem[:threads]
     prios = ["imad"]
     hstreams = [int(v) for v in os.environ.get("SWEEP_HBM_STREAMS", "1").split(",")]
     modes = os.environ.get("SWEEP_HBM_MODES", "streams").split(",")
@@ -54,7 +54,7 @@ def main():
     }
     only = os.environ.get("SWEEP_HBM")
     rebuilds = int(os.environ.get("SWEEP_REBUILDS", "2"))
-    for (pv, pc, sm), (hname, hcfg), prio, hs, mode, shape in itertools.product(pows, hbms.items(), prios, hstreams,
+    for (pv, pc, sm, pt), (hname, hcfg), prio, hs, mode, shape in itertools.product(pows, hbms.items(), prios, hstreams,
                                                                                    modes, shapes):
         if only and hname not in only.split(","):
             continue
@@ -66,7 +66,7 @@ def main():
         for attr in ("_run_launch", "_pair_launch"):
             if hasattr(wl, attr):
                 delattr(wl, attr)
-        wl.pow_cfg_lane = L(ctas_per_sm=pc, variant=pv, chunk=sm)
+        wl.pow_cfg_lane = L(ctas_per_sm=pc, variant=pv, chunk=sm, threads=pt)
         wl.hbm_cfg_lane = {k: v for k, v in hcfg.items() if v is not None}
         # lane streams: torch priority -1 = high, 0 = low (graph kernel nodes inherit it)
         wl._lanes = {"hbm": torch.cuda.Stream(priority=-1 if prio == "hbm" else 0),
@@ -76,14 +76,14 @@ def main():
             try:
                 g = bench.capture_step_graph(wl)
             except Exception as ex:  # noqa: BLE001
-                print(json.dumps({"pow": [pv, pc, sm], "hbm": hname, "error": str(ex)}), flush=True)
+                print(json.dumps({"pow": [pv, pc, sm, pt], "hbm": hname, "error": str(ex)}), flush=True)
                 break
             for _ in range(3):
                 g.replay()
             torch.cuda.synchronize()
             ts = [bench.time_steps_graph(wl, g, 20) / 20 for _ in range(3)]
             ok = all(bench.verify(wl, run=False).values())
-            print(json.dumps({"pow": [pv, pc, sm], "hbm": hname, "prio": prio, "hbm_streams": hs, "mode": mode,
+            print(json.dumps({"pow": [pv, pc, sm, pt], "hbm": hname, "prio": prio, "hbm_streams": hs, "mode": mode,
                               "run_shape": list(shape) if mode != "streams" else None,
                               "rebuild": rb,
                               "ms_per_step": round(statistics.median(ts), 4), "ms_best": round(min(ts), 4),

@@ -485,3 +485,46 @@ def test_pow_rejects_thread_counts(m):
     for cfg in (m.Launch(variant=17, threads=128), m.Launch(variant=11, threads=96), m.Launch(variant=1, threads=64)):
         with pytest.raises(m.MontError):
             m.pow_vec(m.ctx_init(P), b, b, cfg=cfg)
+
+
+@pytest.mark.parametrize("n", [1, 3, 4, 5, 7, 8, 9, 33, 4099, 65537])
+@pytest.mark.parametrize("variant,threads", [(11, 64), (11, 128), (11, 256), (12, 128), (13, 128), (14, 256),
+                                             (9, 256), (10, 256)])
+def test_guards_pow_ladders(m, n, variant, threads):
+    """Round-2 ladders (and Alg. 3 with the 33-bit t for P0) write exactly their n words: canary
+    words on both sides of out (co-aligned operands, the only layout these variants take)."""
+    P = 2013265921
+    base, e = synth.c4_inputs(P, 9, n)
+    buf, o = guarded(n, 0)
+    m.pow_vec(m.ctx_init(P), dev(base), dev(e), out=o, cfg=m.Launch(variant=variant, threads=threads))
+    assert np.array_equal(host(o), oracle.power(P, base, e))
+    assert canaries_intact(buf, n, 0)
+
+
+@pytest.mark.parametrize("n", [4, 8, 2044, 4100, 65540])
+def test_guards_run(m, n):
+    """mont_run writes exactly each job's n words (incl. the fused pair's two outputs)."""
+    P = 998244353
+    ctx = m.ctx_init(P)
+    a, b = synth.c2_inputs(P, 0, n)
+    bufs = [guarded(n, 0) for _ in range(4)]
+    (b0, c), (b1, t), (b2, f), (b3, g) = bufs
+    m.run([m.run_job("mul_vec", ctx, c, dev(a), dev(b)), m.run_job("to_mont", ctx, t, dev(a)),
+           m.run_job("from_mont", ctx, f, t), m.run_job("from_mont", ctx, g, dev(b))])
+    assert np.array_equal(host(c), oracle.mont_mul(P, a, b))
+    assert np.array_equal(host(t), oracle.to_mont(P, a)) and np.array_equal(host(f), a)
+    assert np.array_equal(host(g), oracle.from_mont(P, b))
+    assert all(canaries_intact(buf, n, 0) for buf, _ in bufs)
+
+
+@pytest.mark.parametrize("batch", [1, 5, 33])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5, 6, 7])
+def test_guards_dot(m, batch, variant):
+    P = 2013265921
+    L = 16384
+    A = synth.uniform(42, 35, P, 0, batch * L).reshape(batch, L)
+    x = synth.uniform(42, 36, P, 0, L)
+    buf, o = guarded(batch, 0)
+    m.dot(m.ctx_init(P), dev(A), dev(x), out=o, cfg=m.Launch(variant=variant))
+    assert np.array_equal(host(o), oracle.dot(P, A, x))
+    assert canaries_intact(buf, batch, 0)
