@@ -340,21 +340,30 @@ class Workload:
         mont_run.h: one flat grid over all their tiles, to_mont -> from_mont fused) when
         HBM_MODE == "run", else individually; the IMAD-bound ones as they are."""
         hbm = [x for x in self.launches if x[4] == "hbm"]
-        if HBM_MODE == "pair" and hasattr(self, "abar"):
-            # only the to_mont -> from_mont pair as one fused mont_run launch, the rest individual
-            if not hasattr(self, "_pair_launch"):
+        if HBM_MODE in ("pair", "pairtw") and hasattr(self, "abar"):
+            # the to_mont -> from_mont pair (pairtw: and the twiddle multiply) as one fused mont_run
+            # launch, the rest individual
+            with_tw = HBM_MODE == "pairtw" and hasattr(self, "tw_x")
+            if getattr(self, "_pair_mode", None) != HBM_MODE:
                 m = self.m
                 self.pair_jobs = [m.run_job("to_mont", self.ctx[P0], self.abar, self.c2[P0][0]),
                                   m.run_job("from_mont", self.ctx[P0], self.back, self.abar)]
-                self._pair_launch = ("mont_run[to_mont -> from_mont fused]",
+                if with_tw:
+                    self.pair_jobs.append(m.run_job("twiddle", self.ctx[P0], self.tw_out.view(-1),
+                                                    self.tw_x.view(-1), self.tw))
+                self._pair_launch = ("mont_run[to_mont -> from_mont fused" + (", twiddle" if with_tw else "") + "]",
                                      lambda: m.run(self.pair_jobs, cfg=m.Launch(threads=RUN_SHAPE[0],
                                                                                 unroll=RUN_SHAPE[1])),
-                                     m.run_bytes(self.pair_jobs), 2 * N_C2, "hbm")
+                                     m.run_bytes(self.pair_jobs),
+                                     2 * N_C2 + (TW_BATCH * TW_LEN if with_tw else 0), "hbm")
+                self._pair_mode = HBM_MODE
             out = []
             for x in self.launches:
                 if x[0] == "to_mont":
                     out.append(self._pair_launch)
-                elif x[0] != "from_mont":
+                elif x[0] == "from_mont" or (with_tw and x[0] == "mont_mul_twiddle"):
+                    continue
+                else:
                     out.append(x)
             return out
         if HBM_MODE != "run" or len(hbm) < 2:

@@ -63,7 +63,7 @@ def main():
         if mode == "streams" and shape != shapes[0]:
             continue
         bench.HBM_STREAMS, bench.HBM_MODE, bench.RUN_SHAPE = hs, mode, shape
-        for attr in ("_run_launch", "_pair_launch"):
+        for attr in ("_run_launch", "_pair_launch", "_pair_mode"):
             if hasattr(wl, attr):
                 delattr(wl, attr)
         wl.pow_cfg_lane = L(ctas_per_sm=pc, variant=pv, chunk=sm, threads=pt)
