@@ -81,7 +81,7 @@ extern "C" {
  *                                   mbarrier (any len; 256 threads unless
  *                                   threads is set)
  *   chunk     : mont_mul_twiddle_ex: table columns staged per CTA
- *               (multiple of 4; 0 = min(len, 4096)).  mont_pow_vec_ex
+ *               (multiple of 4; 0 = min(len, 2048)).  mont_pow_vec_ex
  *               variants 11-16: bytes of dynamic shared memory reserved
  *               (never touched) per CTA, an occupancy cap that keeps a
  *               flat pow grid to a few CTAs per SM while other kernels

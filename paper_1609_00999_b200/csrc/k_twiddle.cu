@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(256) k_twiddle_scalar(Ctx c, uint32_t *out, co
 // table (variant 4) peaks at 84-86 us with many small CTAs (64 per SM, 256
 // threads, a few rows and a 4096-column chunk each) and is the path for other
 // row lengths.  Variant 0 = that choice (mont_ext.h).
-static const Launch kTwDefault{512, 64, 4, 0, 4096};
+static const Launch kTwDefault{512, 64, 4, 0, 2048};
 
 template <int U, bool TMA>
 static mont_status_t launch_tw(const Ctx &c, uint32_t *out, const uint32_t *x, const uint32_t *tw, size_t batch,
