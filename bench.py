@@ -1018,14 +1018,18 @@ def nvsmi_id(torch, local_rank: int) -> str:
     return str(local_rank)
 
 
-def ncu_traffic(name: str):
+def ncu_traffic(name: str, nbytes: int = 0):
+    """DRAM bytes per launch of this kernel kind from the committed ncu capture (2^26-element
+    launches); None when this launch's algorithmic bytes are not that capture's (other sizes)."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if not p.exists():
         return None
     try:
         d = json.loads(p.read_text())
         v = d.get("traffic_bytes_per_launch", {}).get(name.split("[")[0])
-        return int(v) if v is not None else None
+        if v is None or (nbytes and not 0.5 <= float(v) / nbytes <= 1.5):
+            return None
+        return int(v)
     except Exception:
         return None
 
@@ -1254,7 +1258,7 @@ def main():
                 if redc_peak:
                     r.update({"redc_chain_peak_measured": round(redc_peak, 4),
                               "frac_redc_measured": round(ach / redc_peak, 4)})
-            r["traffic"] = ncu_traffic(name)
+            r["traffic"] = ncu_traffic(name, nbytes)
             rows.append(r)
         return rows
 
