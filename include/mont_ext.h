@@ -35,7 +35,13 @@ extern "C" {
  *                                   (default 2048), threads <= 256, so few
  *                                   warps stream at full bandwidth
  *                                   (variants 2 and 3: 16-byte co-aligned
- *                                   operands, else the 32-bit path)
+ *                                   operands, else the 32-bit path),
+ *                                   4 (mont_mul_vec_ex and _checksum_ex only)
+ *                                   = flat grid with every product on the
+ *                                   FP64 pipe (two FP64 Barrett products per
+ *                                   element, a b mod P then times R^-1 mod P;
+ *                                   no FMAHeavy instruction; both operands
+ *                                   canonical)
  *                 mont_pow_vec_ex : 0 = library default: 11 when base, exp
  *                                   and out share their address mod 16, else
  *                                   17;  1 = binary ladder with selects;

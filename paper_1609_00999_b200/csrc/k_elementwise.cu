@@ -37,6 +37,18 @@ struct OpFrom {
     uint32_t p, pinv;
     __device__ __forceinline__ uint32_t operator()(uint32_t x) const { return redc1(x, p, pinv); }
 };
+// REDC(a, b) = a b R^-1 mod P computed on the FP64 pipe (mul_vec variant 4): two FP64 Barrett
+// products (mont_core.cuh fmulmod, 6 FP64 ops each: a b mod P, then times R^-1 mod P), no
+// FMAHeavy instruction -- for streaming next to an IMAD-bound kernel.  Both operands canonical.
+struct OpFmont {
+    double pd, pdinv, rinv;
+    __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const {
+        const double x = fmulmod(__uint2double_rn(a), __uint2double_rn(b), pd, pdinv);  // (-P, P)
+        double y = fmulmod(x, rinv, pd, pdinv);
+        y = y < 0.0 ? y + pd : y;
+        return __double2uint_rn(y);
+    }
+};
 struct OpBarrett {
     BarrettDev c;
     __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return barrett(a, b, c); }
@@ -473,6 +485,12 @@ static mont_status_t launch_map1(const Op &op, uint32_t *out, const uint32_t *in
 // persistent grid-stride shape by ~10 % -- the block scheduler balances the
 // slow and fast SMs dynamically, a static round-robin deal does not.
 static const Launch kMulVecDefault{256, 4, 1, 0, 0};
+
+// R^-1 mod P from the context: R R^-1 - P P' = 1 with P' = pneg
+static OpFmont fmont_op(const mont_ctx_t *ctx) {
+    const uint32_t rinv = (uint32_t)((1ull + (unsigned long long)ctx->p * ctx->pneg) >> 32);
+    return OpFmont{(double)ctx->p, 1.0 / (double)ctx->p, (double)rinv};
+}
 static const Launch kMap1Default{512, 4, 2, 0, 0};
 // fused checksum: 2 uint4 per thread x 512 threads -> one atomic per 4096 words
 static const Launch kMulVecSumDefault{512, 4, 2, 0, 0};
@@ -486,7 +504,12 @@ extern "C" mont_status_t mont_mul_vec_ex(const mont_ctx_t *ctx, uint32_t *c, con
     if (!ctx_ok(ctx)) return ctx ? MONT_EINVAL_P : MONT_EINVAL_ARG;
     if (n == 0) return MONT_OK;
     if (!a || !b || !c || ((uintptr_t)a | (uintptr_t)b | (uintptr_t)c) & 3u) return MONT_EINVAL_ARG;
-    const Launch L = resolve(cfg, kMulVecDefault);
+    Launch L = resolve(cfg, kMulVecDefault);
+    if (L.variant == 4) {  // FP64-pipe products, flat grid
+        L.variant = 0;
+        if (!launch_ok(L)) return MONT_EINVAL_ARG;
+        return launch_map2<false>(fmont_op(ctx), c, a, b, n, L, stream);
+    }
     if (!launch_ok(L)) return MONT_EINVAL_ARG;
     return launch_map2<false>(OpMul{ctx->p, 0u - ctx->pneg}, c, a, b, n, L, stream);
 }
@@ -503,7 +526,12 @@ extern "C" mont_status_t mont_mul_vec_checksum_ex(const mont_ctx_t *ctx, uint32_
     if (n == 0) return MONT_OK;
     if (!a || !b || !c || !acc || ((uintptr_t)a | (uintptr_t)b | (uintptr_t)c) & 3u || ((uintptr_t)acc & 7u))
         return MONT_EINVAL_ARG;
-    const Launch L = resolve(cfg, kMulVecSumDefault);
+    Launch L = resolve(cfg, kMulVecSumDefault);
+    if (L.variant == 4) {  // FP64-pipe products, flat grid
+        L.variant = 0;
+        if (!launch_ok(L)) return MONT_EINVAL_ARG;
+        return launch_map2<true>(fmont_op(ctx), c, a, b, n, L, stream, acc);
+    }
     if (!launch_ok(L)) return MONT_EINVAL_ARG;
     return launch_map2<true>(OpMul{ctx->p, 0u - ctx->pneg}, c, a, b, n, L, stream, acc);
 }

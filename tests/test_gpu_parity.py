@@ -528,3 +528,19 @@ def test_guards_dot(m, batch, variant):
     m.dot(m.ctx_init(P), dev(A), dev(x), out=o, cfg=m.Launch(variant=variant))
     assert np.array_equal(host(o), oracle.dot(P, A, x))
     assert canaries_intact(buf, batch, 0)
+
+
+@pytest.mark.parametrize("P", PRIMES + (3, 17, 2147483647, 1073741827))
+@pytest.mark.parametrize("n", [1, 5, 4100, 1 << 18])
+def test_mul_vec_fp64_variant(m, P, n):
+    """mont_mul_vec_ex / _checksum_ex variant 4: the same REDC result from two FP64 Barrett
+    products per element (a b mod P, then times R^-1 mod P), canonical inputs."""
+    a, b = synth.c2_inputs(P, 0, n) if P > 257 else (np.arange(n, dtype=np.uint32) % P, (np.arange(n, dtype=np.uint32) * 7) % P)
+    a, b = a.astype(np.uint32), b.astype(np.uint32)
+    if n >= 3:
+        a[:3], b[:3] = [P - 1, 0, P - 1], [P - 1, P - 1, 1]
+    ref = oracle.mont_mul(P, a, b)
+    cfg = m.Launch(variant=4)
+    assert np.array_equal(host(m.mul_vec(m.ctx_init(P), dev(a), dev(b), cfg=cfg)), ref)
+    c, acc = m.mul_vec_checksum(m.ctx_init(P), dev(a), dev(b), cfg=cfg)
+    assert np.array_equal(host(c), ref) and int(acc.item()) == oracle.raw_sum(ref)
