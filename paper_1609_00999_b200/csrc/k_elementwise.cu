@@ -510,7 +510,7 @@ extern "C" mont_status_t mont_mul_vec_ex(const mont_ctx_t *ctx, uint32_t *c, con
         if (!launch_ok(L)) return MONT_EINVAL_ARG;
         return launch_map2<false>(fmont_op(ctx), c, a, b, n, L, stream);
     }
-    if (!launch_ok(L)) return MONT_EINVAL_ARG;
+    if (!launch_ok(L) || L.variant > 3) return MONT_EINVAL_ARG;
     return launch_map2<false>(OpMul{ctx->p, 0u - ctx->pneg}, c, a, b, n, L, stream);
 }
 
@@ -532,7 +532,7 @@ extern "C" mont_status_t mont_mul_vec_checksum_ex(const mont_ctx_t *ctx, uint32_
         if (!launch_ok(L)) return MONT_EINVAL_ARG;
         return launch_map2<true>(fmont_op(ctx), c, a, b, n, L, stream, acc);
     }
-    if (!launch_ok(L)) return MONT_EINVAL_ARG;
+    if (!launch_ok(L) || L.variant > 3) return MONT_EINVAL_ARG;
     return launch_map2<true>(OpMul{ctx->p, 0u - ctx->pneg}, c, a, b, n, L, stream, acc);
 }
 
@@ -548,7 +548,7 @@ extern "C" mont_status_t to_mont_ex(const mont_ctx_t *ctx, uint32_t *out, const 
     if (n == 0) return MONT_OK;
     if (!in || !out || ((uintptr_t)in | (uintptr_t)out) & 3u) return MONT_EINVAL_ARG;
     const Launch L = resolve(cfg, kMap1Default);
-    if (!launch_ok(L)) return MONT_EINVAL_ARG;
+    if (!launch_ok(L) || L.variant > 3) return MONT_EINVAL_ARG;
     return launch_map1(OpTo{ctx->p, 0u - ctx->pneg, ctx->r2}, out, in, n, L, stream);
 }
 
@@ -563,7 +563,7 @@ extern "C" mont_status_t from_mont_ex(const mont_ctx_t *ctx, uint32_t *out, cons
     if (n == 0) return MONT_OK;
     if (!in || !out || ((uintptr_t)in | (uintptr_t)out) & 3u) return MONT_EINVAL_ARG;
     const Launch L = resolve(cfg, kMap1Default);
-    if (!launch_ok(L)) return MONT_EINVAL_ARG;
+    if (!launch_ok(L) || L.variant > 3) return MONT_EINVAL_ARG;
     return launch_map1(OpFrom{ctx->p, 0u - ctx->pneg}, out, in, n, L, stream);
 }
 
@@ -596,7 +596,7 @@ extern "C" mont_status_t mb_triad(uint32_t *c, const uint32_t *a, const uint32_t
     if (n == 0) return MONT_OK;
     if (!a || !b || !c) return MONT_EINVAL_ARG;
     const Launch L = resolve(cfg, kMulVecDefault);
-    if (!launch_ok(L)) return MONT_EINVAL_ARG;
+    if (!launch_ok(L) || L.variant > 3) return MONT_EINVAL_ARG;
     return launch_map2<false>(OpXor{}, c, a, b, n, L, stream);
 }
 
@@ -605,7 +605,7 @@ extern "C" mont_status_t mb_copy(uint32_t *out, const uint32_t *in, size_t n, co
     if (n == 0) return MONT_OK;
     if (!in || !out) return MONT_EINVAL_ARG;
     const Launch L = resolve(cfg, kMap1Default);
-    if (!launch_ok(L)) return MONT_EINVAL_ARG;
+    if (!launch_ok(L) || L.variant > 3) return MONT_EINVAL_ARG;
     return launch_map1(OpCopy{}, out, in, n, L, stream);
 }
 

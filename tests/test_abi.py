@@ -109,6 +109,15 @@ def test_validation_without_launch():
     assert L.mont_mul_vec_ex(pc, 0x1000, 0x2000, 0x3000, 8, C.byref(cfg), None) == 2
     assert L.synth_fill(None, 4, 1, 1, 0, 17, 0, 0, None) == 2
     assert L.synth_fill(0x1000, 4, 1, 1, 0, 17, 7, 0, None) == 2
+    # variants outside each entry point's documented set are refused, not silently remapped
+    for v, fn in ((5, L.mont_mul_vec_ex), (4, L.to_mont_ex), (4, L.from_mont_ex)):
+        cfg = m.Launch(variant=v)
+        args = (pc, 0x1000, 0x2000, 0x3000, 8) if fn is L.mont_mul_vec_ex else (pc, 0x1000, 0x2000, 8)
+        assert fn(*args, C.byref(cfg), None) == 2, v
+    cfg = m.Launch(variant=18)
+    assert L.mont_pow_vec_ex(pc, 0x1000, 0x2000, 0x3000, 8, C.byref(cfg), None) == 2
+    cfg = m.Launch(variant=5)
+    assert L.mont_mul_twiddle_ex(pc, 0x1000, 0x2000, 0x3000, 4, 16, C.byref(cfg), None) == 2
 
 
 def test_host_run_bytes_fusion_plan():
