@@ -140,15 +140,21 @@ def main():
             k = d["Kernel Name"].split("(")[0][:70]
             agg.setdefault(k, []).append(float(d["Metric Value"]))
         ours = {k: v for k, v in agg.items() if "mont::" in k or k.startswith("void mont::")}
-        # the timed step: the last 2 launches of each of our hot kernels
+        # the step's kernels (the microbenchmarks that give roofline denominators, the input generator
+        # and the twiddle-table builder are excluded); share = each kind's total serialised time over
+        # the command / the total of the step's kinds -- every pass of the command (verify, warm-up,
+        # serial pass, graph replays) runs each step kernel in the same proportion
+        skip = ("k_synth", "twiddle_table", "k_imad", "k_pipe", "k_sm_clock", "OpXor", "OpCopy")
+        hot = {k: v for k, v in ours.items() if not any(x in k for x in skip)}
+        tot = sum(sum(v) for v in hot.values())
         md += ["## Launch list (same bench command, `--metrics gpu__time_duration.sum`)", "",
-               "| kernel | launches | mean µs | share of our hot-kernel time |", "|---|---|---|---|"]
-        hot = {k: v for k, v in ours.items() if "k_synth" not in k and "twiddle_table" not in k}
-        tot = sum(sum(v) / len(v) * (3 if "k_map2" in k else 1) for k, v in hot.items())
+               "ncu serialises every launch, so the two lanes of the timed step do not overlap here: the shares "
+               "are of the serialised kernel time (the step's own overlap is in the bench line's "
+               "`kernels_timed_step`).", "",
+               "| kernel | launches | mean µs | share of the step kernels' serialised time |", "|---|---|---|---|"]
         for k, v in agg.items():
             mean = sum(v) / len(v) / 1e3
-            mult = 3 if "k_map2" in k else 1
-            share = (sum(v) / len(v) * mult / tot) if k in hot and tot else None
+            share = (sum(v) / tot) if k in hot and tot else None
             md.append(f"| `{k}` | {len(v)} | {mean:.1f} | {'' if share is None else f'{share:.3f}'} |")
         md.append("")
     (prof / f"{args.round}_ncu_summary.md").write_text("\n".join(md) + "\n")

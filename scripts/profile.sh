@@ -7,7 +7,7 @@ OUT=${OUT:-gpurun_out}
 ROUND=${ROUND:-r02}
 mkdir -p $OUT
 timeout 900 python bench.py > $OUT/bench_final.log 2>&1; echo "bench rc=$?"
-CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --soak 0"
+CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --soak 0 --no-subruns"
 $CMD > $OUT/plain_small.log 2>&1 || { echo "plain small bench failed"; tail -20 $OUT/plain_small.log; exit 1; }
 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
 echo "launch list rc=$?"
