@@ -1083,16 +1083,19 @@ def main():
     for _ in range(max(3, args.warmup)):
         wl.step()
     torch.cuda.synchronize()
+    # per-kernel durations (`kernels`): a serial pass with events around each launch on the warm GPU,
+    # then the clock the IMAD-bound launch ran at (its roofline is clock-normalised)
+    _, per_ms = time_steps(wl, args.steps)
+    imad_mhz = imad_launch_clock_mhz(wl, max(3, args.steps))
     t_end = time.perf_counter() + args.soak
     while time.perf_counter() < t_end:
         wl.step_concurrent()
         torch.cuda.synchronize()
     shard.barrier()
     torch.cuda.synchronize()
-    # per-kernel durations: a serial pass (each launch bracketed by events), then the clock the
-    # IMAD-bound launch ran at in that state (its roofline is clock-normalised)
-    serial_ms, per_ms = time_steps(wl, args.steps)
-    imad_mhz = imad_launch_clock_mhz(wl, max(3, args.steps))
+    # the serial step after the soak (ms_per_step_serial; it also lets the clock settle before the
+    # timed two-lane step: the overlapped step draws more power than the serial one)
+    serial_ms, _ = time_steps(wl, args.steps)
     for _ in range(3):
         wl.step_concurrent()
     torch.cuda.synchronize()
