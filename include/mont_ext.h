@@ -173,8 +173,9 @@ mont_status_t mb_imad(uint32_t *sink, int kind, int iters, const mont_launch_t *
  *   41 IMAD.WIDE / fmulmod (counted as instructions; 40 and 41 count one REDC or fmulmod as
  *   one).  42: no work; sink[t] = the %warpid of thread t's warp.  43-48: NI REDC + NF
  *   fmulmod chains per thread interleaved instruction by instruction, (NI, NF) = (1,1), (3,1),
- *   (6,2), (2,0), (0,2), (4,0); mb_pipe_ops_per_iter = 32 (NI + NF) products.
- *   kind outside [0, 49) is MONT_EINVAL_ARG.
+ *   (6,2), (2,0), (0,2), (4,0); mb_pipe_ops_per_iter = 32 (NI + NF) products.  49: IMAD.HI
+ *   R,R,R with an RZ addend (mul.hi.u32, as in __umulhi).  kind outside [0, 50) is
+ *   MONT_EINVAL_ARG.
  *   grid = SMs * ctas_per_sm (cfg may be NULL: 8), 256 threads; sink holds one word per
  *   thread.  Executed instructions = threads * iters * 128.  If clk (a DEVICE pointer to 2
  *   uint64) is not NULL, CTA 0 stores its elapsed SM cycles (clock64) and nanoseconds

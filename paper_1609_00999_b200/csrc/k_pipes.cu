@@ -29,6 +29,9 @@ __device__ __forceinline__ void p_imad_cb(uint32_t &a, uint32_t b, uint32_t c) {
 __device__ __forceinline__ void p_imad_hi(uint32_t &a, uint32_t b) {  // IMAD.HI R, R, R, R
     asm volatile("mad.hi.u32 %0, %0, %1, %0;" : "+r"(a) : "r"(b));
 }
+__device__ __forceinline__ void p_imad_hi_rz(uint32_t &a, uint32_t b) {  // IMAD.HI R, R, R, RZ
+    asm volatile("mul.hi.u32 %0, %0, %1;" : "+r"(a) : "r"(b));
+}
 __device__ __forceinline__ void p_imad_hi_imm(uint32_t &a, uint32_t b) {  // IMAD.HI R, R, imm, R
     asm volatile("mad.hi.u32 %0, %0, 0x1c000001, %1;" : "+r"(a) : "r"(b));
 }
@@ -166,6 +169,7 @@ __global__ void __launch_bounds__(256) k_pipe(uint32_t *sink, int iters, uint32_
                 else if (K == 31) { p_dmul(da[k], db[k]); p_dmul(db[k], da[k]); }   // DMUL
                 else if (K == 32) { p_dadd(da[k], db[k]); p_dadd(db[k], da[k]); }   // DADD
                 else if (K == 33) { p_imad(a[k], b[k]); p_dmul(da[k], db[k]); }     // IMAD + DMUL
+                else if (K == 49) { p_imad_hi_rz(a[k], b[k]); p_imad_hi_rz(b[k], a[k]); }  // IMAD.HI, RZ addend
                 else if (K >= 38 && K <= 41) {
                     // warp-specialised pairs: warps 0-3 one kind, warps 4-7 the other (2 instr each)
                     if (!fp_warp) {
@@ -273,12 +277,12 @@ extern "C" mont_status_t mb_sm_clock(unsigned long long *out, long long cycles, 
 static const int kMixNI[6] = {1, 3, 6, 2, 0, 4};
 static const int kMixNF[6] = {1, 1, 2, 0, 2, 0};
 
-#define MB_PIPE_KINDS 49
+#define MB_PIPE_KINDS 50
 
 // instructions (kinds 27-30: modular products) of the timed kind(s) per thread per loop
 // iteration: 8 trips x 8 chains x 2
 extern "C" int mb_pipe_ops_per_iter(int kind) {
-    if (kind >= 43 && kind < MB_PIPE_KINDS) return 32 * (kMixNI[kind - 43] + kMixNF[kind - 43]);
+    if (kind >= 43 && kind <= 48) return 32 * (kMixNI[kind - 43] + kMixNF[kind - 43]);
     return (kind >= 0 && kind < MB_PIPE_KINDS) ? 128 : 0;
 }
 
@@ -305,6 +309,7 @@ extern "C" mont_status_t mb_pipe(uint32_t *sink, int kind, int iters, const mont
         case 46: k_mix<2, 0><<<grid, 256, 0, stream>>>(sink, iters, 469762049.0, 1.0 / 469762049.0, clk); break;
         case 47: k_mix<0, 2><<<grid, 256, 0, stream>>>(sink, iters, 469762049.0, 1.0 / 469762049.0, clk); break;
         case 48: k_mix<4, 0><<<grid, 256, 0, stream>>>(sink, iters, 469762049.0, 1.0 / 469762049.0, clk); break;
+        MB_CASE(49)
         default: return MONT_EINVAL_ARG;
     }
 #undef MB_CASE

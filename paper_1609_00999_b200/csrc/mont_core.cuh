@@ -55,8 +55,8 @@ __device__ __forceinline__ int32_t hi32s(int64_t x) { return (int32_t)(x >> 32);
 
 // Measured on B200 with dependent chains nothing can hoist (mb_pipe, csrc/k_pipes.cu;
 // profiles/r02_pipes.jsonl): IMAD issues at 64 lanes/clk/SM (register, immediate
-// or uniform-register operand alike), IMAD.WIDE at 32 (half rate), IMAD.HI at 32 with an
-// immediate operand and ~26 with three register operands.  So the high halves are taken from
+// or uniform-register operand alike), IMAD.WIDE at 32 (half rate), IMAD.HI at 32 (~26 when
+// all three sources are registers: mad.hi with a register addend).  So the high halves are taken from
 // IMAD.WIDE results, never from mul.hi, and the REDC is written in the "subtract" form, which
 // needs no carry:
 //   T = a b (IMAD.WIDE);  m = lo(T) P^-1 mod 2^32 (IMAD);  M = m P (IMAD.WIDE)

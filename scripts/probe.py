@@ -88,7 +88,7 @@ if args.what == "pipes":
              37: "warp-specialised 1/4 fmulmod (products)", 38: "warps IMAD.WIDE | DFMA",
              39: "warps IMAD.WIDE | DMUL", 40: "warps sredc | DFMA (ops)", 41: "warps IMAD.WIDE | fmulmod (ops)",
              43: "in-warp 1 sredc : 1 fmulmod chains", 44: "in-warp 3:1", 45: "in-warp 6:2", 46: "2 sredc chains",
-             47: "2 fmulmod chains", 48: "4 sredc chains"}
+             47: "2 fmulmod chains", 48: "4 sredc chains", 49: "IMAD.HI R,R,R,RZ (mul.hi)"}
     sink = torch.empty(sms * 32 * 256, dtype=torch.uint32, device=dev)
     clkbuf = torch.zeros(2, dtype=torch.int64, device=dev)
 
@@ -100,7 +100,7 @@ if args.what == "pipes":
         except Exception:
             return None
 
-    kinds = [int(k) for k in os.environ.get("PROBE_KINDS", "").split(",") if k] or list(range(42)) + list(range(43, 49))
+    kinds = [int(k) for k in os.environ.get("PROBE_KINDS", "").split(",") if k] or list(range(42)) + list(range(43, 50))
     if os.environ.get("PROBE_SLOTS"):
         nthr = C.c_ulonglong(0)
         lib().mb_pipe(sink.data_ptr(), 42, 1, C.byref(m.Launch(ctas_per_sm=8)), s.cuda_stream, C.byref(nthr), None)

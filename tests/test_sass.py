@@ -25,7 +25,7 @@ PIPE_KINDS = {
     18: ["IMAD.WIDE.U32", "DFMA"], 19: ["IMAD.WIDE.U32", "IMAD"], 20: ["IMAD", "FFMA"],
     21: ["IMAD", "IADD3"], 22: ["IMAD.WIDE.U32", "LOP3.LUT"], 23: ["IMAD"], 24: ["IMAD", "DFMA"],
     25: ["IMAD.WIDE.U32", "DMUL"], 26: ["IMAD.WIDE.U32", "DADD"], 31: ["DMUL"], 32: ["DADD"],
-    33: ["IMAD", "DMUL"], 38: ["IMAD.WIDE.U32", "DFMA", "MOV", "IMAD.MOV.U32", "LOP3.LUT"],
+    33: ["IMAD", "DMUL"], 49: ["IMAD.HI.U32"], 38: ["IMAD.WIDE.U32", "DFMA", "MOV", "IMAD.MOV.U32", "LOP3.LUT"],
     39: ["IMAD.WIDE.U32", "DMUL", "MOV", "IMAD.MOV.U32", "LOP3.LUT"],
 }
 
@@ -49,4 +49,5 @@ def test_pipe_kind_times_its_instruction(sass, kind):
 
 def test_pipe_ops_per_iter():
     assert all(m.lib().mb_pipe_ops_per_iter(k) == 128 for k in PIPE_KINDS)
-    assert m.lib().mb_pipe_ops_per_iter(43) == 64 and m.lib().mb_pipe_ops_per_iter(49) == 0
+    assert m.lib().mb_pipe_ops_per_iter(43) == 64 and m.lib().mb_pipe_ops_per_iter(49) == 128
+    assert m.lib().mb_pipe_ops_per_iter(50) == 0
