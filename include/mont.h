@@ -96,12 +96,12 @@ mont_status_t mont_mul_vec(const mont_ctx_t *ctx, uint32_t *c, const uint32_t *a
  * row of a row-major batch x len matrix times one broadcast twiddle vector
  * (the NTT-stage twiddle multiply of the paper's modular FFTs, PAPER.md:19,
  * :189; BASELINE configs[2]).  With tw[j] = to_mont(w^j) this is
- * x * w^j mod P in the plain domain.  For power-of-two len the batch is one
- * flat 128-bit stream and the table is read through the read-only (L1) path,
- * where it stays resident; for other len the table is staged per CTA into
- * shared memory by the bulk-copy (TMA) engine, cp.async.bulk + mbarrier
- * (mont_mul_twiddle_ex variant 4 forces that path for any len; DESIGN.md §6
- * has both measured).  Requires len >= 1 when batch > 0.  x and out are batch*len
+ * x * w^j mod P in the plain domain.  Each CTA stages its chunk of the table
+ * into shared memory with the bulk-copy (TMA) engine, cp.async.bulk + mbarrier,
+ * while its first x loads are in flight (mont_mul_twiddle_ex variant 2 instead
+ * treats a power-of-two-len batch as one flat stream and reads the table
+ * through L1; DESIGN.md §6 has both measured).  len not a multiple of 4 or
+ * misaligned operands take a scalar path.  Requires len >= 1 when batch > 0.  x and out are batch*len
  * elements; out may alias x.  8 bytes of HBM traffic per element. */
 mont_status_t mont_mul_twiddle(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *x,
                                const uint32_t *tw, size_t batch, size_t len, cudaStream_t stream);

@@ -74,8 +74,8 @@ extern "C" {
  *                                   window, 4 lanes per thread, table in
  *                                   registers (any alignment).
  *                                   ctas_per_sm = 0 selects a flat grid.
- *                 mont_mul_twiddle_ex : 0 = library default: 2 for power-of-two
- *                                   len, else 4;
+ *                 mont_mul_twiddle_ex : 0 = library default: 4 (the table
+ *                                   staged in shared memory by TMA);
  *                                   1 = table read through L1/L2 (no smem),
  *                                   2 = flat stream (power-of-two len; else 4),
  *                                   3 = whole table staged once per CTA

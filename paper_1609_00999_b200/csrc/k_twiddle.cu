@@ -197,12 +197,12 @@ __global__ void __launch_bounds__(256) k_twiddle_scalar(Ctx c, uint32_t *out, co
     }
 }
 
-// B200 sweeps: for power-of-two rows the flat stream with the
-// table through L1 (variant 2, 512 threads x 4 uint4) runs at the to_mont rate
-// (82 us for configs[2], 1.0x the measured copy peak); the bulk-copy staged
-// table (variant 4) peaks at 84-86 us with many small CTAs (64 per SM, 256
-// threads, a few rows and a 4096-column chunk each) and is the path for other
-// row lengths.  Variant 0 = that choice (mont_ext.h).
+// B200 sweeps: the bulk-copy (TMA) staged table (variant 4: 64 CTAs per SM of
+// 256 threads, a few rows and a 2048-column chunk each) runs configs[2] in 84.35 us, the flat
+// stream with the table through L1 (variant 2, 512 threads x 4 uint4) in 84.26 us
+// (profiles/r02_probe_twiddle_paths.jsonl); inside bench.py's two-lane step the staged path is
+// the faster one (0.5956 vs 0.5997 ms per step, profiles/r02_step_sweep.jsonl), so variant 0
+// (the library default) is variant 4 for every row length.
 static const Launch kTwDefault{512, 64, 4, 0, 2048};
 
 template <int U, bool TMA>
@@ -263,7 +263,7 @@ extern "C" mont_status_t mont_mul_twiddle_ex(const mont_ctx_t *ctx, uint32_t *ou
     }
     const bool pow2 = (len & (len - 1)) == 0;
     int v = L.variant;
-    if (v == 0) v = pow2 ? 2 : 4;  // library default
+    if (v == 0) v = 4;  // library default: the TMA-staged table (ties the L1 path alone, wins in the step)
     if (v == 3 && len * 4 <= 200 * 1024) {  // staged once per CTA + CLC work stealing
         const uint32_t rows_per_item = 2u;
         const size_t items = (batch + rows_per_item - 1) / rows_per_item;
