@@ -46,8 +46,14 @@ mont_status_t mont_ntt(const mont_ctx_t *ctx, uint32_t *data, size_t batch, int 
  * and each butterfly computes x w mod P as x w - hi(x w') P (Shoup), one high
  * product instead of REDC's two,
  * 4 / 5 = variants 0 / 3 with the XOR-swizzled shared layout (bit reversal in
- * the final gather; for measurement).  Variants 3-5 need log_n >= 5, else
- * MONT_EUNSUPPORTED.  For P < 2^30 variants 0 and 3 keep values between stages
+ * the final gather; for measurement),
+ * 6 / 7 = variants 0 / 3 as a persistent grid (resident CTAs x SMs looping over
+ * the rows; the next row's loads are issued before this row's stores).  At
+ * log_n = 15 (one CTA per SM) variants 0 / 3 run these kernels.  Variants 3-7
+ * need log_n >= 5, else MONT_EUNSUPPORTED.  At log_n = 14 variants 0 / 3 also
+ * prefetch the rows one wave ahead into L2 (cp.async.bulk.prefetch; the
+ * environment variable MONT_NTT_NO_PF=1, read once, turns that off for
+ * measurement).  For P < 2^30 variants 0, 3, 6 and 7 keep values between stages
  * in [0, 2P) (lazy butterflies, one correction fewer each; the environment
  * variable MONT_NTT_NO_LAZY=1, read once, turns that off for measurement).
  * All variants give identical outputs. */

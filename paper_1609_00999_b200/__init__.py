@@ -19,6 +19,8 @@ from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "libmont.so"
+if os.environ.get("MONT_LIB_AB"):  # measurement only: an A/B build of the same library (scripts/ab_build.sh)
+    LIB_PATH = _HERE / "csrc" / "build_ab" / f"libmont_{os.environ['MONT_LIB_AB']}.so"
 
 __all__ = [
     "Ctx", "MontError", "ctx_init", "to_mont", "from_mont", "mul_vec", "mul_vec_checksum", "mul_twiddle", "pow_vec",

@@ -18,10 +18,12 @@
 // plain twiddle with its precomputed quotient (Shoup).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "../../include/mont_ntt.h"
 #include "abi_util.h"
+#include "tma.cuh"
 
 namespace mont {
 
@@ -194,12 +196,161 @@ __host__ __device__ constexpr uint32_t brev_bits(uint32_t x) {
 // a - d + 2P < 4P goes into the product unreduced, and the product's own final correction is
 // dropped (REDC and the precomputed-quotient product both return [0, 2P) before it) -- one ALU op
 // fewer per butterfly; outputs are canonicalised once at the end.
+// L2 prefetch of the row group `grp` (rpc rows of N words, contiguous) in 4 KiB pieces, one per
+// thread of the first warps: issued at the start of a CTA for the group a CTA will take about one
+// wave later, so that group's first-trip loads come from L2 instead of HBM
+__device__ __forceinline__ void prefetch_group(const uint32_t *data, size_t batch, size_t grp, uint32_t rpc,
+                                               uint32_t N) {
+    const size_t r0 = grp * rpc;
+    if (r0 >= batch) return;
+    const size_t rows = batch - r0 < rpc ? batch - r0 : rpc;
+    const size_t bytes = rows * N * 4;
+    const size_t off = (size_t)threadIdx.x * 4096;
+    if (off < bytes) {
+        const size_t len = bytes - off < 4096 ? bytes - off : 4096;
+        bulk_prefetch_l2(data + r0 * N + off / 4, (uint32_t)len);
+    }
+}
+
+// The butterflies of one DIF trip (window bits [wlo, wlo + 5), stages with pair distance < 2^top)
+// on the 32 values v[] of one thread; tl = the thread's index bits below the window.  (Writing the
+// REDC's last step as one three-input add hi T - hi M + P and min(r, r - P), to keep it off the
+// FMAHeavy pipe, compiles to the same SASS: ptxas canonicalises both forms.)
+template <int LOG_N, bool PQ, bool LAZY>
+__device__ __forceinline__ void dif_trip(const Ctx &c, uint32_t (&v)[32], const int top, const int wlo,
+                                         const uint32_t tl, const uint32_t *__restrict__ tw) {
+#pragma unroll
+    for (int lb = 4; lb >= 0; --lb) {
+        const int b = wlo + lb;  // pair distance 2^b
+        if (b >= top) continue;  // done by an earlier trip
+        const uint32_t *twb = tw + ((1u << b) - 1u) + tl;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int k0 = ((q >> lb) << (lb + 1)) | (q & ((1 << lb) - 1));
+            const int k1 = k0 | (1 << lb);
+            const uint32_t j = (uint32_t)(k0 & ((1 << lb) - 1));
+            const uint32_t a = v[k0], d = v[k1];
+            const uint32_t p2 = 2u * c.p;
+            if (LAZY) {
+                const uint32_t sum = a + d;  // [0, 4P)
+                v[k0] = umin(sum, sum - p2);  // [0, 2P)
+            } else {
+                v[k0] = mod_add(a, d, c.p);
+            }
+            if (wlo == 0 && j == 0) {  // twiddle w^0 = 1: no product (see k_ntt_dif)
+                if (LAZY) {
+                    const uint32_t x = a - d + p2;
+                    v[k1] = umin(x, x - p2);
+                } else {
+                    v[k1] = mod_sub(a, d, c.p);
+                }
+            } else if (PQ) {
+                const uint2 wq = __ldg(reinterpret_cast<const uint2 *>(tw) + ((1u << b) - 1u) + tl + (j << wlo));
+                const uint32_t x = a - d + (LAZY ? p2 : c.p);
+                const uint32_t qq = __umulhi(x, wq.y);
+                const uint32_t r = x * wq.x - qq * c.p;
+                v[k1] = LAZY ? r : umin(r, r - c.p);
+            } else if (LAZY) {
+                const uint64_t T = mul_wide_u32(a - d + p2, __ldg(twb + (j << wlo)));
+                const uint32_t m = (uint32_t)T * c.pinv;
+                v[k1] = hi32(T) - hi32(mul_wide_u32(m, c.p)) + c.p;
+            } else {
+                v[k1] = redc(a - d + c.p, __ldg(twb + (j << wlo)), c.p, c.pinv);
+            }
+        }
+    }
+}
+
+// Persistent, software-pipelined form of k_ntt_dif<LOG_N, PQ, PAD = true, LAZY> (variants 6 / 7):
+// a grid of (resident CTAs per SM) x SMs loops over the row groups, and the first trip's HBM loads
+// of the NEXT group are issued right after the last trip's bit-reversed store -- before this group's
+// final gather and its HBM stores -- so their latency hides behind that phase instead of leaving
+// the SM with half its warps waiting at the start of every CTA.  Same arithmetic, same outputs.
+template <int LOG_N, bool PQ, bool LAZY>
+__global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
+    k_ntt_difp(Ctx c, uint32_t *data, size_t batch, const uint32_t *__restrict__ tw, uint32_t scale, Tw2D t2,
+               uint32_t pf) {
+    constexpr uint32_t N = 1u << LOG_N, T = N >> 5;
+    constexpr uint32_t NP = N + (N >> 5);
+    constexpr int NTRIP = (LOG_N + 4) / 5;
+    constexpr int WLO0 = LOG_N - 5 > 0 ? LOG_N - 5 : 0;
+    extern __shared__ uint32_t sm[];
+    const uint32_t rpc = blockDim.x / T;
+    const uint32_t rl = threadIdx.x / T, t = threadIdx.x % T;
+    uint32_t *s = sm + (size_t)rl * NP;
+    const uint32_t base0 = (t & ((1u << WLO0) - 1u)) | ((t >> WLO0) << (WLO0 + 5));
+    uint32_t v[32];
+    size_t grp = blockIdx.x;
+    {
+        const size_t row = grp * rpc + rl;
+        if (row < batch) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) v[k] = ld_stream1(data + row * N + base0 + ((uint32_t)k << WLO0));
+        }
+    }
+    for (; grp * rpc < batch; grp += gridDim.x) {  // uniform over the CTA
+        const size_t row = grp * rpc + rl;
+        const bool live = row < batch;
+        if (pf) prefetch_group(data, batch, grp + gridDim.x, rpc, N);
+#pragma unroll
+        for (int trip = 0; trip < NTRIP; ++trip) {
+            const int top = LOG_N - 5 * trip;
+            const int wlo = top - 5 > 0 ? top - 5 : 0;
+            const uint32_t tl = t & ((1u << wlo) - 1u);
+            const uint32_t base = tl | ((t >> wlo) << (wlo + 5));
+            const uint32_t sb = lay<true>(base);
+            if (trip > 0) {
+#pragma unroll
+                for (int k = 0; k < 32; ++k) v[k] = s[lay_comb<true>(sb, lay<true>((uint32_t)k << wlo))];
+            }
+            dif_trip<LOG_N, PQ, LAZY>(c, v, top, wlo, tl, tw);
+            if (trip == NTRIP - 1) {
+                if (NTRIP > 1) __syncthreads();
+                const uint32_t bb = lay<true>(brev_bits<LOG_N>(base));
+#pragma unroll
+                for (int k = 0; k < 32; ++k) s[bb + lay<true>(brev_bits<LOG_N>((uint32_t)k << wlo))] = v[k];
+            } else {
+#pragma unroll
+                for (int k = 0; k < 32; ++k) s[lay_comb<true>(sb, lay<true>((uint32_t)k << wlo))] = v[k];
+            }
+            __syncthreads();
+        }
+        // next group's first-trip loads, in flight during this group's gather and stores
+        const size_t nrow = row + (size_t)gridDim.x * rpc;
+        if (nrow < batch) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) v[k] = ld_stream1(data + nrow * N + base0 + ((uint32_t)k << WLO0));
+        }
+        if (live) {
+            uint32_t *g = data + row * N;
+            const uint32_t bt = lay<true>(t);
+            const uint64_t rowg = (uint64_t)(row + t2.row0);
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                const uint32_t idx = t + (uint32_t)k * T;
+                uint32_t x = s[bt + lay<true>((uint32_t)k * T)];
+                if (LAZY) x = umin(x, x - c.p);
+                if (t2.lo) {
+                    const uint64_t e = (rowg * idx) & t2.mask;
+                    const uint32_t we = redc(__ldg(t2.hi + (e >> t2.shift)), __ldg(t2.lo + (e & t2.lomask)), c.p, c.pinv);
+                    x = redc(x, we, c.p, c.pinv);
+                }
+                if (scale != c.r1) x = redc(x, scale, c.p, c.pinv);
+                st_stream1(g + idx, x);
+            }
+        }
+        __syncthreads();  // the next group's first trip overwrites s
+    }
+}
+
 template <int LOG_N, bool PQ = false, bool PAD = false, bool LAZY = false>
 __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
-    k_ntt_dif(Ctx c, uint32_t *data, size_t batch, const uint32_t *__restrict__ tw, uint32_t scale, Tw2D t2) {
+    k_ntt_dif(Ctx c, uint32_t *data, size_t batch, const uint32_t *__restrict__ tw, uint32_t scale, Tw2D t2,
+              uint32_t pf) {
     constexpr uint32_t N = 1u << LOG_N, T = N >> 5;
     constexpr uint32_t NP = PAD ? N + (N >> 5) : N;  // words per row in shared memory
     extern __shared__ uint32_t sm[];
+    if (pf) prefetch_group(data, batch, (size_t)blockIdx.x + pf, blockDim.x / T, N);
     const uint32_t rl = threadIdx.x / T, t = threadIdx.x % T;
     const size_t row = (size_t)blockIdx.x * (blockDim.x / T) + rl;
     const bool live = row < batch;
@@ -435,6 +586,13 @@ __global__ void __launch_bounds__(C * (1 << LOG_N) / 32, C * (1 << LOG_N) / 32 <
     }
 }
 
+// L2 prefetch of the row group one wave ahead in the row kernels; MONT_NTT_NO_PF=1 turns it off
+// (measurement)
+static bool ntt_pf() {
+    static const bool on = !(getenv("MONT_NTT_NO_PF") && getenv("MONT_NTT_NO_PF")[0] == '1');
+    return on;
+}
+
 template <int LOG_N, int C, bool PQ, bool LAZY = false>
 static mont_status_t launch_ntt_col(const Ctx &c, uint32_t *data, size_t ld, const uint32_t *tw, Tw2D t2,
                                     cudaStream_t stream) {
@@ -462,7 +620,42 @@ static mont_status_t launch_ntt_dif(const Ctx &c, uint32_t *data, size_t batch, 
         cudaFuncSetAttribute(k_ntt_dif<LOG_N, PQ, PAD, LAZY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess)
         return MONT_ECUDA;
-    k_ntt_dif<LOG_N, PQ, PAD, LAZY><<<(unsigned)grid, rpc * T, smem, stream>>>(c, data, batch, tw, scale, t2);
+    // L2 prefetch one wave of resident CTAs ahead (2 per SM at 2^14): 2^14 rows 221.7 -> 217.6 us;
+    // for shorter rows it measured 2 % slower, so it is off there
+    // (profiles/r02_probe_ntt_persistent.jsonl)
+    const int sms = sm_count();
+    const uint32_t pf = LOG_N == 14 && ntt_pf() && sms > 0 ? (uint32_t)sms * 2u : 0u;
+    k_ntt_dif<LOG_N, PQ, PAD, LAZY><<<(unsigned)grid, rpc * T, smem, stream>>>(c, data, batch, tw, scale, t2, pf);
+    return launch_status();
+}
+
+template <int LOG_N, bool PQ, bool LAZY>
+static mont_status_t launch_ntt_difp(const Ctx &c, uint32_t *data, size_t batch, const uint32_t *tw, uint32_t scale,
+                                     cudaStream_t stream, Tw2D t2) {
+    constexpr uint32_t N = 1u << LOG_N, T = N >> 5;
+    constexpr uint32_t rpc = T >= 256 ? 1u : 256u / T;
+    const size_t smem = (size_t)rpc * (N + (N >> 5)) * 4;
+    static int resident = 0;  // CTAs per SM, once per instantiation
+    if (resident == 0) {
+        if (smem > 48 * 1024 &&
+            cudaFuncSetAttribute(k_ntt_difp<LOG_N, PQ, LAZY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess)
+            return MONT_ECUDA;
+        int nb = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_ntt_difp<LOG_N, PQ, LAZY>, (int)(rpc * T), smem) !=
+                cudaSuccess ||
+            nb < 1)
+            return MONT_ECUDA;
+        resident = nb;
+        if (getenv("MONT_NTT_DEBUG")) fprintf(stderr, "k_ntt_difp<%d>: %d CTAs/SM\n", LOG_N, nb);
+    }
+    const int sms = sm_count();
+    if (sms <= 0) return MONT_ECUDA;
+    const size_t groups = (batch + rpc - 1) / rpc;
+    size_t grid = (size_t)resident * (size_t)sms;
+    if (grid > groups) grid = groups;
+    k_ntt_difp<LOG_N, PQ, LAZY><<<(unsigned)grid, rpc * T, smem, stream>>>(c, data, batch, tw, scale, t2,
+                                                                          ntt_pf() ? 1u : 0u);
     return launch_status();
 }
 
@@ -544,14 +737,24 @@ static mont_status_t transpose(uint32_t *dst, const uint32_t *src, size_t R, siz
     return launch_status();
 }
 
+// 2^15 rows (one 1024-thread CTA per SM): variants 0 / 3 run the persistent kernel (variants 6 / 7),
+// which hides the next row's HBM loads behind this row's stores (297 -> 275 us REDC, 252 -> 234 us
+// precomputed-quotient for 2048 rows); with 2 or more CTAs per SM the other CTA already covers
+// that phase and the persistent form measured slower (2^14: 222 -> 258 us),
+// profiles/r02_probe_ntt_persistent.jsonl
 #define MONT_NTT_CASE(L)                                                                           \
     case L:                                                                                        \
+        if (L == 15 && (kind == 0 || kind == 3)) kind = kind == 0 ? 6 : 7;                          \
         return kind == 0   ? (lazy ? launch_ntt_dif<L, false, true, true>(c, data, batch, tw, scale, s, t2)   \
                                    : launch_ntt_dif<L, false, true>(c, data, batch, tw, scale, s, t2))      \
                : kind == 3 ? (lazy ? launch_ntt_dif<L, true, true, true>(c, data, batch, tw, scale, s, t2)    \
                                    : launch_ntt_dif<L, true, true>(c, data, batch, tw, scale, s, t2))       \
                : kind == 4 ? launch_ntt_dif<L, false, false>(c, data, batch, tw, scale, s, t2)    \
                : kind == 5 ? launch_ntt_dif<L, true, false>(c, data, batch, tw, scale, s, t2)     \
+               : kind == 6 ? (lazy ? launch_ntt_difp<L, false, true>(c, data, batch, tw, scale, s, t2) \
+                                   : launch_ntt_difp<L, false, false>(c, data, batch, tw, scale, s, t2)) \
+               : kind == 7 ? (lazy ? launch_ntt_difp<L, true, true>(c, data, batch, tw, scale, s, t2) \
+                                   : launch_ntt_difp<L, true, false>(c, data, batch, tw, scale, s, t2)) \
                            : launch_ntt_r32<L>(c, data, batch, tw, scale, s, t2);
 
 // lazy [0, 2P) butterflies when 4P < 2^32 (P < 2^30); MONT_NTT_NO_LAZY=1 turns them off (measurement)
@@ -715,12 +918,12 @@ extern "C" mont_status_t mont_ntt_ex(const mont_ctx_t *ctx, uint32_t *data, size
     if (log_n < 1 || log_n > 15) return MONT_EUNSUPPORTED;
     if (batch == 0) return MONT_OK;
     if (!data || !tw || ((uintptr_t)data & 3u) || ((uintptr_t)tw & 3u) || scale >= ctx->p) return MONT_EINVAL_ARG;
-    if (batch > 0x7fffffffu || variant < 0 || variant > 5) return variant < 0 || variant > 5 ? MONT_EINVAL_ARG
+    if (batch > 0x7fffffffu || variant < 0 || variant > 7) return variant < 0 || variant > 7 ? MONT_EINVAL_ARG
                                                                                              : MONT_EUNSUPPORTED;
-    const bool pair = variant == 3 || variant == 5;
+    const bool pair = variant == 3 || variant == 5 || variant == 7;
     if (pair && ((uintptr_t)tw & 7u)) return MONT_EINVAL_ARG;  // pair table: 8-byte entries
     const uint32_t N = 1u << log_n;
-    if (variant >= 3 && log_n < 5) return MONT_EUNSUPPORTED;
+    if (variant >= 3 && log_n < 5) return MONT_EUNSUPPORTED;  // the 32-per-thread kernels
     if (log_n >= 5 && variant != 2)
         return ntt_rows(to_dev(ctx), data, batch, log_n, tw, scale, stream, Tw2D{nullptr, nullptr, 0, 0, 0, 0},
                         variant);

@@ -344,10 +344,11 @@ if args.what in ("ntt",):
         m.synth_fill(d, 42, 5, 0, P)
         d = d.view(batch, N)
         tw2 = m.ntt_twiddles_pq(ctx, w, log_n)
-        for variant in (0, 1, 3, 4, 5):
-            med, best = timeit(lambda: m.ntt(ctx, d, tw2 if variant in (3, 5) else tw, variant=variant), reps=10)
+        for variant in [int(v) for v in os.environ.get("PROBE_NTT_VARIANTS", "0,1,3,4,5,6,7").split(",")]:
+            med, best = timeit(lambda: m.ntt(ctx, d, tw2 if variant in (3, 5, 7) else tw, variant=variant), reps=10)
             redc = batch * (N // 2) * log_n
-            out(what="ntt", variant={0: "dif", 1: "dit", 3: "dif_pq", 4: "dif_swizzled", 5: "dif_pq_swizzled"}[variant],
+            out(what="ntt", variant={0: "dif", 1: "dit", 3: "dif_pq", 4: "dif_swizzled", 5: "dif_pq_swizzled", 6: "dif_persistent",
+                         7: "dif_pq_persistent"}[variant],
                 log_n=log_n, batch=batch, us=med * 1e6,
                 gbs=8 * batch * N / med / 1e9, tredc=redc / med / 1e12,
                 frac_imad_floor=redc / med / (148 * 64 / 5 * 1.965e9))

@@ -51,6 +51,8 @@ def main():
         "all256u4": {"mul": L(threads=256, unroll=4), "conv": L(threads=256, unroll=4),
                      "tw": L(threads=256, unroll=4, variant=2)},
         "u2c4": {"mul": L(threads=256, unroll=2), "conv": L(threads=256, unroll=4)},
+        "u2c4tma": {"mul": L(threads=256, unroll=2), "conv": L(threads=256, unroll=4), "tw": L(variant=4)},
+        "u2c4tma4k": {"mul": L(threads=256, unroll=2), "conv": L(threads=256, unroll=4), "tw": L(variant=4, chunk=4096)},
         "fp64mul": {"mul": L(threads=256, unroll=2, variant=4), "conv": L(threads=256, unroll=4)},
         "fp64mul512": {"mul": L(threads=512, unroll=2, variant=4), "conv": L(threads=256, unroll=4)},
     }

@@ -35,14 +35,14 @@ def pq_tables(m, ctx, w, winv, log_n):
 
 @pytest.mark.parametrize("P", list(GEN))
 @pytest.mark.parametrize("log_n", [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12])
-@pytest.mark.parametrize("variant", [None, 1, 2, 3, 4, 5])
+@pytest.mark.parametrize("variant", [None, 1, 2, 3, 4, 5, 6, 7])
 def test_ntt_vs_dft(m, P, log_n, variant):
     N = 1 << log_n
     batch = 3
     ctx, w, winv, tw, twi, ninv_m = tables(m, P, N)
-    if variant in (3, 4, 5) and log_n < 5:
-        pytest.skip("variants 3-5 need log_n >= 5")
-    if variant in (3, 5):
+    if variant in (3, 4, 5, 6, 7) and log_n < 5:
+        pytest.skip("variants 3-7 need log_n >= 5")
+    if variant in (3, 5, 7):
         tw, twi = pq_tables(m, ctx, w, winv, log_n)
     x = synth.uniform(42, 21, P, 0, batch * N).reshape(batch, N)
     x[0, :2] = [0, P - 1]
@@ -67,12 +67,45 @@ def test_ntt_full_rows_vs_dft(m, P, log_n):
     x[0, :3] = [P - 1, 0, P - 1]
     x[1, -2:] = [P - 1, P - 1]
     ref = oracle.dft(P, w, x)
-    for variant, (t, ti) in ((None, (tw, twi)), (3, pq_tables(m, ctx, w, winv, log_n))):
+    pq = pq_tables(m, ctx, w, winv, log_n)
+    for variant, (t, ti) in ((None, (tw, twi)), (3, pq), (6, (tw, twi)), (7, pq)):
         d = torch.from_numpy(x).cuda()
         m.ntt(ctx, d, t, variant=variant)
         assert np.array_equal(d.cpu().numpy(), ref), variant
         m.ntt(ctx, d, ti, scale=ninv_m, variant=variant)
         assert np.array_equal(d.cpu().numpy(), x), variant
+
+
+@pytest.mark.parametrize("P", list(GEN))
+@pytest.mark.parametrize("log_n", [5, 8, 10, 12, 13, 14, 15])
+def test_ntt_persistent_rounds(m, P, log_n):
+    """Variants 6 / 7 (persistent grid, next row group's loads issued before this group's stores) on a
+    batch that takes every CTA through several row groups with a ragged last round: bit-exact
+    against variants 0 / 3 (pinned to the definition-DFT above), sampled outputs of the last rows
+    against the DFT evaluated one output at a time, and the inverse round trip."""
+    N = 1 << log_n
+    rows_per_cta = max(1, 256 // (N // 32))
+    batch = (2 * 148 * 2 * 2 + 37) * rows_per_cta + 3 if log_n < 15 else 148 * 3 + 5
+    ctx, w, winv, tw, twi, ninv_m = tables(m, P, N)
+    pq, pqi = pq_tables(m, ctx, w, winv, log_n)
+    x = torch.empty(batch * N, dtype=torch.uint32, device="cuda")
+    m.synth_fill(x, 42, 24 + log_n, 0, P)
+    x = x.view(batch, N)
+    for ref_v, v, t, ti in ((None, 6, tw, twi), (3, 7, pq, pqi)):
+        ref = x.clone()
+        m.ntt(ctx, ref, t, variant=ref_v)
+        d = x.clone()
+        m.ntt(ctx, d, t, variant=v)
+        assert torch.equal(d, ref), v
+        last = [int(u) for u in x[-1].cpu().numpy()]
+        for k in (0, 1, N - 1):
+            wk, acc, pw = pow(w, k, P), 0, 1
+            for u in last:
+                acc = (acc + u * pw) % P
+                pw = pw * wk % P
+            assert int(d[-1, k]) == acc, (v, k)
+        m.ntt(ctx, d, ti, scale=ninv_m, variant=v)
+        assert torch.equal(d, x), v
 
 
 def test_ntt_non_lazy_path(tmp_path):
@@ -109,12 +142,12 @@ sys.exit(0 if ok else 1)
 
 
 @pytest.mark.parametrize("log_n", [13, 14, 15])
-@pytest.mark.parametrize("variant", [None, 1, 3, 4, 5])
+@pytest.mark.parametrize("variant", [None, 1, 3, 4, 5, 6, 7])
 def test_ntt_large_properties(m, log_n, variant):
     P = 998244353
     N = 1 << log_n
     ctx, w, winv, tw, twi, ninv_m = tables(m, P, N)
-    if variant in (3, 5):
+    if variant in (3, 5, 7):
         tw, twi = pq_tables(m, ctx, w, winv, log_n)
     x = synth.uniform(42, 22, P, 0, 2 * N).reshape(2, N)
     d = torch.from_numpy(x).cuda()
