@@ -1344,6 +1344,9 @@ def main():
         "gpu_launches": (len(wl.step_launches) if graph is not None else len(wl.launches)) * args.steps,
         "schedule": ("each step alone between CUDA events after an L2 flush" if wl.kind == "c1" else
                      "serial, one stream" if args.serial else
+                     ("one lane: " + ", ".join(x[0] for x in wl.launches) + " in order on one stream" +
+                      (", replayed as one CUDA graph" if args.graph else ""))
+                     if len({x[4] for x in wl.launches}) < 2 else
                      ("two lanes: the HBM-bound operations as ONE mont_run launch (one flat grid over all their "
                       "tiles, to_mont -> from_mont fused)" if HBM_MODE == "run" else
                       "two lanes: the HBM-bound launches in order on one stream (mul_vec+checksum 256 threads x 2 "
