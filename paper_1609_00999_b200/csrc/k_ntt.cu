@@ -237,7 +237,9 @@ __device__ __forceinline__ void dif_trip(const Ctx &c, uint32_t (&v)[32], const 
             } else {
                 v[k0] = mod_add(a, d, c.p);
             }
-            if (wlo == 0 && j == 0) {  // twiddle w^0 = 1: no product (see k_ntt_dif)
+            if (wlo == 0 && j == 0) {
+                // pos = 0 (tl is empty when wlo = 0): the twiddle is w^0 = 1, so the product is
+                // skipped (a compile-time decision; 30 of the last trip's 64 butterflies at 2^14)
                 if (LAZY) {
                     const uint32_t x = a - d + p2;
                     v[k1] = umin(x, x - p2);
@@ -246,16 +248,20 @@ __device__ __forceinline__ void dif_trip(const Ctx &c, uint32_t (&v)[32], const 
                 }
             } else if (PQ) {
                 const uint2 wq = __ldg(reinterpret_cast<const uint2 *>(tw) + ((1u << b) - 1u) + tl + (j << wlo));
-                const uint32_t x = a - d + (LAZY ? p2 : c.p);
-                const uint32_t qq = __umulhi(x, wq.y);
-                const uint32_t r = x * wq.x - qq * c.p;
+                const uint32_t x = a - d + (LAZY ? p2 : c.p);  // (0, 2P) or (0, 4P): any x < 2^32 is allowed
+                const uint32_t qq = __umulhi(x, wq.y);         // floor(x w' / 2^32)
+                const uint32_t r = x * wq.x - qq * c.p;        // x w - q P in [0, 2P), exact mod 2^32
                 v[k1] = LAZY ? r : umin(r, r - c.p);
             } else if (LAZY) {
+                // (a - d + 2P) w < 4P P < 2^32 P: REDC's precondition holds; keep t' + P in (0, 2P)
                 const uint64_t T = mul_wide_u32(a - d + p2, __ldg(twb + (j << wlo)));
                 const uint32_t m = (uint32_t)T * c.pinv;
                 v[k1] = hi32(T) - hi32(mul_wide_u32(m, c.p)) + c.p;
             } else {
-                v[k1] = redc(a - d + c.p, __ldg(twb + (j << wlo)), c.p, c.pinv);
+                // REDC needs only (a - d) w < 2^32 P, so a - d + P in (0, 2P) goes in unreduced:
+                // the subtraction's correction is folded into the multiply
+                const uint32_t w = __ldg(twb + (j << wlo));
+                v[k1] = redc(a - d + c.p, w, c.p, c.pinv);
             }
         }
     }
@@ -375,52 +381,7 @@ __global__ void __launch_bounds__(LOG_N == 15 ? 1024 : 512, LOG_N == 15 ? 1 : 2)
 #pragma unroll
             for (int k = 0; k < 32; ++k) v[k] = s[lay_comb<PAD>(sb, lay<PAD>((uint32_t)k << wlo))];
         }
-#pragma unroll
-        for (int lb = 4; lb >= 0; --lb) {
-            const int b = wlo + lb;                     // pair distance 2^b
-            if (b >= top) continue;                     // done by an earlier trip
-            const uint32_t *twb = tw + ((1u << b) - 1u) + tl;
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                const int k0 = ((q >> lb) << (lb + 1)) | (q & ((1 << lb) - 1));
-                const int k1 = k0 | (1 << lb);
-                const uint32_t j = (uint32_t)(k0 & ((1 << lb) - 1));
-                const uint32_t a = v[k0], d = v[k1];
-                const uint32_t p2 = 2u * c.p;
-                if (LAZY) {
-                    const uint32_t sum = a + d;                  // [0, 4P)
-                    v[k0] = umin(sum, sum - p2);                 // [0, 2P)
-                } else {
-                    v[k0] = mod_add(a, d, c.p);
-                }
-                if (wlo == 0 && j == 0) {
-                    // pos = 0 (tl is empty when wlo = 0): the twiddle is w^0 = 1, so the product is
-                    // skipped (a compile-time decision; 30 of the last trip's 64 butterflies at 2^14)
-                    if (LAZY) {
-                        const uint32_t x = a - d + p2;           // (0, 4P)
-                        v[k1] = umin(x, x - p2);
-                    } else {
-                        v[k1] = mod_sub(a, d, c.p);
-                    }
-                } else if (PQ) {
-                    const uint2 wq = __ldg(reinterpret_cast<const uint2 *>(tw) + ((1u << b) - 1u) + tl + (j << wlo));
-                    const uint32_t x = a - d + (LAZY ? p2 : c.p);  // (0, 2P) or (0, 4P): any x < 2^32 is allowed
-                    const uint32_t q = __umulhi(x, wq.y);     // floor(x w' / 2^32)
-                    const uint32_t r = x * wq.x - q * c.p;    // x w - q P in [0, 2P), exact mod 2^32
-                    v[k1] = LAZY ? r : umin(r, r - c.p);
-                } else if (LAZY) {
-                    // (a - d + 2P) w < 4P P < 2^32 P: REDC's precondition holds; keep t' + P in (0, 2P)
-                    const uint64_t T = mul_wide_u32(a - d + p2, __ldg(twb + (j << wlo)));
-                    const uint32_t m = (uint32_t)T * c.pinv;
-                    v[k1] = hi32(T) - hi32(mul_wide_u32(m, c.p)) + c.p;
-                } else {
-                    const uint32_t w = __ldg(twb + (j << wlo));
-                    // REDC needs only (a - d) w < 2^32 P, so a - d + P in (0, 2P) goes in unreduced:
-                    // the subtraction's correction is folded into the multiply
-                    v[k1] = redc(a - d + c.p, w, c.p, c.pinv);
-                }
-            }
-        }
+        dif_trip<LOG_N, PQ, LAZY>(c, v, top, wlo, tl, tw);
         if (PAD && trip == NTRIP - 1) {
             // last trip: the transform's outputs are in bit-reversed order; store each at its
             // natural index brev(pos) (other threads' words: everyone must have loaded first)
