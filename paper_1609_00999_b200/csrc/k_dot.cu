@@ -9,6 +9,7 @@
 #include "../../include/mont_dot.h"
 #include "../../include/mont_ext.h"
 #include "abi_util.h"
+#include "tma.cuh"
 
 namespace mont {
 
@@ -213,6 +214,82 @@ __global__ void __launch_bounds__(256) k_dot_split(Ctx c, uint32_t *out, const u
     }
 }
 
+
+// Copy-engine streaming (variant 8): a persistent grid (ctas_per_sm x SMs CTAs of 256 threads);
+// CTA b owns rows b, b + G, b + 2G, ... (G = gridDim.x) and streams them as tiles of tile4 uint4
+// through an S-stage shared-memory ring filled by cp.async.bulk (one mbarrier per stage,
+// transaction-byte completion): each stage holds a tile of A and the matching tile of x, so S
+// tiles are always in flight whatever the warps are doing and x never competes with the ring for
+// L1.  The partial sum of a row is reduced across the CTA when its last tile has been consumed
+// (part[] double-buffered by row parity).
+template <int S>
+__global__ void __launch_bounds__(256) k_dot_pipe(Ctx c, uint32_t *out, const uint32_t *A, const uint32_t *x,
+                                                   size_t batch, size_t len, uint32_t tile4) {
+    extern __shared__ __align__(128) uint4 ring[];  // [S][2][tile4]: A tile, x tile
+    __shared__ __align__(8) uint64_t full[S];
+    __shared__ long long part[2][8];
+    const size_t n4 = len >> 2;
+    const uint32_t tpr = (uint32_t)((n4 + tile4 - 1) / tile4);  // tiles per row
+    const size_t mine = batch > blockIdx.x ? (batch - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const size_t ntiles = mine * tpr;
+    // producer cursor (thread 0): the (row, tile) of the next load, advanced without divisions
+    uint32_t pk = 0, prow = 0;
+    auto load_next = [&](int st) {
+        const size_t row = blockIdx.x + (size_t)prow * gridDim.x;
+        const size_t c0 = (size_t)pk * tile4;
+        const uint32_t cnt = (uint32_t)(n4 - c0 < tile4 ? n4 - c0 : tile4);
+        mbar_expect_tx(&full[st], cnt * 32u);
+        bulk_g2s(ring + (size_t)st * 2 * tile4, reinterpret_cast<const uint4 *>(A + row * len) + c0, cnt * 16u,
+                 &full[st]);
+        bulk_g2s(ring + ((size_t)st * 2 + 1) * tile4, reinterpret_cast<const uint4 *>(x) + c0, cnt * 16u, &full[st]);
+        if (++pk == tpr) pk = 0, ++prow;
+    };
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < S; ++st) mbar_init(&full[st], 1);
+        fence_mbar_init();
+        for (int st = 0; st < S; ++st)
+            if ((size_t)st < ntiles) load_next(st);
+    }
+    __syncthreads();
+    const int32_t p = (int32_t)c.p, pinv = (int32_t)c.pinv;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    long long s = 0;
+    uint32_t kin = 0, rk = 0, st = 0, phase = 0;  // consumer cursor
+    for (size_t k = 0; k < ntiles; ++k) {
+        const size_t c0 = (size_t)kin * tile4;
+        const uint32_t cnt = (uint32_t)(n4 - c0 < tile4 ? n4 - c0 : tile4);
+        mbar_wait(&full[st], phase);
+        const uint4 *ta = ring + (size_t)st * 2 * tile4, *tx = ta + tile4;
+        for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+            const uint4 a = ta[i], b = tx[i];
+            s += (long long)sredc((int32_t)a.x, (int32_t)b.x, p, pinv) + (long long)sredc((int32_t)a.y, (int32_t)b.y, p, pinv) +
+                 (long long)sredc((int32_t)a.z, (int32_t)b.z, p, pinv) + (long long)sredc((int32_t)a.w, (int32_t)b.w, p, pinv);
+        }
+        const bool row_end = kin == tpr - 1;
+        if (row_end) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+            if (lane == 0) part[rk & 1][wid] = s;
+            s = 0;
+        }
+        __syncthreads();  // stage st consumed by everyone (and part[] written)
+        if (threadIdx.x == 0 && k + S < ntiles) load_next((int)st);
+        if (row_end && wid == 0) {
+            long long r = lane < (int)(blockDim.x >> 5) ? part[rk & 1][lane] : 0ll;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
+            if (lane == 0) {
+                r %= (long long)c.p;  // the single reduction of the row
+                if (r < 0) r += c.p;
+                out[blockIdx.x + (size_t)rk * gridDim.x] = (uint32_t)r;
+            }
+        }
+        if (row_end) kin = 0, ++rk;
+        else ++kin;
+        if (++st == S) st = 0, phase ^= 1u;
+    }
+}
+
 }  // namespace mont
 
 using namespace mont;
@@ -226,8 +303,29 @@ extern "C" mont_status_t mont_dot_ex(const mont_ctx_t *ctx, uint32_t *out, const
     if (batch > 0x7fffffffu) return MONT_EUNSUPPORTED;
     const int variant = cfg ? cfg->variant : 0;
     const int chunk_req = cfg ? cfg->chunk : 0;
-    if (variant < 0 || variant > 7 || chunk_req < 0 || (chunk_req % 1024) != 0) return MONT_EINVAL_ARG;
+    if (variant < 0 || variant > 8 || chunk_req < 0 || (chunk_req % 1024) != 0) return MONT_EINVAL_ARG;
     const bool vec = (len % 4 == 0) && (((uintptr_t)A | (uintptr_t)x) & 15u) == 0;
+    if (variant == 8 && vec) {
+        const int stages = cfg && cfg->unroll ? cfg->unroll : 4;
+        const int k = cfg && cfg->ctas_per_sm ? cfg->ctas_per_sm : 2;
+        const uint32_t tile4 = (chunk_req ? (uint32_t)chunk_req : 4096u) / 4u;
+        if ((stages != 2 && stages != 4 && stages != 8) || k < 1 || k > 8) return MONT_EINVAL_ARG;
+        const size_t smem = (size_t)stages * tile4 * 32;
+        if (smem > 200 * 1024) return MONT_EINVAL_ARG;
+        const int sms = sm_count();
+        if (sms <= 0) return MONT_ECUDA;
+        size_t grid = (size_t)sms * k;
+        if (grid > batch) grid = batch;
+        const Ctx c = to_dev(ctx);
+#define MONT_DOT_PIPE(SS)                                                                                       \
+    if (smem > 48 * 1024 &&                                                                                     \
+        cudaFuncSetAttribute(k_dot_pipe<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) \
+        return MONT_ECUDA;                                                                                      \
+    k_dot_pipe<SS><<<(unsigned)grid, 256, smem, stream>>>(c, out, A, x, batch, len, tile4);
+        if (stages == 2) { MONT_DOT_PIPE(2) } else if (stages == 4) { MONT_DOT_PIPE(4) } else { MONT_DOT_PIPE(8) }
+#undef MONT_DOT_PIPE
+        return launch_status();
+    }
     const uint32_t chunk = chunk_req ? (uint32_t)chunk_req : 4096u;  // 4 uint4 per thread of 256
     const size_t S = (len + chunk - 1) / chunk;
     if (variant == 5 && vec && S >= 2 && batch * S <= 0x7fffffffu) {
@@ -245,7 +343,7 @@ extern "C" mont_status_t mont_dot_ex(const mont_ctx_t *ctx, uint32_t *out, const
         case 2: k_dot<8, false><<<(unsigned)batch, 256, 0, stream>>>(c, out, A, x, len, vec); break;
         case 3: k_dot<4, true><<<(unsigned)batch, 256, 0, stream>>>(c, out, A, x, len, vec); break;
         case 4: k_dot<8, true><<<(unsigned)batch, 256, 0, stream>>>(c, out, A, x, len, vec); break;
-        default: k_dot<4, false><<<(unsigned)batch, 256, 0, stream>>>(c, out, A, x, len, vec); break;  // 0, 1, 5-7
+        default: k_dot<4, false><<<(unsigned)batch, 256, 0, stream>>>(c, out, A, x, len, vec); break;  // 0, 1, 5-8
     }
     return launch_status();
 }

@@ -396,7 +396,11 @@ if args.what in ("dot",):
                       ("8 uint4 (variant 2)", m.Launch(variant=2)), ("4 uint4 prefetched (variant 3)", m.Launch(variant=3)),
                       ("8 uint4 prefetched (variant 4)", m.Launch(variant=4)),
                       ("split 4096 (variant 5)", m.Launch(variant=5)), ("split 8192", m.Launch(variant=5, chunk=8192)),
-                      ("2 rows per CTA (variant 6)", m.Launch(variant=6)), ("4 rows per CTA (variant 7)", m.Launch(variant=7))):
+                      ("2 rows per CTA (variant 6)", m.Launch(variant=6)), ("4 rows per CTA (variant 7)", m.Launch(variant=7)),
+                      *[(f"bulk-copy ring (variant 8) stages={st} ctas/SM={k} tile={ch}",
+                         m.Launch(variant=8, unroll=st, ctas_per_sm=k, chunk=ch))
+                        for st, k, ch in ((2, 2, 4096), (4, 1, 4096), (2, 1, 8192), (2, 3, 4096), (4, 2, 2048),
+                                          (2, 4, 2048), (8, 1, 2048))]):
         med, _ = timeit(lambda: m.dot(ctx, A, x, out=o, cfg=cfg))
         same = bool((o.view(torch.int32) == ref.view(torch.int32)).all())
         out(what="dot", launch=name, us=med * 1e6, gbs=4 * batch * L / med / 1e9, gmulmod=batch * L / med / 1e9,

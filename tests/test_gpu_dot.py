@@ -39,7 +39,8 @@ def test_dot_misaligned_and_extremes(m):
 
 
 @pytest.mark.parametrize("P", [2013265921, 469762049, 3, 2147483647])
-@pytest.mark.parametrize("cfg", [None, (1, 0), (2, 0), (3, 0), (4, 0), (5, 1024), (5, 2048), (5, 0), (5, 8192), (6, 0), (7, 0)])
+@pytest.mark.parametrize("cfg", [None, (1, 0), (2, 0), (3, 0), (4, 0), (5, 1024), (5, 2048), (5, 0), (5, 8192), (6, 0), (7, 0),
+                                 (8, 0), (8, 1024), (8, 8192)])
 @pytest.mark.parametrize("batch,L", [(3, 8192), (5, 16384), (2, 16384 + 1028), (7, 40000), (1, 1 << 20)])
 def test_dot_split_rows(m, P, cfg, batch, L):
     """The split-row path (chunks per CTA, canonical partials added into out by modular CAS) and
@@ -58,6 +59,34 @@ def test_dot_ex_rejects(m):
     ctx = m.ctx_init(2013265921)
     A = torch.zeros((2, 8192), dtype=torch.int32, device="cuda").view(torch.uint32)
     x = torch.zeros(8192, dtype=torch.int32, device="cuda").view(torch.uint32)
-    for cfg in (m.Launch(variant=8), m.Launch(chunk=1000)):
+    for cfg in (m.Launch(variant=9), m.Launch(chunk=1000), m.Launch(variant=8, unroll=3),
+                m.Launch(variant=8, ctas_per_sm=9), m.Launch(variant=8, chunk=1 << 20)):
         with pytest.raises(m.MontError):
             m.dot(ctx, A, x, cfg=cfg)
+
+
+@pytest.mark.parametrize("P", [2013265921, 998244353])
+@pytest.mark.parametrize("stages,ctas,chunk", [(4, 2, 0), (2, 1, 1024), (8, 1, 4096), (8, 4, 2048), (4, 8, 1024)])
+@pytest.mark.parametrize("batch,L", [(700, 4096), (301, 16384 + 1028), (1500, 12)])
+def test_dot_pipe_many_rows(m, P, stages, ctas, chunk, batch, L):
+    """Variant 8 (persistent CTAs streaming their rows through a bulk-copy ring): batches larger
+    than the grid, so every CTA runs several rows (and its ring wraps many times), ragged last
+    tiles, rows shorter than one tile; against the oracle's definition."""
+    A = synth.uniform(42, 35, P, 0, batch * L).reshape(batch, L)
+    x = synth.uniform(42, 36, P, 0, L)
+    A[-1, :] = P - 1
+    x[:] = np.where(np.arange(L) % 5 == 0, P - 1, x)
+    out = torch.full((batch,), 7, dtype=torch.int32, device="cuda").view(torch.uint32)
+    m.dot(m.ctx_init(P), torch.from_numpy(A).cuda(), torch.from_numpy(x).cuda(), out=out,
+          cfg=m.Launch(variant=8, unroll=stages, ctas_per_sm=ctas, chunk=chunk))
+    assert np.array_equal(out.cpu().numpy(), oracle.dot(P, A, x))
+
+
+def test_dot_pipe_misaligned_falls_back(m):
+    """Variant 8 needs 16-byte rows and operands; otherwise the one-CTA-per-row kernel runs."""
+    P = 2013265921
+    L = 1001
+    A = synth.uniform(42, 37, P, 0, 4 * L).reshape(4, L)
+    x = synth.uniform(42, 38, P, 0, L)
+    out = m.dot(m.ctx_init(P), torch.from_numpy(A).cuda(), torch.from_numpy(x).cuda(), cfg=m.Launch(variant=8))
+    assert np.array_equal(out.cpu().numpy(), oracle.dot(P, A, x))
