@@ -34,7 +34,8 @@ mont_status_t mont_dot(const mont_ctx_t *ctx, uint32_t *out, const uint32_t *A, 
  * zeroes out (out must not overlap A or x); 6 / 7 = 2 / 4 rows per CTA
  * against one load of x (len % 4 == 0, 16-byte aligned A and x, else 1);
  * 8 = a persistent grid (cfg->ctas_per_sm x SMs CTAs, 0 = 2) streaming each
- * CTA's rows through a cfg->unroll-stage (2, 4 or 8; 0 = 4) shared-memory
+ * CTA's rows through a cfg->unroll-stage (2, 4 or 8; 0 = 4, or 2 if 4 do
+ * not fit) shared-memory
  * ring of cfg->chunk-element tiles of A and x (0 = 4096) filled by bulk
  * copies (len % 4 == 0, 16-byte aligned A and x, else 1; at most 200 KiB of
  * ring).  cfg may be NULL.  Errors as mont_dot, plus MONT_EINVAL_ARG for

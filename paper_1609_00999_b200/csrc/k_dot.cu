@@ -306,9 +306,10 @@ extern "C" mont_status_t mont_dot_ex(const mont_ctx_t *ctx, uint32_t *out, const
     if (variant < 0 || variant > 8 || chunk_req < 0 || (chunk_req % 1024) != 0) return MONT_EINVAL_ARG;
     const bool vec = (len % 4 == 0) && (((uintptr_t)A | (uintptr_t)x) & 15u) == 0;
     if (variant == 8 && vec) {
-        const int stages = cfg && cfg->unroll ? cfg->unroll : 4;
         const int k = cfg && cfg->ctas_per_sm ? cfg->ctas_per_sm : 2;
         const uint32_t tile4 = (chunk_req ? (uint32_t)chunk_req : 4096u) / 4u;
+        // default stage count: 4, or 2 where 4 would not fit
+        const int stages = cfg && cfg->unroll ? cfg->unroll : ((size_t)4 * tile4 * 32 <= 200 * 1024 ? 4 : 2);
         if ((stages != 2 && stages != 4 && stages != 8) || k < 1 || k > 8) return MONT_EINVAL_ARG;
         const size_t smem = (size_t)stages * tile4 * 32;
         if (smem > 200 * 1024) return MONT_EINVAL_ARG;

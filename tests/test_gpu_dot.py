@@ -66,7 +66,7 @@ def test_dot_ex_rejects(m):
 
 
 @pytest.mark.parametrize("P", [2013265921, 998244353])
-@pytest.mark.parametrize("stages,ctas,chunk", [(4, 2, 0), (2, 1, 1024), (8, 1, 4096), (8, 4, 2048), (4, 8, 1024)])
+@pytest.mark.parametrize("stages,ctas,chunk", [(4, 2, 0), (2, 1, 1024), (8, 1, 2048), (8, 4, 2048), (4, 8, 1024), (2, 3, 4096)])
 @pytest.mark.parametrize("batch,L", [(700, 4096), (301, 16384 + 1028), (1500, 12)])
 def test_dot_pipe_many_rows(m, P, stages, ctas, chunk, batch, L):
     """Variant 8 (persistent CTAs streaming their rows through a bulk-copy ring): batches larger
