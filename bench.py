@@ -1408,12 +1408,11 @@ def main_reference(args, rank, world):
         return
     kind = args.workload
     v0, cores, sample, secs, frac = cpu_baseline(kind, target_s=1.0)
-    times, mm_step = [], None
-    import numpy as np  # noqa: F401
+    plan, cores = _ref_plan(kind, frac)
+    sample = f"{frac:.4g} of the {kind} workload (inputs generated once, outside the timed calls)"
+    times = []
     for i in range(max(0, args.warmup) + args.steps):
-        t0 = time.perf_counter()
-        v, cores, sample, secs, frac2 = _ref_step(kind, frac)
-        t = time.perf_counter() - t0
+        v, secs = _ref_step(plan)
         if i >= args.warmup:
             times.append((secs, v))
     tot_s = sum(s for s, _ in times)
@@ -1430,8 +1429,9 @@ def main_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def _ref_step(kind, frac):
-    """One reference step = the oracle over the fixed bounded sample."""
+def _ref_plan(kind, frac):
+    """The reference arm's bounded sample, generated ONCE (host-side synth/, untimed): a list of
+    (oracle call, mulmods) that every reference step then runs and times."""
     import numpy as np
 
     import oracle
@@ -1440,50 +1440,47 @@ def _ref_step(kind, frac):
     n2 = max(4, int(N_C2 * frac))
     n4 = max(4, int(N_C4 * frac))
     rows = max(1, int(TW_BATCH * frac))
-    t_total, mm = 0.0, 0
+    plan = []
     if kind == "c1":
         a, b = synth.c1_inputs(P0)
         reps = max(1, int(frac * 1024))
-        t0 = time.perf_counter()
-        for _ in range(reps):
-            oracle.mont_mul(P0, a, b, nthreads=cores)
-        t_total += time.perf_counter() - t0
-        mm += a.size * reps
+
+        def c1_calls(a=a, b=b, reps=reps):
+            for _ in range(reps):
+                oracle.mont_mul(P0, a, b, nthreads=cores)
+        plan.append((c1_calls, a.size * reps))
     if kind in ("step", "c2", "c5"):
         for P in (PRIMES if kind != "c5" else (P0,)):
             a, b = synth.c2_inputs(P, 0, n2)
-            t0 = time.perf_counter()
-            c = oracle.mont_mul(P, a, b, nthreads=cores)
-            oracle.checksum(P, c, nthreads=cores)
-            t_total += time.perf_counter() - t0
-            mm += n2
+            plan.append((lambda P=P, a=a, b=b: oracle.checksum(P, oracle.mont_mul(P, a, b, nthreads=cores),
+                                                               nthreads=cores), n2))
     if kind == "step":
         a, _ = synth.c2_inputs(P0, 0, n2)
-        t0 = time.perf_counter()
-        oracle.from_mont(P0, oracle.to_mont(P0, a, nthreads=cores), nthreads=cores)
-        t_total += time.perf_counter() - t0
-        mm += 2 * n2
+        plan.append((lambda a=a: oracle.from_mont(P0, oracle.to_mont(P0, a, nthreads=cores), nthreads=cores), 2 * n2))
     if kind in ("step", "c3"):
         x = synth.c3_x(P0, batch=rows, length=TW_LEN)
         tw = oracle.twiddle_table(P0, oracle.root_of_unity(P0, G11_GENERATOR, TW_LEN), TW_LEN)
-        t0 = time.perf_counter()
-        oracle.twiddle(P0, x, tw, nthreads=cores)
-        t_total += time.perf_counter() - t0
-        mm += rows * TW_LEN
+        plan.append((lambda x=x, tw=tw: oracle.twiddle(P0, x, tw, nthreads=cores), rows * TW_LEN))
     if kind in ("step", "c4"):
         base, e = synth.c4_inputs(P1, 0, n4)
-        t0 = time.perf_counter()
-        oracle.power(P1, base, e, nthreads=cores)
-        t_total += time.perf_counter() - t0
-        mm += 31 * n4 + int(np.unpackbits(e.view(np.uint8)).sum())
+        plan.append((lambda base=base, e=e: oracle.power(P1, base, e, nthreads=cores),
+                     31 * n4 + int(np.unpackbits(e.view(np.uint8)).sum())))
     if kind == "ntt":
         x = synth.c3_x(P0, batch=1, length=TW_LEN)
         w = oracle.root_of_unity(P0, G11_GENERATOR, TW_LEN)
+        plan.append((lambda x=x, w=w: oracle.dft(P0, w, x), (TW_LEN // 2) * 14))
+    return plan, cores
+
+
+def _ref_step(plan):
+    """One reference step = the oracle over the fixed bounded sample (inputs already generated)."""
+    t_total, mm = 0.0, 0
+    for fn, mulmods in plan:
         t0 = time.perf_counter()
-        oracle.dft(P0, w, x)
+        fn()
         t_total += time.perf_counter() - t0
-        mm += (TW_LEN // 2) * 14
-    return mm / t_total / 1e9, cores, f"{frac:.4g} of the {kind} workload", t_total, frac
+        mm += mulmods
+    return mm / t_total / 1e9, t_total
 
 
 if __name__ == "__main__":
