@@ -20,7 +20,8 @@ extern "C" {
  *   ctas_per_sm: CTAs per SM for the persistent grid (grid = SMs * ctas_per_sm)
  *   unroll    : 128-bit chunks per thread per loop trip (1, 2, 4 or 8)
  *   variant   : kernel variant (kernel-specific; 0 = the library default, which
- *               for every kernel but mont_mul_twiddle_ex is variant 0 itself).
+ *               is variant 0 itself except for mont_pow_vec_ex and
+ *               mont_mul_twiddle_ex, where 0 selects another variant below).
  *                 mont_mul_vec_ex, mont_mul_vec_checksum_ex, to_mont_ex,
  *                 from_mont_ex, mb_triad, mb_copy : 0 = flat grid (one
  *                                   tile of threads*unroll uint4 per CTA),

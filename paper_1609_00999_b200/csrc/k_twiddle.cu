@@ -2,15 +2,17 @@
 // (BASELINE configs[2]: batch 4096 x len 2^14, the
 // twiddle multiply of one NTT stage of the paper's modular FFTs).
 //
-// B200 design, three table paths, all measured:
-//  * variant 2 (default for power-of-two rows): the batch as one flat 128-bit
-//    stream, table quads read through the read-only path where the 64 KiB
-//    table stays L1-resident per SM;
-//  * variant 0 (other row lengths): a 2-D grid, blockIdx.x = a column chunk of
-//    the table, blockIdx.y = a block of rows; each CTA stages its chunk ONCE
-//    into shared memory with the bulk-copy engine (cp.async.bulk, completion
-//    counted on an mbarrier by transaction bytes -- the TMA path, SASS UBLKCP)
-//    and reads it with conflict-free LDS.128;
+// B200 design, table paths, all measured:
+//  * variant 4 (the library default, variant 0, since round 2): a 2-D grid,
+//    blockIdx.x = a column chunk of the table, blockIdx.y = a block of rows;
+//    each CTA stages its chunk ONCE into shared memory with the bulk-copy
+//    engine (cp.async.bulk, completion counted on an mbarrier by transaction
+//    bytes -- the TMA path, SASS UBLKCP) and reads it with conflict-free
+//    LDS.128 (alone it ties variant 2; inside bench.py's two-lane step it is
+//    faster);
+//  * variant 2 (power-of-two rows): the batch as one flat 128-bit stream,
+//    table quads read through the read-only path where the 64 KiB table
+//    stays L1-resident per SM; variant 1: the 2-D grid with the table via L1;
 //  * variant 3: the whole table staged once per CTA lifetime plus cluster
 //    launch control work stealing.
 // HBM traffic is the 8 B/elem of x and out in every case.
