@@ -257,3 +257,48 @@ def test_bench_hbm_launch_shapes_fullsize(m):
     ha, hb = synth.c2_inputs_at(P0, idx.astype(np.uint64))
     assert np.array_equal(c.cpu().numpy()[idx], oracle.mont_mul(P0, ha, hb))
     assert np.array_equal(t.cpu().numpy()[idx], oracle.to_mont(P0, ha))
+
+
+def test_beyond_2_32_elements(m):
+    """Maximum sizes: n = 2^32 + 1029 (more elements than a 32-bit count holds, and a misaligned
+    head and ragged tail at offsets past 2^32) through mont_mul_vec_checksum, to_mont / from_mont
+    and mont_pow_vec: the Montgomery identity and canonical range on every element, the round
+    trip on every element, the checksum against a torch reduction, and samples around index 2^32
+    against the oracle / Python pow."""
+    n = (1 << 32) + 1029
+    free, _ = torch.cuda.mem_get_info()
+    if free < 4 * 4 * n + (8 << 30):
+        pytest.skip("not enough device memory for 4 x 16 GiB")
+    ctx = m.ctx_init(P0)
+    buf = gen(n + 1, 1, P0, m=m)
+    a = buf[1:]                                   # 4-byte aligned, not 16: the head is peeled
+    b = gen(n, 2, P0, m=m)
+    c, acc = m.mul_vec_checksum(ctx, a, b)
+    torch.cuda.synchronize()
+    assert identity_all(P0, a, b, c, chunk=1 << 27)
+    tot = 0
+    for s in range(0, n, 1 << 28):
+        tot += int(i64(c[s:s + (1 << 28)]).sum().item())
+    assert int(acc.item()) == tot
+    idx = np.unique(np.concatenate([np.arange(8), np.arange((1 << 32) - 8, (1 << 32) + 8), np.arange(n - 8, n),
+                                    np.random.default_rng(1).integers(0, n, 2000)])).astype(np.int64)
+    ia = torch.from_numpy(idx).cuda()
+    ha, hb = (a.view(torch.int32)[ia].cpu().numpy().view(np.uint32), b.view(torch.int32)[ia].cpu().numpy().view(np.uint32))
+    assert np.array_equal(c.view(torch.int32)[ia].cpu().numpy().view(np.uint32), oracle.mont_mul(P0, ha, hb))
+    del c
+    # conversions: to_mont into b's storage (b is no longer needed), then back into a fresh buffer
+    tm = m.to_mont(ctx, a, out=b)
+    back = m.from_mont(ctx, tm)
+    for s in range(0, n, 1 << 28):
+        assert bool((a[s:s + (1 << 28)].view(torch.int32) == back[s:s + (1 << 28)].view(torch.int32)).all())
+    assert np.array_equal(tm.view(torch.int32)[ia].cpu().numpy().view(np.uint32), oracle.to_mont(P0, ha))
+    del back, tm
+    # pow: exponents from the generator, results sampled around 2^32 against Python's pow
+    e = gen(n, 4, P0, mode=2, m=m)
+    out = m.pow_vec(ctx, a, e, out=b)
+    torch.cuda.synchronize()
+    he = e.view(torch.int32)[ia].cpu().numpy().view(np.uint32)
+    got = out.view(torch.int32)[ia].cpu().numpy().view(np.uint32)
+    assert all(int(g) == pow(int(x), int(y), P0) for g, x, y in zip(got, ha, he))
+    del a, b, e, out, buf
+    torch.cuda.empty_cache()
