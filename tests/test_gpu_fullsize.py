@@ -302,3 +302,55 @@ def test_beyond_2_32_elements(m):
     assert all(int(g) == pow(int(x), int(y), P0) for g, x, y in zip(got, ha, he))
     del a, b, e, out, buf
     torch.cuda.empty_cache()
+
+
+def test_twiddle_ntt_run_beyond_2_32_elements(m):
+    """Maximum sizes for the batched forms: 2^18 + 3 rows of 2^14 (4.3 G elements, row offsets
+    past 2^32) through mont_mul_twiddle (the TMA-staged default), one mont_run launch and the
+    default NTT rows: the Montgomery identity of every twiddle product, the inverse-NTT round trip
+    of every element, and NTT outputs of the last rows against the DFT evaluated one output at a
+    time."""
+    batch, L = (1 << 18) + 3, 1 << 14
+    n = batch * L
+    free, _ = torch.cuda.mem_get_info()
+    if free < 3 * 4 * n + (8 << 30):
+        pytest.skip("not enough device memory for 3 x 16 GiB")
+    ctx = m.ctx_init(P0)
+    w = oracle.root_of_unity(P0, 31, L)
+    tw = m.twiddle_table(ctx, w, L)
+    x = gen(n, 5, P0, m=m).view(batch, L)
+    out = m.mul_twiddle(ctx, x, tw)
+    torch.cuda.synchronize()
+    t64 = i64(tw)
+    rows = 1 << 12
+    for r in range(0, batch, rows):
+        xx, oo = i64(x[r:r + rows]), i64(out[r:r + rows])
+        assert bool(((oo << 32) % P0 == (xx * t64) % P0).all()) and bool((oo < P0).all()), r
+    # the same product as one mont_run job (out overwritten), bit-identical
+    ref_last = out[-2:].clone()
+    out.zero_()
+    m.run([m.run_job("twiddle", ctx, out.view(-1), x.view(-1), tw)])
+    assert torch.equal(out[-2:], ref_last)
+    assert bool((out[:2].view(torch.int32) != 0).any())
+    del out, ref_last
+    torch.cuda.empty_cache()
+    # NTT rows in place, then the inverse with the 1/N scale: back to x on every element
+    x0 = x.clone()
+    twn = m.ntt_twiddles(ctx, w, 14)
+    winv = oracle.inverse(w, P0)
+    twi = m.ntt_twiddles(ctx, winv, 14)
+    ninv_m = int(oracle.to_mont(P0, np.array([oracle.inverse(L, P0)], np.uint32))[0])
+    m.ntt(ctx, x, twn)
+    torch.cuda.synchronize()
+    last = [int(v) for v in x0[-1].cpu().numpy()]
+    for k in (0, 1, L - 1, 12345):
+        wk, acc, pw = pow(w, k, P0), 0, 1
+        for v in last:
+            acc = (acc + v * pw) % P0
+            pw = pw * wk % P0
+        assert int(x[-1, k]) == acc, k
+    m.ntt(ctx, x, twi, scale=ninv_m)
+    for r in range(0, batch, rows):
+        assert torch.equal(x[r:r + rows], x0[r:r + rows]), r
+    del x, x0
+    torch.cuda.empty_cache()
