@@ -77,6 +77,9 @@ HBM_MODE = os.environ.get("MONT_HBM_MODE", "pair")
 # tile shape of that mont_run launch inside the step (threads, uint4 per thread): 256-thread tiles
 # leave the co-running pow grid the room 512-thread ones take (profiles/r02_step_sweep.jsonl)
 RUN_SHAPE = tuple(int(v) for v in os.environ.get("MONT_RUN_SHAPE", "512,2").split(","))
+# programmatic dependent launch inside the HBM lane: every HBM launch after the lane's first may
+# start while the previous one drains (MONT_LAUNCH_OVERLAP_PREV; the lane's launches are independent)
+PDL = os.environ.get("MONT_PDL", "1") == "1"
 # streams the HBM-bound launches are spread over inside the step (independent launches only)
 HBM_STREAMS = int(os.environ.get("MONT_HBM_STREAMS", "1"))
 
@@ -219,6 +222,11 @@ class Workload:
         self.hbm_cfg_lane = {"mul": m.Launch(threads=256, unroll=2), "conv": m.Launch(threads=256, unroll=4)}
         if os.environ.get("MONT_HBM_DEFAULTS") == "1":
             self.hbm_cfg_lane = {}
+        ov = m.OVERLAP_PREV
+        self.hbm_cfg_lane_pdl = {k: m.Launch(threads=v.threads, unroll=v.unroll, flags=ov)
+                                 for k, v in self.hbm_cfg_lane.items()}
+        self.hbm_cfg_lane_pdl.setdefault("tw", m.Launch(flags=ov))
+        self.run_flags = 0   # flags of the mont_run launches (set per launch by step_concurrent)
         self.hbm_cfg = {}    # the serial step: library defaults (each kernel's best standalone shape)
         self.lane_events = None
         L = self.launches
@@ -353,7 +361,8 @@ class Workload:
                                                     self.tw_x.view(-1), self.tw))
                 self._pair_launch = ("mont_run[to_mont -> from_mont fused" + (", twiddle" if with_tw else "") + "]",
                                      lambda: m.run(self.pair_jobs, cfg=m.Launch(threads=RUN_SHAPE[0],
-                                                                                unroll=RUN_SHAPE[1])),
+                                                                                unroll=RUN_SHAPE[1],
+                                                                                flags=self.run_flags)),
                                      m.run_bytes(self.pair_jobs),
                                      2 * N_C2 + (TW_BATCH * TW_LEN if with_tw else 0), "hbm")
                 self._pair_mode = HBM_MODE
@@ -388,7 +397,8 @@ class Workload:
             self.run_jobs = jobs
             self.run_bytes = m.run_bytes(jobs)
             self._run_launch = ("mont_run[hbm lane: " + ", ".join(x[0] for x in hbm) + "]",
-                                lambda: m.run(self.run_jobs, cfg=m.Launch(threads=RUN_SHAPE[0], unroll=RUN_SHAPE[1])),
+                                lambda: m.run(self.run_jobs, cfg=m.Launch(threads=RUN_SHAPE[0], unroll=RUN_SHAPE[1],
+                                                                          flags=self.run_flags)),
                                 self.run_bytes, sum(x[3] for x in hbm), "hbm")
         return [self._run_launch] + [x for x in self.launches if x[4] != "hbm"]
 
@@ -423,10 +433,12 @@ class Workload:
             g = "conv" if name in ("to_mont", "from_mont") else name
             if _rest[-1] == "hbm" and g not in groups:
                 groups.append(g)
+        m_ov = self.m.OVERLAP_PREV
         ev = torch.cuda.Event()
         ev.record(cur)
         for st in list(self._lanes.values()) + self._hbm_extra:
             st.wait_event(ev)
+        started = set()   # streams that already carry an HBM launch of this step
         for lane in LANE_ORDER:
             for i, (name, fn, _, _, bound) in enumerate(launches):
                 if bound != lane:
@@ -434,6 +446,12 @@ class Workload:
                 if lane == "hbm":
                     g = "conv" if name in ("to_mont", "from_mont") else name
                     st = hbm_streams[groups.index(g) % nh]
+                    # PDL: a launch whose predecessor on its stream is another (independent) HBM launch
+                    # of this step may overlap that one's tail; never with external events in between
+                    pdl = PDL and both and st in started and self.lane_events is None
+                    self.hbm_cfg = self.hbm_cfg_lane_pdl if pdl else self.hbm_cfg_lane if both else {}
+                    self.run_flags = m_ov if pdl else 0
+                    started.add(st)
                 else:
                     st = self._lanes[lane]
                 with torch.cuda.stream(st):
@@ -446,6 +464,7 @@ class Workload:
             cur.wait_stream(st)
         self.pow_cfg = None
         self.hbm_cfg = {}
+        self.run_flags = 0
 
     def h2d_bytes(self):
         return sum(t.numel() * 4 for t in self.inputs)
@@ -1350,7 +1369,9 @@ def main():
                      ("two lanes: the HBM-bound operations as ONE mont_run launch (one flat grid over all their "
                       "tiles, to_mont -> from_mont fused)" if HBM_MODE == "run" else
                       "two lanes: the HBM-bound launches in order on one stream (mul_vec+checksum 256 threads x 2 "
-                      "uint4 x 3, to_mont -> from_mont as one fused mont_run launch, twiddle default)"
+                      "uint4 x 3, to_mont -> from_mont as one fused mont_run launch, twiddle default" +
+                      (", each after the first launched with MONT_LAUNCH_OVERLAP_PREV: programmatic dependent "
+                       "launch, its CTAs start in the previous one's tail)" if PDL else ")")
                       if HBM_MODE == "pair" else
                       f"two lanes: the HBM-bound launches on {HBM_STREAMS} stream(s) (mul_vec+checksum 256 threads x 2 "
                       "uint4, to/from_mont 256 x 4, twiddle default)") +

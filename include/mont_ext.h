@@ -99,7 +99,17 @@ typedef struct mont_launch {
     int unroll;
     int variant;
     int chunk;
+    int flags;
 } mont_launch_t;
+
+/* mont_launch_t.flags.  MONT_LAUNCH_OVERLAP_PREV (mont_mul_vec_ex / _checksum_ex default flat grid,
+ * mont_mul_twiddle_ex variants 0 / 1 / 4, mont_run_ex; ignored elsewhere): the launch may start
+ * while the previous kernel on the stream is still running (programmatic dependent launch: its
+ * CTAs fill the SMs that kernel's tail leaves idle).  The CALLER guarantees that this operation
+ * neither reads what the previous kernel writes nor writes what it reads or writes.  The
+ * operation still completes only after the previous kernel has completed, so everything launched
+ * after it keeps plain stream order.  Inside a CUDA graph capture it becomes a programmatic edge. */
+#define MONT_LAUNCH_OVERLAP_PREV 1
 
 mont_status_t mont_mul_vec_ex(const mont_ctx_t *ctx, uint32_t *c, const uint32_t *a, const uint32_t *b,
                               size_t n, const mont_launch_t *cfg, cudaStream_t stream);

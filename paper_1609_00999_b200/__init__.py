@@ -45,7 +45,10 @@ class Ctx(C.Structure):
 class Launch(C.Structure):
     """mont_launch_t (include/mont_ext.h); zero fields = library default."""
     _fields_ = [("threads", C.c_int), ("ctas_per_sm", C.c_int), ("unroll", C.c_int),
-                ("variant", C.c_int), ("chunk", C.c_int)]
+                ("variant", C.c_int), ("chunk", C.c_int), ("flags", C.c_int)]
+
+
+OVERLAP_PREV = 1  # mont_launch_t.flags: MONT_LAUNCH_OVERLAP_PREV (include/mont_ext.h)
 
 
 _lib = None

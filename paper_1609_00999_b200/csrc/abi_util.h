@@ -39,7 +39,7 @@ inline uint32_t head_elems(uintptr_t p, size_t n) {
 }
 
 struct Launch {
-    int threads, ctas_per_sm, unroll, variant, chunk;
+    int threads, ctas_per_sm, unroll, variant, chunk, flags;
 };
 
 inline Launch resolve(const mont_launch_t *cfg, Launch def) {
@@ -50,6 +50,7 @@ inline Launch resolve(const mont_launch_t *cfg, Launch def) {
     if (cfg->unroll > 0) l.unroll = cfg->unroll;
     if (cfg->variant > 0) l.variant = cfg->variant;
     if (cfg->chunk > 0) l.chunk = cfg->chunk;
+    l.flags = cfg->flags;
     return l;
 }
 
@@ -57,6 +58,29 @@ inline bool launch_ok(const Launch &l) {
     return l.threads >= 32 && l.threads <= 1024 && (l.threads % 32) == 0 && l.ctas_per_sm >= 1 && l.chunk >= 0 &&
            (l.chunk % 4) == 0 &&
            l.ctas_per_sm <= 32 && (l.unroll == 1 || l.unroll == 2 || l.unroll == 4 || l.unroll == 8);
+}
+
+// <<<>>> or, with MONT_LAUNCH_OVERLAP_PREV, cudaLaunchKernelEx with programmatic stream
+// serialisation: the launch may begin while the previous kernel on the stream is still running
+// (the kernel brackets itself with pdl_trigger / pdl_wait, mont_core.cuh)
+template <typename... KArgs, typename... Args>
+inline mont_status_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, int flags,
+                              Args... args) {
+    if (!(flags & MONT_LAUNCH_OVERLAP_PREV)) {
+        kern<<<grid, block, smem, s>>>(args...);
+        return launch_status();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...) == cudaSuccess ? launch_status() : MONT_ECUDA;
 }
 
 }  // namespace mont

@@ -103,6 +103,7 @@ __device__ __forceinline__ unsigned long long sum4(const uint4 &v) {
 template <int U, class Op, bool SUM>
 __global__ void __launch_bounds__(512) k_map2(Op op, uint32_t *c, const uint32_t *a, const uint32_t *b,
                                                 uint32_t head, size_t n4, uint32_t tail, unsigned long long *acc) {
+    pdl_trigger();
     unsigned long long s = 0;
     if (blockIdx.x == 0 && threadIdx.x < head + tail) {
         size_t i = threadIdx.x < head ? threadIdx.x : head + 4 * n4 + (threadIdx.x - head);
@@ -138,6 +139,7 @@ __global__ void __launch_bounds__(512) k_map2(Op op, uint32_t *c, const uint32_t
         }
     }
     if (SUM) block_sum_to(acc, s);
+    pdl_wait();
 }
 
 // Bulk-copy (TMA) variant: each CTA stages one tile of a and one of b into
@@ -403,11 +405,12 @@ static mont_status_t launch_map2(const Op &op, uint32_t *c, const uint32_t *a, c
         if (grid > need) grid = need;
         if (grid == 0) grid = 1;
         if (grid > 0x7fffffff) return MONT_EUNSUPPORTED;
+        const dim3 g((unsigned)grid), bl((unsigned)L.threads);
         switch (L.unroll) {
-            case 1: k_map2<1, Op, SUM><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, head, n4, tail, acc); break;
-            case 2: k_map2<2, Op, SUM><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, head, n4, tail, acc); break;
-            case 4: k_map2<4, Op, SUM><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, head, n4, tail, acc); break;
-            default: k_map2<8, Op, SUM><<<(unsigned)grid, L.threads, 0, s>>>(op, c, a, b, head, n4, tail, acc); break;
+            case 1: return launch_k(k_map2<1, Op, SUM>, g, bl, 0, s, L.flags, op, c, a, b, head, n4, tail, acc);
+            case 2: return launch_k(k_map2<2, Op, SUM>, g, bl, 0, s, L.flags, op, c, a, b, head, n4, tail, acc);
+            case 4: return launch_k(k_map2<4, Op, SUM>, g, bl, 0, s, L.flags, op, c, a, b, head, n4, tail, acc);
+            default: return launch_k(k_map2<8, Op, SUM>, g, bl, 0, s, L.flags, op, c, a, b, head, n4, tail, acc);
         }
     } else {
         const size_t tile = (size_t)L.unroll * L.threads;

@@ -47,6 +47,7 @@ __device__ __forceinline__ unsigned long long run_warp_sum(unsigned long long v)
 
 template <int kRunThreads, int kRunU>
 __global__ void __launch_bounds__(kRunThreads) k_run(const __grid_constant__ RunParams P) {
+    pdl_trigger();
     constexpr size_t kRunTile = (size_t)kRunU * kRunThreads;  // uint4 per tile
     const size_t t = blockIdx.x;
     int j = 0;
@@ -136,6 +137,7 @@ __global__ void __launch_bounds__(kRunThreads) k_run(const __grid_constant__ Run
             }
         }
     }
+    pdl_wait();
 }
 
 struct Range {
@@ -249,17 +251,16 @@ extern "C" mont_status_t mont_run_ex(const mont_run_job_t *jobs, int njobs, cons
     if (st != MONT_OK) return st;
     if (tiles == 0) return MONT_OK;
     if (tiles > 0x7fffffffu) return MONT_EUNSUPPORTED;
-    const unsigned g = (unsigned)tiles;
+    const dim3 g((unsigned)tiles), b((unsigned)threads);
+    const int flags = cfg ? cfg->flags : 0;
     if (threads == 512) {
-        if (unroll == 1) k_run<512, 1><<<g, 512, 0, stream>>>(P);
-        else if (unroll == 2) k_run<512, 2><<<g, 512, 0, stream>>>(P);
-        else k_run<512, 4><<<g, 512, 0, stream>>>(P);
-    } else {
-        if (unroll == 1) k_run<256, 1><<<g, 256, 0, stream>>>(P);
-        else if (unroll == 2) k_run<256, 2><<<g, 256, 0, stream>>>(P);
-        else k_run<256, 4><<<g, 256, 0, stream>>>(P);
+        if (unroll == 1) return launch_k(k_run<512, 1>, g, b, 0, stream, flags, P);
+        if (unroll == 2) return launch_k(k_run<512, 2>, g, b, 0, stream, flags, P);
+        return launch_k(k_run<512, 4>, g, b, 0, stream, flags, P);
     }
-    return launch_status();
+    if (unroll == 1) return launch_k(k_run<256, 1>, g, b, 0, stream, flags, P);
+    if (unroll == 2) return launch_k(k_run<256, 2>, g, b, 0, stream, flags, P);
+    return launch_k(k_run<256, 4>, g, b, 0, stream, flags, P);
 }
 
 extern "C" mont_status_t mont_run(const mont_run_job_t *jobs, int njobs, cudaStream_t stream) {

@@ -36,6 +36,7 @@ __global__ void __launch_bounds__(512) k_twiddle(Ctx c, uint32_t *out, const uin
                                                   size_t batch, size_t len, uint32_t chunk, size_t rows_per_cta) {
     extern __shared__ __align__(128) uint4 s_tw[];
     __shared__ __align__(8) uint64_t bar;
+    pdl_trigger();
     const size_t c0 = (size_t)blockIdx.x * chunk;
     const size_t r0 = (size_t)blockIdx.y * rows_per_cta;
     if (r0 >= batch || c0 >= len) return;  // uniform per CTA
@@ -97,6 +98,7 @@ __global__ void __launch_bounds__(512) k_twiddle(Ctx c, uint32_t *out, const uin
         }
     }
     if (!waited) mbar_wait(&bar, 0);  // never leave with a copy in flight
+    pdl_wait();
 }
 
 // Flat variant (variant 2) for power-of-two len: the batch is one flat stream
@@ -229,8 +231,8 @@ static mont_status_t launch_tw(const Ctx &c, uint32_t *out, const uint32_t *x, c
             return MONT_ECUDA;
     }
     dim3 grid((unsigned)nchunks, (unsigned)gy);
-    k_twiddle<U, TMA><<<grid, L.threads, smem, s>>>(c, out, x, tw, batch, len, (uint32_t)chunk, rows_per_cta);
-    return launch_status();
+    return launch_k(k_twiddle<U, TMA>, grid, dim3((unsigned)L.threads), smem, s, L.flags, c, out, x, tw, batch, len,
+                    (uint32_t)chunk, rows_per_cta);
 }
 
 }  // namespace mont

@@ -36,6 +36,14 @@ struct Ctx {  // device view of mont_ctx_t (by value in kernel params); pinv = -
 
 __device__ __forceinline__ uint32_t umin(uint32_t x, uint32_t y) { return x < y ? x : y; }
 
+// Programmatic dependent launch (mont_launch_t.flags & MONT_LAUNCH_OVERLAP_PREV): a kernel lets the
+// next overlap-flagged launch on its stream start as soon as all of its CTAs are running
+// (pdl_trigger, at the top), and waits at its very end for the launch before it to complete
+// (pdl_wait), so that its own completion still implies its predecessor's -- stream order holds for
+// everything launched after it.  Both are no-ops for a launch without the attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // 32 x 32 -> 64 products (IMAD.WIDE): both halves of the paper's "2l-bit" product
 // in one register pair.  (A 64-bit addend is not fused: ptxas splits mad.wide with a
 // register-pair addend into IMAD.WIDE + IADD3 + IADD3.X, so the carry form of Alg. 2 costs ALU

@@ -58,8 +58,9 @@ def main():
     }
     only = os.environ.get("SWEEP_HBM")
     rebuilds = int(os.environ.get("SWEEP_REBUILDS", "2"))
-    for (pv, pc, sm, pt), (hname, hcfg), prio, hs, mode, shape in itertools.product(pows, hbms.items(), prios, hstreams,
-                                                                                   modes, shapes):
+    pdls = [v == "1" for v in os.environ.get("SWEEP_PDL", "0").split(",")]
+    for (pv, pc, sm, pt), (hname, hcfg), prio, hs, mode, shape, pdl in itertools.product(
+            pows, hbms.items(), prios, hstreams, modes, shapes, pdls):
         if only and hname not in only.split(","):
             continue
         if mode == "run" and (hs != 1 or hname != "default"):
@@ -72,6 +73,10 @@ def main():
                 delattr(wl, attr)
         wl.pow_cfg_lane = L(ctas_per_sm=pc, variant=pv, chunk=sm, threads=pt)
         wl.hbm_cfg_lane = {k: v for k, v in hcfg.items() if v is not None}
+        bench.PDL = pdl
+        wl.hbm_cfg_lane_pdl = {k: L(threads=v.threads, ctas_per_sm=v.ctas_per_sm, unroll=v.unroll, variant=v.variant,
+                                    chunk=v.chunk, flags=1) for k, v in wl.hbm_cfg_lane.items()}
+        wl.hbm_cfg_lane_pdl.setdefault("tw", L(flags=1))
         # lane streams: torch priority -1 = high, 0 = low (graph kernel nodes inherit it)
         wl._lanes = {"hbm": torch.cuda.Stream(priority=-1 if prio == "hbm" else 0),
                      "imad": torch.cuda.Stream(priority=-1 if prio == "imad" else 0)}
@@ -88,6 +93,7 @@ def main():
             ts = [bench.time_steps_graph(wl, g, 20) / 20 for _ in range(3)]
             ok = all(bench.verify(wl, run=False).values())
             print(json.dumps({"pow": [pv, pc, sm, pt], "hbm": hname, "prio": prio, "hbm_streams": hs, "mode": mode,
+                              "pdl": pdl,
                               "run_shape": list(shape) if mode != "streams" else None,
                               "rebuild": rb,
                               "ms_per_step": round(statistics.median(ts), 4), "ms_best": round(min(ts), 4),
