@@ -1339,6 +1339,11 @@ def main():
                                 "frac": round(hb / (w * 1e-3) / 1e9 / hbm_peak, 4),
                                 "what": "all HBM launches of the step as timed (first start to last end, external "
                                         "graph events), algorithmic bytes / wall time"}
+            # the same bytes over the timed step itself (no events between the launches, so with the
+            # programmatic-dependent-launch overlap): the HBM lane is the critical path, so this is a
+            # lower bound on the lane's bandwidth as timed
+            roof["hbm_lane"]["achieved_gbs_timed_step"] = round(hb / (ms_per_step * 1e-3) / 1e9, 1)
+            roof["hbm_lane"]["frac_timed_step"] = round(hb / (ms_per_step * 1e-3) / 1e9 / hbm_peak, 4)
     else:
         roof["duration"] = "median over the K timed steps of a serial pass with CUDA events around each launch"
     line = {
