@@ -207,3 +207,21 @@ def test_run_plan_bytes_and_validation():
     bad = m.Ctx()
     assert bytes_of([_run_job(1, bad, D, A, n=n)])[0] == 1
     assert bytes_of([])[0] == 0 and bytes_of([])[1] == 0
+
+
+def test_binding_structs_match_headers():
+    """The ctypes mirrors of the C structs list the same fields in the same order as the headers
+    (mont_launch_t in include/mont_ext.h, mont_run_job_t in include/mont_run.h), and the flag value
+    matches MONT_LAUNCH_OVERLAP_PREV."""
+    root = Path(__file__).resolve().parents[1] / "include"
+
+    def fields(header, name):
+        txt = (root / header).read_text()
+        body = re.search(r"typedef struct " + name + r" \{(.*?)\}", txt, re.S).group(1)
+        return [re.findall(r"(\w+)\s*;", line)[0] for line in body.splitlines() if ";" in line and "(" not in line]
+
+    assert fields("mont_ext.h", "mont_launch") == [f for f, _ in m.Launch._fields_]
+    assert C.sizeof(m.Launch) == 4 * len(m.Launch._fields_)
+    assert fields("mont_run.h", "mont_run_job") == [f for f, *_ in m.RunJob._fields_]
+    flag = re.search(r"#define MONT_LAUNCH_OVERLAP_PREV (\d+)", (root / "mont_ext.h").read_text()).group(1)
+    assert int(flag) == m.OVERLAP_PREV
