@@ -62,6 +62,7 @@ def test_overlap_flag_same_results(m, graph):
     ref = make_bufs(m, ctx, n, rows, L)
     got = tuple(t.clone() for t in ref)
     s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())   # inputs were generated on the current stream
     with torch.cuda.stream(s):
         sequence(m, ctx, ref, False, s)
         if graph:
@@ -94,9 +95,10 @@ def test_overlap_flag_keeps_stream_order(m):
     ref = m.pow_vec(ctx, base, e)
     ref_m = m.to_mont(ctx, ref)
     s = torch.cuda.Stream()
-    for _ in range(5):
-        out.zero_()
+    s.wait_stream(torch.cuda.current_stream())   # inputs were generated on the current stream
+    for _ in range(20):
         with torch.cuda.stream(s):
+            out.zero_()                           # on s, ordered before the pow
             m.pow_vec(ctx, base, e, out=out, stream=s)
             m.mul_vec(ctx, a, b, out=c, stream=s, cfg=m.Launch(flags=m.OVERLAP_PREV))
             got = m.to_mont(ctx, out, stream=s)
