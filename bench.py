@@ -1389,7 +1389,9 @@ def main():
         "kernels_note": ("'kernels': each launch alone (serial pass, library-default launch shapes); "
                          "'kernels_in_step': the same individual launches inside the two-lane step (HBM ones one "
                          "after another next to the pow lane); 'kernels_timed_step': the launches of the timed "
-                         "step itself (the HBM lane as one mont_run launch)"),
+                         "step itself (its HBM lane as timed: the to_mont -> from_mont pair as one fused mont_run "
+                         "launch in the default 'pair' mode), with external events between them, so without the "
+                         "programmatic-dependent-launch overlap of the timed graph"),
         "clocks": {k: clocks.get(k) for k in ("sm_mhz", "sm_max_mhz", "reasons", "samples", "samples_under_load")},
         "parity": {"checks": checks, "box_checksums": box_checksums},
     }
