@@ -226,6 +226,8 @@ class Workload:
         self.hbm_cfg_lane_pdl = {k: m.Launch(threads=v.threads, unroll=v.unroll, flags=ov)
                                  for k, v in self.hbm_cfg_lane.items()}
         self.hbm_cfg_lane_pdl.setdefault("tw", m.Launch(flags=ov))
+        # one HBM lane alone (c2): the library-default shapes, flagged
+        self.hbm_cfg_pdl_alone = {k: m.Launch(flags=ov) for k in ("mul", "conv", "tw")}
         self.run_flags = 0   # flags of the mont_run launches (set per launch by step_concurrent)
         self.hbm_cfg = {}    # the serial step: library defaults (each kernel's best standalone shape)
         self.lane_events = None
@@ -448,8 +450,9 @@ class Workload:
                     st = hbm_streams[groups.index(g) % nh]
                     # PDL: a launch whose predecessor on its stream is another (independent) HBM launch
                     # of this step may overlap that one's tail; never with external events in between
-                    pdl = PDL and both and st in started and self.lane_events is None
-                    self.hbm_cfg = self.hbm_cfg_lane_pdl if pdl else self.hbm_cfg_lane if both else {}
+                    pdl = PDL and st in started and self.lane_events is None
+                    self.hbm_cfg = ((self.hbm_cfg_lane_pdl if both else self.hbm_cfg_pdl_alone) if pdl
+                                    else self.hbm_cfg_lane if both else {})
                     self.run_flags = m_ov if pdl else 0
                     started.add(st)
                 else:
@@ -1369,6 +1372,8 @@ def main():
         "schedule": ("each step alone between CUDA events after an L2 flush" if wl.kind == "c1" else
                      "serial, one stream" if args.serial else
                      ("one lane: " + ", ".join(x[0] for x in wl.launches) + " in order on one stream" +
+                      (", each after the first chained by programmatic dependent launch (MONT_LAUNCH_OVERLAP_PREV)"
+                       if PDL and len(wl.launches) > 1 else "") +
                       (", replayed as one CUDA graph" if args.graph else ""))
                      if len({x[4] for x in wl.launches}) < 2 else
                      ("two lanes: the HBM-bound operations as ONE mont_run launch (one flat grid over all their "
