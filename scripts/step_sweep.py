@@ -53,6 +53,11 @@ def main():
         "u2c4": {"mul": L(threads=256, unroll=2), "conv": L(threads=256, unroll=4)},
         "u2c4tma": {"mul": L(threads=256, unroll=2), "conv": L(threads=256, unroll=4), "tw": L(variant=4)},
         "u2c4tma4k": {"mul": L(threads=256, unroll=2), "conv": L(threads=256, unroll=4), "tw": L(variant=4, chunk=4096)},
+        "m256u1tma": {"mul": L(threads=256, unroll=1), "tw": L(variant=4)},
+        "m256u4tma": {"mul": L(threads=256, unroll=4), "tw": L(variant=4)},
+        "m512u2tma": {"mul": L(threads=512, unroll=2), "tw": L(variant=4)},
+        "m128u4tma": {"mul": L(threads=128, unroll=4), "tw": L(variant=4)},
+        "m512u1tma": {"mul": L(threads=512, unroll=1), "tw": L(variant=4)},
         "fp64mul": {"mul": L(threads=256, unroll=2, variant=4), "conv": L(threads=256, unroll=4)},
         "fp64mul512": {"mul": L(threads=512, unroll=2, variant=4), "conv": L(threads=256, unroll=4)},
     }
