@@ -104,3 +104,33 @@ def test_overlap_flag_keeps_stream_order(m):
             got = m.to_mont(ctx, out, stream=s)
         s.synchronize()
         assert torch.equal(got, ref_m)
+
+
+def test_overlap_flag_without_a_predecessor(m):
+    """A flagged launch that is the first work on a fresh stream (and the first node of a captured
+    graph) behaves as a plain launch."""
+    ctx = m.ctx_init(P0)
+    n = (1 << 20) + 4
+    a, b = gen(m, n, 1, P0), gen(m, n, 2, P0)
+    ref = m.mul_vec(ctx, a, b)
+    torch.cuda.synchronize()
+    ov = m.Launch(flags=m.OVERLAP_PREV)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        c = torch.empty_like(a)
+        m.mul_vec(ctx, a, b, out=c, stream=s, cfg=ov)
+    s.synchronize()
+    assert torch.equal(c, ref)
+    g = torch.cuda.CUDAGraph()
+    c2 = torch.empty_like(a)
+    s2 = torch.cuda.Stream()
+    with torch.cuda.stream(s2):
+        with torch.cuda.graph(g, stream=s2):
+            m.mul_vec(ctx, a, b, out=c2, stream=s2, cfg=ov)
+            m.mul_twiddle(ctx, a[:4096 * 256].view(256, 4096), b[:4096], out=c[:4096 * 256].view(256, 4096),
+                          stream=s2, cfg=ov)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(c2, ref)
+    t = m.mul_twiddle(ctx, a[:4096 * 256].view(256, 4096), b[:4096])
+    assert torch.equal(c[:4096 * 256].view(256, 4096), t)
