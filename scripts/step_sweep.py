@@ -29,7 +29,7 @@ def main():
     # (variant, ctas_per_sm, reserved smem bytes): ctas 0 = flat grid
     pows = [tuple(int(x) for x in (v.split(":") + ["256"])[:4]) for v in
             os.environ.get("SWEEP_POWS", "10:1:0,11:1:0,10:2:0").split(",")]   # variant:ctas:smem[:threads]
-    prios = ["imad"]
+    prios = [None if v == "none" else v for v in os.environ.get("SWEEP_PRIOS", "imad").split(",")]
     hstreams = [int(v) for v in os.environ.get("SWEEP_HBM_STREAMS", "1").split(",")]
     modes = os.environ.get("SWEEP_HBM_MODES", "streams").split(",")
     shapes = [tuple(int(x) for x in v.split("x")) for v in os.environ.get("SWEEP_RUN_SHAPES", "256x2").split(",")]
